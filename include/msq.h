@@ -1,0 +1,152 @@
+/*
+ * msq.h -- C ABI of the B200 maximal-square library (libmsq.so).
+ *
+ * The hot path is the reference's frequency algorithm,
+ * /root/reference/pkg/src/squarelab/squares.py:68-114 (_freq_core), reached
+ * through freq_square(m, audit=None) -> SquareResult (squares.py:117-126).
+ * The reference has no FFI of its own (it is pure Python); these entry points
+ * are what its Python solver signature binds to through ctypes (see
+ * INTEGRATION.md).  Plain pointers and sizes only; no torch types.
+ *
+ * Conventions
+ *   - Device pointers are caller-owned; the library never frees them.
+ *   - u8 cells must be 0 or 1 (grid.py:61-62); any other byte -> MSQ_EVALUE.
+ *   - Bit-packed rows: bit b of uint32 word w is column 32*w + b (LSB = lowest
+ *     column); padding bits past `cols` are ignored.
+ *   - Results: side, area = side^2, cells_visited = rows*cols (squares.py:114),
+ *     top/left = the top-left corner of the first maximal square in row-major
+ *     order of its bottom-right cell (the cell of Algorithm 1's final threshold
+ *     raise, squares.py:93-97); top = left = -1 when side == 0.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Every call is reentrant per stream as long as concurrent calls use
+ *     distinct workspaces (the msq_solve_* convenience calls share one
+ *     internal per-device workspace and serialise on it).
+ */
+#ifndef MSQ_H
+#define MSQ_H
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define MSQ_OK 0
+#define MSQ_EINVAL 1   /* bad shape / stride / alignment / unsupported width */
+#define MSQ_EVALUE 2   /* a u8 cell outside {0,1} -> Python ValueError       */
+#define MSQ_ECUDA 3    /* CUDA runtime error -> Python RuntimeError          */
+#define MSQ_ENOMEM 4   /* workspace allocation failed                        */
+
+/* input formats */
+#define MSQ_FMT_U8 0
+#define MSQ_FMT_BITS 1
+
+typedef struct {
+    int64_t side;
+    int64_t area;
+    int64_t cells_visited;
+    int64_t top;
+    int64_t left;
+} msq_result;
+
+/* Device-side result block written by a launch (one per matrix). */
+typedef struct {
+    uint64_t key_pass1;  /* best key from band passes                     */
+    uint64_t key_fix;    /* best key from band-boundary fix-ups            */
+    uint32_t status;     /* bit 0: invalid u8 cell                         */
+    int32_t best_side;   /* running best side shared between bands         */
+    uint64_t reserved;
+} msq_devresult;
+
+/* Launch plan: everything the kernels need that depends only on the shape. */
+typedef struct {
+    int32_t fmt;          /* MSQ_FMT_U8 / MSQ_FMT_BITS                      */
+    int32_t batch;        /* matrices (stacked, contiguous) >= 1            */
+    int64_t rows, cols;   /* per matrix                                     */
+    int64_t ld;           /* row stride in elements (bytes / uint32 words)  */
+    int32_t words;        /* ceil(cols / 32)                                */
+    int32_t wpt;          /* words per thread                               */
+    int32_t threads;      /* CTA size                                       */
+    int32_t tile_rows;    /* rows per test tile                             */
+    int32_t nbands;       /* row bands per matrix (1 for batch)             */
+    int32_t nstage;       /* TMA ring depth in tiles (0 = direct loads)     */
+    int32_t row_stage_bytes;
+    int32_t smem_pass1, smem_fixup;
+    int32_t deterministic;/* 1: no cross-band threshold sharing             */
+    int64_t row_base;     /* global row index of row 0 (row-band sharding)  */
+    int64_t ws_bytes;     /* required workspace bytes                       */
+} msq_plan;
+
+/* Build a plan.  nbands <= 0 picks a default (one band per SM, bands of
+ * >= 64 rows, <= 65535 rows each).  Returns MSQ_EINVAL for unsupported
+ * shapes (cols > 65536, rows >= 2^21, misaligned TMA-incompatible strides
+ * are handled by the direct-load path, not rejected). */
+int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld,
+                  int32_t nbands, int32_t deterministic, msq_plan* plan);
+
+/* Enqueue a solve on `stream`.  d_ws: >= plan->ws_bytes of device memory;
+ * d_result: plan->batch msq_devresult blocks (device memory).  Nothing is
+ * synchronised; decode with msq_decode after the stream completes. */
+int msq_launch(const msq_plan* plan, const void* d_src, void* d_ws, msq_devresult* d_result,
+               void* stream);
+
+/* Decode a (host copy of a) device result block. Returns MSQ_EVALUE if the
+ * status flags an invalid cell. */
+int msq_decode(const msq_devresult* r, int64_t rows, int64_t cols, msq_result* out);
+
+/* Synchronous convenience calls (internal per-device workspace). */
+int msq_solve_u8(const uint8_t* d_cells, int64_t rows, int64_t cols, int64_t ld,
+                 msq_result* out, void* stream);
+int msq_solve_bits(const uint32_t* d_words, int64_t rows, int64_t cols, int64_t ld_words,
+                   msq_result* out, void* stream);
+int msq_solve_batch_u8(const uint8_t* d_cells, int64_t batch, int64_t rows, int64_t cols,
+                       msq_result* out, void* stream);
+
+/* Host-buffer entry points: copy H2D on `stream`, solve, copy the result
+ * back (the path a CPU caller of freq_square takes). */
+int msq_solve_u8_host(const uint8_t* h_cells, int64_t rows, int64_t cols, int64_t ld,
+                      msq_result* out, void* stream);
+int msq_solve_bits_host(const uint32_t* h_words, int64_t rows, int64_t cols, int64_t ld_words,
+                        msq_result* out, void* stream);
+
+/* ---- row-band sharding across GPUs (one process per GPU) ----------------
+ * A rank owns rows [row_base, row_base + plan->rows) of the global matrix.
+ *   1. msq_rank_pass1   : band passes over the local rows (fills d_ws)
+ *   2. msq_rank_summary : per column bottom run of the local slice
+ *                         (uint32; == plan->rows means all ones)
+ *   3. (caller) all-gather the summaries of all ranks
+ *   4. msq_compose_carry: carry-in heights for this rank from the gathered
+ *                         summaries of the ranks above it
+ *   5. msq_rank_fixup   : data-free band-boundary fix-ups, including the top
+ *                         boundary of the slice when d_base_carry != NULL
+ *   6. (caller) all-reduce(max) of max(key_pass1, key_fix) over ranks      */
+int msq_rank_pass1(const msq_plan* plan, const void* d_src, void* d_ws,
+                   msq_devresult* d_result, void* stream);
+int msq_rank_summary(const msq_plan* plan, const void* d_ws, uint32_t* d_summary, void* stream);
+int msq_compose_carry(const uint32_t* d_summaries, const int64_t* h_rank_rows, int32_t nranks,
+                      int32_t rank, int64_t cols, uint32_t* d_base_carry, void* stream);
+int msq_rank_fixup(const msq_plan* plan, void* d_ws, const uint32_t* d_base_carry,
+                   msq_devresult* d_result, void* stream);
+
+/* Intermediate outputs (tests): per band leading-ones depth e, bottom run b
+ * (uint16 [nbands][words*32]) and all-ones masks (uint32 [nbands][words]),
+ * pass-1 band keys (uint64 [nbands]); device pointers into d_ws. */
+int msq_ws_views(const msq_plan* plan, void* d_ws, uint16_t** e, uint16_t** b, uint32_t** allones,
+                 uint64_t** band_keys);
+
+/* Seeded counter-hash matrix generator (bench / test inputs, not the hot
+ * path): cell (i,j) = mix64(seed + (i*cols+j+1)*0x9E3779B97F4A7C15)>>11 < thr53. */
+int msq_gen_hash(int32_t fmt, uint64_t seed, uint64_t thr53, int64_t row0, int64_t nrows,
+                 int64_t cols, int64_t ld, void* d_out, void* stream);
+
+/* Number of kernel launches the last msq_launch enqueued (instrumentation). */
+int32_t msq_last_launch_count(void);
+
+const char* msq_strerror(int code);
+const char* msq_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

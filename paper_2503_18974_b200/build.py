@@ -1,0 +1,59 @@
+"""In-tree build of libmsq.so (sm_100a) with plain nvcc.
+
+The library is a C-ABI shared object (include/msq.h); it links the CUDA runtime
+dynamically so it shares torch's runtime instance when both are loaded.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIBDIR = os.path.join(PKG, "_lib")
+LIB = os.path.join(LIBDIR, "libmsq.so")
+SOURCES = [os.path.join(CSRC, "msq.cu")]
+HEADERS = [os.path.join(CSRC, "msq_engine.cuh"), os.path.join(ROOT, "include", "msq.h")]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(s) > t for s in SOURCES + HEADERS + [__file__])
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not stale():
+        return LIB
+    os.makedirs(LIBDIR, exist_ok=True)
+    cmd = [nvcc(), *ARCH, "-O3", "-std=c++17", "-lineinfo", "--use_fast_math",
+           "-Xptxas", "-v" if verbose else "-O3",
+           "-shared", "-Xcompiler", "-fPIC", "-cudart", "shared",
+           "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+           "-Xlinker", "-rpath,/usr/local/cuda/lib64",
+           "-o", LIB + ".tmp", *SOURCES]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed building libmsq.so")
+    if verbose:
+        sys.stderr.write(res.stderr)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

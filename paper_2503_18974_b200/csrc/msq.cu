@@ -1,0 +1,470 @@
+// msq.cu -- C ABI (include/msq.h) over the sm_100a kernels in msq_engine.cuh.
+//
+// Replaces the reference's Python hot loop, squares.py:68-114 (_freq_core),
+// behind the same call shape freq_square(m, audit=None) -> SquareResult
+// (squares.py:117-126); the Python mirror lives in ../squares.py.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "msq.h"
+#include "msq_engine.cuh"
+
+namespace {
+
+constexpr int kSmemMax = 232448;  // 227 KB opt-in dynamic shared memory per CTA (sm_100)
+constexpr int kTileRows = 2;
+constexpr int kMaxWords = 2048;   // 65536 columns
+
+thread_local int32_t g_last_launches = 0;
+
+inline long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
+inline long long round_up(long long a, long long b) { return ceil_div(a, b) * b; }
+
+int num_sms() {
+    static int sms[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (dev < 64 && sms[dev] == 0) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+            v = 148;
+        sms[dev] = v;
+    }
+    return dev < 64 ? sms[dev] : 148;
+}
+
+struct WsLayout {
+    size_t band_keys, fix_keys, e, b, ao, total;
+};
+
+WsLayout ws_layout(const msq_plan* p) {
+    WsLayout L{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += round_up((long long)bytes, 256);
+        return o;
+    };
+    const size_t nb = (size_t)p->nbands;
+    const size_t cols_pad = (size_t)p->words * 32;
+    L.band_keys = take((size_t)p->batch * nb * 8);
+    L.fix_keys = take(nb * 8);
+    const bool summaries = p->batch == 1;
+    L.e = take(summaries ? nb * cols_pad * 2 : 0);
+    L.b = take(summaries ? nb * cols_pad * 2 : 0);
+    L.ao = take(summaries ? nb * (size_t)p->words * 4 : 0);
+    L.total = off;
+    return L;
+}
+
+// ------------------------------------------------------------- dispatch
+template <int WPT, bool U8, bool TMA>
+cudaError_t launch_pass1_t(const msq_plan* pl, const msq::Pass1Params& prm, cudaStream_t st) {
+    auto kern = msq::pass1_kernel<WPT, kTileRows, U8, TMA>;
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !attr_set[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+        if (e != cudaSuccess) return e;
+        attr_set[dev] = true;
+    }
+    dim3 grid((unsigned)pl->nbands, (unsigned)pl->batch);
+    kern<<<grid, pl->threads, pl->smem_pass1, st>>>(prm);
+    return cudaGetLastError();
+}
+
+template <int WPT>
+cudaError_t launch_fixup_t(const msq_plan* pl, const msq::FixParams& prm, int nblocks, cudaStream_t st) {
+    auto kern = msq::fixup_kernel<WPT, kTileRows>;
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !attr_set[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+        if (e != cudaSuccess) return e;
+        attr_set[dev] = true;
+    }
+    kern<<<nblocks, pl->threads, pl->smem_fixup, st>>>(prm);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pass1(const msq_plan* pl, const msq::Pass1Params& prm, cudaStream_t st) {
+    const bool u8 = pl->fmt == MSQ_FMT_U8;
+    const bool tma = pl->nstage > 0;
+#define MSQ_P1(W_, U_, T_) \
+    if (pl->wpt == W_ && u8 == U_ && tma == T_) return launch_pass1_t<W_, U_, T_>(pl, prm, st);
+    MSQ_P1(1, true, true) MSQ_P1(1, true, false) MSQ_P1(1, false, true) MSQ_P1(1, false, false)
+    MSQ_P1(2, true, true) MSQ_P1(2, true, false) MSQ_P1(2, false, true) MSQ_P1(2, false, false)
+    MSQ_P1(4, true, true) MSQ_P1(4, true, false) MSQ_P1(4, false, true) MSQ_P1(4, false, false)
+#undef MSQ_P1
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_fixup(const msq_plan* pl, const msq::FixParams& prm, int nblocks, cudaStream_t st) {
+    if (nblocks <= 0) return cudaSuccess;
+    switch (pl->wpt) {
+        case 1: return launch_fixup_t<1>(pl, prm, nblocks, st);
+        case 2: return launch_fixup_t<2>(pl, prm, nblocks, st);
+        case 4: return launch_fixup_t<4>(pl, prm, nblocks, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+msq::Pass1Params make_pass1(const msq_plan* pl, const void* src, void* ws, msq_devresult* res,
+                            bool summaries) {
+    WsLayout L = ws_layout(pl);
+    uint8_t* w = (uint8_t*)ws;
+    msq::Pass1Params p{};
+    p.src = (const uint8_t*)src;
+    const long long esz = pl->fmt == MSQ_FMT_U8 ? 1 : 4;
+    p.ld_bytes = pl->ld * esz;
+    p.batch_stride = pl->rows * pl->ld * esz;
+    p.rows = (int)pl->rows;
+    p.cols = (int)pl->cols;
+    p.W = pl->words;
+    p.nbands = pl->nbands;
+    p.cols_pad = pl->words * 32;
+    p.row_base = pl->row_base;
+    p.nstage = pl->nstage;
+    p.rs = pl->row_stage_bytes;
+    p.row_bytes = pl->row_stage_bytes;
+    p.share = (pl->deterministic || pl->nbands == 1) ? 0 : 1;
+    p.write_summaries = summaries ? 1 : 0;
+    p.e_out = summaries ? (uint16_t*)(w + L.e) : nullptr;
+    p.b_out = summaries ? (uint16_t*)(w + L.b) : nullptr;
+    p.ao_out = summaries ? (uint32_t*)(w + L.ao) : nullptr;
+    p.band_keys = (unsigned long long*)(w + L.band_keys);
+    p.results = (unsigned char*)res;
+    return p;
+}
+
+msq::FixParams make_fix(const msq_plan* pl, void* ws, const uint32_t* base, msq_devresult* res) {
+    WsLayout L = ws_layout(pl);
+    uint8_t* w = (uint8_t*)ws;
+    msq::FixParams f{};
+    f.rows = (int)pl->rows;
+    f.cols = (int)pl->cols;
+    f.W = pl->words;
+    f.nbands = pl->nbands;
+    f.cols_pad = pl->words * 32;
+    f.row_base = pl->row_base;
+    f.band_begin = base ? 0 : 1;
+    f.e_in = (const uint16_t*)(w + L.e);
+    f.b_in = (const uint16_t*)(w + L.b);
+    f.ao_in = (const uint32_t*)(w + L.ao);
+    f.base_carry = base;
+    f.share = pl->deterministic ? 0 : 1;
+    f.fix_keys = (unsigned long long*)(w + L.fix_keys);
+    f.results = (unsigned char*)res;
+    return f;
+}
+
+int cuda_status(cudaError_t e) { return e == cudaSuccess ? MSQ_OK : MSQ_ECUDA; }
+
+// --------------------------------------------------- internal workspace
+struct DevCache {
+    std::mutex mu;
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    void* in = nullptr;  // staging for host-buffer calls
+    size_t in_bytes = 0;
+    msq_devresult* res = nullptr;
+    size_t res_cap = 0;
+    msq_devresult* hres = nullptr;  // pinned
+    size_t hres_cap = 0;
+};
+DevCache g_cache[64];
+
+int grow(void** p, size_t* cap, size_t need) {
+    if (*cap >= need) return MSQ_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    if (cudaMalloc(p, need) != cudaSuccess) {
+        cudaGetLastError();
+        return MSQ_ENOMEM;
+    }
+    *cap = need;
+    return MSQ_OK;
+}
+
+int solve_sync(int32_t fmt, int64_t batch, const void* d_src, int64_t rows, int64_t cols, int64_t ld,
+               msq_result* out, void* stream) {
+    if (!out) return MSQ_EINVAL;
+    if (rows == 0 || cols == 0) {
+        if (rows < 0 || cols < 0 || (rows == 0 && cols != 0)) return MSQ_EINVAL;
+        for (int64_t k = 0; k < std::max<int64_t>(batch, 1); ++k) out[k] = msq_result{0, 0, 0, -1, -1};
+        return MSQ_OK;
+    }
+    msq_plan pl;
+    int rc = msq_plan_make(fmt, (int32_t)batch, rows, cols, ld, 0, 0, &pl);
+    if (rc) return rc;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return MSQ_ECUDA;
+    DevCache& C = g_cache[dev];
+    std::lock_guard<std::mutex> lk(C.mu);
+    if ((rc = grow(&C.ws, &C.ws_bytes, (size_t)std::max<int64_t>(pl.ws_bytes, 256)))) return rc;
+    if ((rc = grow((void**)&C.res, &C.res_cap, sizeof(msq_devresult) * (size_t)batch))) return rc;
+    if (C.hres_cap < (size_t)batch) {
+        if (C.hres) cudaFreeHost(C.hres);
+        C.hres = nullptr;
+        C.hres_cap = 0;
+        if (cudaMallocHost((void**)&C.hres, sizeof(msq_devresult) * (size_t)batch) != cudaSuccess)
+            return MSQ_ENOMEM;
+        C.hres_cap = (size_t)batch;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    rc = msq_launch(&pl, d_src, C.ws, C.res, stream);
+    if (rc) return rc;
+    if (cudaMemcpyAsync(C.hres, C.res, sizeof(msq_devresult) * (size_t)batch, cudaMemcpyDeviceToHost,
+                        st) != cudaSuccess)
+        return MSQ_ECUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return MSQ_ECUDA;
+    int worst = MSQ_OK;
+    for (int64_t k = 0; k < batch; ++k) {
+        int r = msq_decode(&C.hres[k], rows, cols, &out[k]);
+        if (r) worst = r;
+    }
+    return worst;
+}
+
+}  // namespace
+
+extern "C" {
+
+int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld, int32_t nbands,
+                  int32_t deterministic, msq_plan* plan) {
+    if (!plan || (fmt != MSQ_FMT_U8 && fmt != MSQ_FMT_BITS) || batch < 1) return MSQ_EINVAL;
+    if (rows < 1 || cols < 1 || rows >= (1ll << 21) || cols > 65536) return MSQ_EINVAL;
+    const int64_t words = ceil_div(cols, 32);
+    if (fmt == MSQ_FMT_U8 && ld < cols) return MSQ_EINVAL;
+    if (fmt == MSQ_FMT_BITS && ld < words) return MSQ_EINVAL;
+    if (words > kMaxWords) return MSQ_EINVAL;
+    msq_plan p{};
+    p.fmt = fmt;
+    p.batch = batch;
+    p.rows = rows;
+    p.cols = cols;
+    p.ld = ld;
+    p.words = (int32_t)words;
+    p.wpt = words <= 512 ? 1 : (words <= 1024 ? 2 : 4);
+    p.threads = (int32_t)std::max<long long>(32, round_up(ceil_div(words, p.wpt), 32));
+    p.tile_rows = kTileRows;
+    // bands: one per SM for large single matrices; none for batches
+    int nb = nbands;
+    if (batch > 1) {
+        nb = 1;
+    } else if (nb <= 0) {
+        nb = (int)std::min<long long>(num_sms(), std::max<long long>(1, rows / 64));
+    }
+    nb = (int)std::max<long long>(nb, ceil_div(rows, 65535));
+    if (nb > rows) nb = (int)rows;
+    if (batch > 1 && nb != 1) return MSQ_EINVAL;
+    p.nbands = nb;
+    p.deterministic = deterministic ? 1 : 0;
+    p.row_base = 0;
+    const long long wpad = (long long)p.threads * p.wpt;
+    const long long zbytes = wpad * 32 * 2;
+    const long long hbytes = (long long)kTileRows * wpad * 4;
+    const long long misc = 64;
+    const long long row_bytes = fmt == MSQ_FMT_U8 ? cols : words * 4;
+    const long long ld_bytes = fmt == MSQ_FMT_U8 ? ld : ld * 4;
+    p.row_stage_bytes = (int32_t)row_bytes;
+    p.nstage = 0;
+    const bool tma_ok = (row_bytes % 16 == 0) && (ld_bytes % 16 == 0) && row_bytes <= 65536;
+    if (tma_ok) {
+        const long long avail = kSmemMax - zbytes - hbytes - misc - 128;
+        long long ns = avail / ((long long)kTileRows * row_bytes);
+        ns = std::min<long long>(ns, batch > 1 ? 3 : 8);
+        if (ns >= 2) p.nstage = (int32_t)ns;
+    }
+    long long s1 = zbytes + hbytes + misc;
+    if (p.nstage) s1 += (long long)p.nstage * kTileRows * row_bytes + round_up(p.nstage * 8, 16);
+    p.smem_pass1 = (int32_t)s1;
+    p.smem_fixup = (int32_t)(wpad * 32 * 3 + hbytes + misc);
+    if (p.smem_pass1 > kSmemMax || p.smem_fixup > kSmemMax) return MSQ_EINVAL;
+    p.ws_bytes = (int64_t)ws_layout(&p).total;
+    *plan = p;
+    return MSQ_OK;
+}
+
+int msq_launch(const msq_plan* pl, const void* d_src, void* d_ws, msq_devresult* d_result, void* stream) {
+    if (!pl || !d_src || !d_result || (!d_ws && pl->ws_bytes > 0)) return MSQ_EINVAL;
+    if (pl->nstage > 0 && ((uintptr_t)d_src % 16) != 0) {
+        msq_plan q = *pl;  // misaligned base: fall back to direct loads
+        q.nstage = 0;
+        return msq_launch(&q, d_src, d_ws, d_result, stream);
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    g_last_launches = 0;
+    if (cudaMemsetAsync(d_result, 0, sizeof(msq_devresult) * (size_t)pl->batch, st) != cudaSuccess)
+        return MSQ_ECUDA;
+    const bool multi = pl->batch == 1 && pl->nbands > 1;
+    msq::Pass1Params p1 = make_pass1(pl, d_src, d_ws, d_result, multi);
+    cudaError_t e = launch_pass1(pl, p1, st);
+    if (e != cudaSuccess) return MSQ_ECUDA;
+    g_last_launches = 1;
+    if (multi) {
+        msq::FixParams f = make_fix(pl, d_ws, nullptr, d_result);
+        e = launch_fixup(pl, f, pl->nbands - 1, st);
+        if (e != cudaSuccess) return MSQ_ECUDA;
+        g_last_launches = 2;
+    }
+    return MSQ_OK;
+}
+
+int msq_decode(const msq_devresult* r, int64_t rows, int64_t cols, msq_result* out) {
+    if (!r || !out) return MSQ_EINVAL;
+    const unsigned long long key = std::max(r->key_pass1, r->key_fix);
+    if (key == 0) {
+        *out = msq_result{0, 0, rows * cols, -1, -1};
+    } else {
+        const int64_t side = (int64_t)(key >> (2 * msq::KEY_DIM_BITS));
+        const int64_t bottom = (int64_t)(msq::KEY_DIM_MASK - ((key >> msq::KEY_DIM_BITS) & msq::KEY_DIM_MASK));
+        const int64_t right = (int64_t)(msq::KEY_DIM_MASK - (key & msq::KEY_DIM_MASK));
+        *out = msq_result{side, side * side, rows * cols, bottom - side + 1, right - side + 1};
+    }
+    return (r->status & 1u) ? MSQ_EVALUE : MSQ_OK;
+}
+
+int msq_solve_u8(const uint8_t* d_cells, int64_t rows, int64_t cols, int64_t ld, msq_result* out,
+                 void* stream) {
+    return solve_sync(MSQ_FMT_U8, 1, d_cells, rows, cols, ld, out, stream);
+}
+
+int msq_solve_bits(const uint32_t* d_words, int64_t rows, int64_t cols, int64_t ld_words, msq_result* out,
+                   void* stream) {
+    return solve_sync(MSQ_FMT_BITS, 1, d_words, rows, cols, ld_words, out, stream);
+}
+
+int msq_solve_batch_u8(const uint8_t* d_cells, int64_t batch, int64_t rows, int64_t cols, msq_result* out,
+                       void* stream) {
+    if (batch < 1) return MSQ_EINVAL;
+    return solve_sync(MSQ_FMT_U8, batch, d_cells, rows, cols, cols, out, stream);
+}
+
+static int solve_host(int32_t fmt, const void* h, int64_t rows, int64_t cols, int64_t ld, msq_result* out,
+                      void* stream) {
+    if (!out) return MSQ_EINVAL;
+    if (rows == 0 || cols == 0) return solve_sync(fmt, 1, h, rows, cols, ld, out, stream);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return MSQ_ECUDA;
+    const size_t bytes = (size_t)rows * (size_t)ld * (fmt == MSQ_FMT_U8 ? 1 : 4);
+    void* din;
+    {
+        DevCache& C = g_cache[dev];
+        std::lock_guard<std::mutex> lk(C.mu);
+        int rc = grow(&C.in, &C.in_bytes, bytes);
+        if (rc) return rc;
+        din = C.in;
+        if (cudaMemcpyAsync(din, h, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream) != cudaSuccess)
+            return MSQ_ECUDA;
+    }
+    return solve_sync(fmt, 1, din, rows, cols, ld, out, stream);
+}
+
+int msq_solve_u8_host(const uint8_t* h_cells, int64_t rows, int64_t cols, int64_t ld, msq_result* out,
+                      void* stream) {
+    return solve_host(MSQ_FMT_U8, h_cells, rows, cols, ld, out, stream);
+}
+
+int msq_solve_bits_host(const uint32_t* h_words, int64_t rows, int64_t cols, int64_t ld_words,
+                        msq_result* out, void* stream) {
+    return solve_host(MSQ_FMT_BITS, h_words, rows, cols, ld_words, out, stream);
+}
+
+int msq_rank_pass1(const msq_plan* pl, const void* d_src, void* d_ws, msq_devresult* d_result, void* stream) {
+    if (!pl || pl->batch != 1 || !d_src || !d_ws || !d_result) return MSQ_EINVAL;
+    if (pl->nstage > 0 && ((uintptr_t)d_src % 16) != 0) {
+        msq_plan q = *pl;
+        q.nstage = 0;
+        return msq_rank_pass1(&q, d_src, d_ws, d_result, stream);
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemsetAsync(d_result, 0, sizeof(msq_devresult), st) != cudaSuccess) return MSQ_ECUDA;
+    msq::Pass1Params p1 = make_pass1(pl, d_src, d_ws, d_result, true);
+    g_last_launches = 1;
+    return cuda_status(launch_pass1(pl, p1, st));
+}
+
+int msq_rank_summary(const msq_plan* pl, const void* d_ws, uint32_t* d_summary, void* stream) {
+    if (!pl || !d_ws || !d_summary || pl->batch != 1) return MSQ_EINVAL;
+    WsLayout L = ws_layout(pl);
+    const uint8_t* w = (const uint8_t*)d_ws;
+    const int threads = 256;
+    const int blocks = (int)ceil_div(pl->cols, threads);
+    msq::rank_summary_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
+        (int)pl->rows, (int)pl->cols, pl->words, pl->nbands, pl->words * 32, (const uint16_t*)(w + L.b),
+        (const uint32_t*)(w + L.ao), d_summary);
+    return cuda_status(cudaGetLastError());
+}
+
+int msq_compose_carry(const uint32_t* d_summaries, const int64_t* h_rank_rows, int32_t nranks, int32_t rank,
+                      int64_t cols, uint32_t* d_base_carry, void* stream) {
+    if (!d_summaries || !h_rank_rows || !d_base_carry || nranks < 1 || nranks > 64 || rank < 0 ||
+        rank >= nranks || cols < 1)
+        return MSQ_EINVAL;
+    msq::RankRows rr{};
+    for (int q = 0; q < nranks; ++q) rr.r[q] = h_rank_rows[q];
+    const int threads = 256;
+    msq::compose_carry_kernel<<<(int)ceil_div(cols, threads), threads, 0, (cudaStream_t)stream>>>(
+        d_summaries, rr, rank, (int)cols, d_base_carry);
+    return cuda_status(cudaGetLastError());
+}
+
+int msq_rank_fixup(const msq_plan* pl, void* d_ws, const uint32_t* d_base_carry, msq_devresult* d_result,
+                   void* stream) {
+    if (!pl || !d_ws || !d_result || pl->batch != 1) return MSQ_EINVAL;
+    msq::FixParams f = make_fix(pl, d_ws, d_base_carry, d_result);
+    const int nblocks = pl->nbands - f.band_begin;
+    return cuda_status(launch_fixup(pl, f, nblocks, (cudaStream_t)stream));
+}
+
+int msq_ws_views(const msq_plan* pl, void* d_ws, uint16_t** e, uint16_t** b, uint32_t** allones,
+                 uint64_t** band_keys) {
+    if (!pl || !d_ws) return MSQ_EINVAL;
+    WsLayout L = ws_layout(pl);
+    uint8_t* w = (uint8_t*)d_ws;
+    if (e) *e = (uint16_t*)(w + L.e);
+    if (b) *b = (uint16_t*)(w + L.b);
+    if (allones) *allones = (uint32_t*)(w + L.ao);
+    if (band_keys) *band_keys = (uint64_t*)(w + L.band_keys);
+    return MSQ_OK;
+}
+
+int msq_gen_hash(int32_t fmt, uint64_t seed, uint64_t thr53, int64_t row0, int64_t nrows, int64_t cols,
+                 int64_t ld, void* d_out, void* stream) {
+    if (!d_out || nrows < 0 || cols < 1) return MSQ_EINVAL;
+    const int threads = 256, blocks = 148 * 8;
+    if (fmt == MSQ_FMT_U8)
+        msq::gen_hash_u8_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(seed, thr53, row0, nrows, cols,
+                                                                              ld, (uint8_t*)d_out);
+    else if (fmt == MSQ_FMT_BITS)
+        msq::gen_hash_bits_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(seed, thr53, row0, nrows,
+                                                                                cols, ld, (uint32_t*)d_out);
+    else
+        return MSQ_EINVAL;
+    return cuda_status(cudaGetLastError());
+}
+
+int32_t msq_last_launch_count(void) { return g_last_launches; }
+
+const char* msq_strerror(int code) {
+    switch (code) {
+        case MSQ_OK: return "ok";
+        case MSQ_EINVAL: return "invalid argument (shape, stride or unsupported width)";
+        case MSQ_EVALUE: return "cells must contain only 0 or 1";
+        case MSQ_ECUDA: return "CUDA runtime error";
+        case MSQ_ENOMEM: return "device memory allocation failed";
+        default: return "unknown error";
+    }
+}
+
+const char* msq_version(void) { return "msq 0.1.0 sm_100a"; }
+
+}  // extern "C"

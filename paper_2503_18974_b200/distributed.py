@@ -1,0 +1,145 @@
+"""Row-band sharding of one matrix across GPUs (one process per GPU).
+
+Rank r owns rows [rows*r/N, rows*(r+1)/N).  Per solve:
+
+1. band passes over the local rows (libmsq: msq_rank_pass1) -> per-band column
+   summaries + a local key;
+2. per column, the bottom run of the local slice (msq_rank_summary, uint32,
+   == local rows when the column is all ones);
+3. ONE all-gather of those summaries (NCCL over NVLink; cols*4 bytes/rank);
+4. carry-in heights for the slice top from the ranks above
+   (msq_compose_carry: P5 fold);
+5. data-free band-boundary fix-ups, including the slice's top boundary
+   (msq_rank_fixup);
+6. all-reduce(max) of the 64-bit (side, -bottom, -right) key.
+
+The orchestration is independent of where the per-rank steps run: ``GpuBackend``
+calls the C ABI; tests substitute a CPU backend built on the oracle to check
+the exchange logic under gloo without a GPU.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as N
+from .squares import SquareResult
+
+KEY_DIM_BITS = 21
+KEY_DIM_MASK = (1 << KEY_DIM_BITS) - 1
+
+
+def slice_rows(rows: int, world: int, rank: int) -> tuple[int, int]:
+    r0 = rows * rank // world
+    return r0, rows * (rank + 1) // world - r0
+
+
+def decode_key(key: int, status: int, rows: int, cols: int) -> SquareResult:
+    if status & 1:
+        raise ValueError("cells must contain only 0 or 1")
+    if key == 0:
+        return SquareResult(0, 0, rows * cols)
+    side = key >> (2 * KEY_DIM_BITS)
+    bottom = KEY_DIM_MASK - ((key >> KEY_DIM_BITS) & KEY_DIM_MASK)
+    right = KEY_DIM_MASK - (key & KEY_DIM_MASK)
+    return SquareResult(side, side * side, rows * cols, bottom - side + 1, right - side + 1)
+
+
+class GpuBackend:
+    """Per-rank steps on the local GPU through libmsq."""
+
+    def __init__(self, fmt: int, local_rows: int, cols: int, row_base: int, ld: int | None = None,
+                 nbands: int = 0, device=None):
+        import torch
+        self.torch = torch
+        words = (cols + 31) // 32
+        ld = ld if ld is not None else (cols if fmt == N.FMT_U8 else words)
+        self.plan = N.plan(fmt, 1, local_rows, cols, ld, nbands)
+        self.plan.row_base = row_base
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.ws = torch.empty(max(int(self.plan.ws_bytes), 256), dtype=torch.uint8, device=dev)
+        self.res = torch.zeros(32, dtype=torch.uint8, device=dev)
+        self.summary = torch.empty(cols, dtype=torch.int32, device=dev)
+        self.base = torch.empty(cols, dtype=torch.int32, device=dev)
+        self.cols = cols
+        self.lib = N.load()
+        self.launches = 0
+
+    def _stream(self):
+        return ctypes.c_void_p(self.torch.cuda.current_stream().cuda_stream)
+
+    def pass1(self, src):
+        N.check(self.lib.msq_rank_pass1(ctypes.byref(self.plan), ctypes.c_void_p(src.data_ptr()),
+                                        ctypes.c_void_p(self.ws.data_ptr()),
+                                        ctypes.c_void_p(self.res.data_ptr()), self._stream()))
+        self.launches += 1
+
+    def rank_summary(self):
+        N.check(self.lib.msq_rank_summary(ctypes.byref(self.plan),
+                                          ctypes.c_void_p(self.ws.data_ptr()),
+                                          ctypes.c_void_p(self.summary.data_ptr()), self._stream()))
+        self.launches += 1
+        return self.summary
+
+    def new_gather_buffer(self, world: int):
+        return self.torch.empty((world, self.cols), dtype=self.torch.int32, device=self.summary.device)
+
+    def compose(self, gathered, rank_rows: list[int], rank: int):
+        rr = (ctypes.c_int64 * len(rank_rows))(*rank_rows)
+        N.check(self.lib.msq_compose_carry(ctypes.c_void_p(gathered.data_ptr()), rr,
+                                           len(rank_rows), rank, self.cols,
+                                           ctypes.c_void_p(self.base.data_ptr()), self._stream()))
+        self.launches += 1
+        return self.base
+
+    def fixup(self, base):
+        ptr = ctypes.c_void_p(base.data_ptr()) if base is not None else None
+        N.check(self.lib.msq_rank_fixup(ctypes.byref(self.plan), ctypes.c_void_p(self.ws.data_ptr()),
+                                        ptr, ctypes.c_void_p(self.res.data_ptr()), self._stream()))
+        nb = int(self.plan.nbands) - (0 if base is not None else 1)
+        self.launches += 1 if nb > 0 else 0
+
+    def key_status(self):
+        """int64 tensor [key, status] for the all-reduce (keys < 2^63)."""
+        v = self.res.view(self.torch.int64)
+        key = self.torch.maximum(v[0], v[1]).reshape(1)
+        status = (v[2] & 0xFFFFFFFF).reshape(1)
+        return self.torch.cat([key, status])
+
+
+class RowBandSolver:
+    """Solve one (rows x cols) matrix sharded by rows over a process group."""
+
+    def __init__(self, rows: int, cols: int, rank: int, world: int, backend, group=None):
+        self.rows, self.cols, self.rank, self.world = rows, cols, rank, world
+        self.row0, self.local_rows = slice_rows(rows, world, rank)
+        self.rank_rows = [slice_rows(rows, world, q)[1] for q in range(world)]
+        self.backend = backend
+        self.group = group
+        self.gathered = backend.new_gather_buffer(world) if world > 1 else None
+        self._ks = None
+
+    def launch(self, src) -> None:
+        import torch.distributed as dist
+        be = self.backend
+        be.pass1(src)
+        base = None
+        if self.world > 1:
+            summary = be.rank_summary()
+            dist.all_gather_into_tensor(self.gathered, summary, group=self.group)
+            if self.rank > 0:
+                base = be.compose(self.gathered, self.rank_rows, self.rank)
+        be.fixup(base)
+        ks = be.key_status()
+        if self.world > 1:
+            dist.all_reduce(ks, op=dist.ReduceOp.MAX, group=self.group)
+        self._ks = ks
+
+    def result(self) -> SquareResult:
+        ks = self._ks.cpu().numpy().astype(np.int64)
+        return decode_key(int(ks[0]), int(ks[1]), self.rows, self.cols)
+
+    def solve(self, src) -> SquareResult:
+        self.launch(src)
+        return self.result()

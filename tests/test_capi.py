@@ -1,0 +1,64 @@
+"""C-ABI library checks that need no GPU: it loads, exports every symbol that
+include/msq.h declares, and plans shapes the way DESIGN.md says."""
+import ctypes
+
+import pytest
+
+from paper_2503_18974_b200 import _native as N
+from paper_2503_18974_b200 import build as B
+
+
+@pytest.fixture(scope="module")
+def lib():
+    B.build()
+    return N.load()
+
+
+def test_every_header_symbol_is_exported(lib):
+    names = N.header_symbols()
+    assert len(names) >= 15
+    for name in names:
+        assert hasattr(lib, name), name
+
+
+def test_strerror_and_version(lib):
+    assert lib.msq_strerror(N.MSQ_EVALUE).decode() == "cells must contain only 0 or 1"
+    assert b"sm_100a" in lib.msq_version()
+
+
+def test_plan_shapes(lib):
+    p = N.plan(N.FMT_BITS, 1, 65536, 65536, 2048)
+    assert (p.words, p.wpt, p.threads) == (2048, 4, 512)
+    assert p.nstage >= 2 and p.smem_pass1 <= 232448 and p.smem_fixup <= 232448
+    assert 1 <= p.nbands <= 148
+    p = N.plan(N.FMT_U8, 1, 32768, 32768, 32768)
+    assert (p.words, p.wpt, p.threads) == (1024, 2, 512)
+    assert p.nstage >= 2
+    p = N.plan(N.FMT_U8, 4096, 256, 256, 256)
+    assert (p.nbands, p.threads, p.batch) == (1, 32, 4096)
+    # odd width: no TMA staging (rows are not 16-byte multiples)
+    p = N.plan(N.FMT_U8, 1, 7, 13, 13)
+    assert p.nstage == 0 and p.nbands == 1
+
+
+def test_plan_rejects_bad_shapes(lib):
+    with pytest.raises(ValueError):
+        N.plan(N.FMT_U8, 1, 10, 70000, 70000)  # wider than 65536 columns
+    with pytest.raises(ValueError):
+        N.plan(N.FMT_U8, 1, 10, 10, 5)  # ld < cols
+    with pytest.raises(ValueError):
+        N.plan(N.FMT_U8, 1, 0, 10, 10)
+
+
+def test_bands_respect_uint16_heights(lib):
+    p = N.plan(N.FMT_BITS, 1, 2**20, 64, 2, nbands=1)
+    assert p.nbands >= 17  # every band <= 65535 rows
+
+
+def test_decode_empty_key(lib):
+    r = N.MsqDevResult()
+    out = N.MsqResult()
+    assert lib.msq_decode(ctypes.byref(r), 3, 4, ctypes.byref(out)) == 0
+    assert (out.side, out.area, out.cells_visited, out.top, out.left) == (0, 0, 12, -1, -1)
+    r.status = 1
+    assert lib.msq_decode(ctypes.byref(r), 3, 4, ctypes.byref(out)) == N.MSQ_EVALUE

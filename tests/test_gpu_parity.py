@@ -1,0 +1,211 @@
+"""GPU parity: the sm_100a library (through the C ABI) against the CPU oracle
+and the reference's golden vectors.  Bit-exact on side, area, cells_visited,
+top and left; intermediates (band summaries, band keys) bit-exact against the
+oracle's restatement of the band algebra."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2503_18974_b200 import _native as N
+from paper_2503_18974_b200 import configs, grid
+from paper_2503_18974_b200.squares import Solver, freq_square, freq_square_bits, solve_batch
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    from paper_2503_18974_b200 import build
+    build.build()
+    return t
+
+
+def _same(res, want):
+    assert (res.side, res.area, res.cells_visited, res.top, res.left) == (
+        want.side, want.area, want.cells_visited, want.top, want.left)
+
+
+def test_golden_kats(torch):
+    with open(os.path.join(GOLDEN, "golden.json")) as f:
+        g = json.load(f)
+    for case in g["kats"]:
+        m = grid.BinaryMatrix.from_rows(case["rows"])
+        r = freq_square(m)
+        assert (r.side, r.top, r.left) == (case["side"], case["top"], case["left"]), case["name"]
+        assert r.area == r.side ** 2 and r.cells_visited == m.rows * m.cols
+    for case in g["genspec"]:
+        m = grid.generate_matrix(grid.GenSpec(*case["spec"]))
+        r = freq_square(m)
+        assert (r.side, r.top, r.left) == (case["side"], case["top"], case["left"]), case["spec"]
+    for case in g["edge"]:
+        if case["kind"] == "empty":
+            r = freq_square(grid.EMPTY_MATRIX)
+            assert (r.side, r.area, r.cells_visited, r.top, r.left) == (0, 0, 0, -1, -1)
+            continue
+        m = grid.generate_edge_case(grid.EdgeKind(case["kind"]), case["n"])
+        r = freq_square(m)
+        assert (r.side, r.top, r.left) == (case["side"], case["top"], case["left"]), case["name"]
+
+
+def test_exhaustive_4x4_batched(torch):
+    ex = np.load(os.path.join(GOLDEN, "exhaustive4x4.npz"))
+    total = 0
+    for r in range(1, 5):
+        for c in range(1, 5):
+            bits = r * c
+            pats = np.arange(2 ** bits, dtype=np.int64)
+            cells = ((pats[:, None] >> np.arange(bits - 1, -1, -1)) & 1).astype(np.uint8)
+            res = solve_batch(cells.reshape(-1, r, c))
+            assert np.array_equal([x.side for x in res], ex[f"side_{r}x{c}"])
+            assert np.array_equal([x.top for x in res], ex[f"top_{r}x{c}"])
+            assert np.array_equal([x.left for x in res], ex[f"left_{r}x{c}"])
+            total += len(pats)
+    assert total == 74_954
+
+
+def test_random_campaign_10k(torch):
+    rc = np.load(os.path.join(GOLDEN, "random_campaign.npz"))
+    for k in range(len(rc["rows"])):
+        spec = grid.GenSpec(int(rc["rows"][k]), int(rc["cols"][k]), float(rc["density"][k]),
+                            int(rc["seed"][k]))
+        r = freq_square(grid.generate_matrix(spec))
+        assert (r.side, r.top, r.left) == (rc["side"][k], rc["top"][k], rc["left"][k]), k
+
+
+def _planted(rng, rows, cols, p, k):
+    a = (rng.random((rows, cols)) < p).astype(np.uint8)
+    if k and k <= min(rows, cols):
+        t = int(rng.integers(0, rows - k + 1))
+        l_ = int(rng.integers(0, cols - k + 1))
+        a[t:t + k, l_:l_ + k] = 1
+    return a
+
+
+@pytest.mark.parametrize("fmt", ["u8", "bits"])
+def test_band_intermediates_match_oracle(torch, fmt):
+    """Deterministic mode: e/b/all-ones summaries and pass-1 band keys == oracle P6 pass."""
+    rng = np.random.default_rng(21 if fmt == "u8" else 22)
+    for it in range(60):
+        rows = int(rng.integers(8, 400))
+        cols = int(rng.choice([32, 64, 96, 200, 256, 512, 1000, 2048]))
+        p = float(rng.choice([0.6, 0.9, 0.97, 0.995, 1.0]))
+        a = _planted(rng, rows, cols, p, int(rng.integers(0, 60)))
+        nb = int(rng.integers(1, min(rows, 40) + 1))
+        if fmt == "u8":
+            src = torch.from_numpy(a).cuda()
+            s = Solver(N.FMT_U8, rows, cols, nbands=nb, deterministic=True)
+            host = a
+            f = 0
+        else:
+            w = grid.pack_bits(a)
+            src = torch.from_numpy(w.view(np.int32)).cuda()
+            s = Solver(N.FMT_BITS, rows, cols, nbands=nb, deterministic=True)
+            host = w
+            f = 1
+        res = s.solve(src)[0]
+        _same(res, oracle.freq(a))
+        if s.nbands > 1:
+            e, b, ao, bk = (x.cpu().numpy() for x in s.views())
+            for band in range(s.nbands):
+                r0 = rows * band // s.nbands
+                r1 = rows * (band + 1) // s.nbands
+                oe, ob, oao, okey = oracle.band_pass(host, f, r0, r1, cols, 1)
+                assert np.array_equal(e[band, :cols].view(np.uint16), oe), (it, band)
+                assert np.array_equal(b[band, :cols].view(np.uint16), ob), (it, band)
+                assert np.array_equal(ao[band].view(np.uint32), oao), (it, band)
+                assert int(bk[band]) == okey, (it, band)
+
+
+def test_random_banded_solves(torch):
+    """Non-deterministic (shared-threshold) mode, many band counts and shapes."""
+    rng = np.random.default_rng(7)
+    for it in range(300):
+        rows = int(rng.integers(1, 700))
+        cols = int(rng.integers(1, 700))
+        p = float(rng.choice([0.3, 0.8, 0.95, 0.99, 1.0]))
+        a = _planted(rng, rows, cols, p, int(rng.integers(0, 120)))
+        want = oracle.freq(a)
+        src = torch.from_numpy(a).cuda()
+        nb = int(rng.integers(1, min(rows, 64) + 1))
+        _same(Solver(N.FMT_U8, rows, cols, nbands=nb).solve(src)[0], want)
+        if it % 3 == 0:
+            w = torch.from_numpy(grid.pack_bits(a).view(np.int32)).cuda()
+            _same(Solver(N.FMT_BITS, rows, cols, nbands=nb).solve(w)[0], want)
+
+
+def test_strided_and_odd_widths(torch):
+    rng = np.random.default_rng(9)
+    for cols in (1, 3, 17, 31, 33, 63, 65, 100, 130):
+        a = (rng.random((50, cols)) < 0.9).astype(np.uint8)
+        wide = np.zeros((50, cols + 19), np.uint8)
+        wide[:, :cols] = a
+        t = torch.from_numpy(wide).cuda()
+        s = Solver(N.FMT_U8, 50, cols, ld=cols + 19, nbands=3)
+        _same(s.solve(t)[0], oracle.freq(a))
+        _same(freq_square(a), oracle.freq(a))
+        _same(freq_square_bits(grid.pack_bits(a), cols), oracle.freq(a))
+
+
+def test_invalid_cells_raise_value_error(torch):
+    a = np.ones((40, 64), np.uint8)
+    a[17, 5] = 2
+    with pytest.raises(ValueError):
+        freq_square(a)
+    t = torch.from_numpy(a).cuda()
+    with pytest.raises(ValueError):
+        freq_square(t)
+
+
+def test_device_generator_matches_oracle(torch):
+    thr = configs.thr53(0.97)
+    d = configs.device_hash("u8", 77, 0.97, 64, 300).cpu().numpy()
+    assert np.array_equal(d, oracle.gen_hash_u8(77, thr, 0, 64, 300))
+    w = configs.device_hash("bits", 77, 0.97, 64, 300).cpu().numpy().view(np.uint32)
+    assert np.array_equal(w, oracle.gen_hash_bits(77, thr, 0, 64, 300))
+
+
+def test_cfg1(torch):
+    r = freq_square(grid.generate_matrix(grid.GenSpec(512, 512, 0.7, 0)))
+    assert (r.side, r.area, r.cells_visited, r.top, r.left) == (5, 25, 512 * 512, 0, 67)
+
+
+def test_cfg2_batch_vs_oracle(torch):
+    cells = configs.cfg2_array(count=512)
+    got = solve_batch(cells)
+    want = oracle.freq_batch(cells)
+    for g_, w_ in zip(got, want):
+        _same(g_, w_)
+
+
+def test_cfg3_planted_and_edges(torch):
+    m = configs.cfg3_device()
+    want = oracle.freq(m.cpu().numpy())
+    _same(freq_square(m), want)
+    top, left = configs.cfg3_square_pos()
+    assert want.side >= 2048
+    z = torch.zeros((16384, 16384), dtype=torch.uint8, device="cuda")
+    r = freq_square(z)
+    assert (r.side, r.top, r.left) == (0, -1, -1)
+    z.fill_(1)
+    r = freq_square(z)
+    assert (r.side, r.area, r.top, r.left) == (16384, 16384 ** 2, 0, 0)
+
+
+@pytest.mark.slow
+def test_cfg4_full_size(torch):
+    w = configs.cfg4_device()
+    got = freq_square_bits(w, 65536)
+    host = w.cpu().numpy().view(np.uint32)
+    _same(got, oracle.freq_bits(host, 65536))
+
+
+@pytest.mark.slow
+def test_cfg5_full_size(torch):
+    m = configs.cfg5_device()
+    got = freq_square(m)
+    _same(got, oracle.freq(m.cpu().numpy()))
