@@ -73,7 +73,7 @@ cudaError_t launch_pass1_t(const msq_plan* pl, const msq::Pass1Params& prm, cuda
         if (e != cudaSuccess) return e;
         attr_set[dev] = true;
     }
-    dim3 grid((unsigned)pl->nbands, (unsigned)pl->batch);
+    dim3 grid((unsigned)pl->nbands * (unsigned)pl->batch);
     kern<<<grid, pl->threads, pl->smem_pass1, st>>>(prm);
     return cudaGetLastError();
 }

@@ -241,8 +241,8 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int NT = blockDim.x;
     const int tau = threadIdx.x;
-    const int band = blockIdx.x;
-    const int mat = blockIdx.y;
+    const int band = (int)(blockIdx.x % (unsigned)p.nbands);
+    const int mat = (int)(blockIdx.x / (unsigned)p.nbands);
     const int W = p.W;
     const int Wpad = NT * WPT;
     const int r0 = band_row0(p.rows, p.nbands, band);
