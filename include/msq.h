@@ -76,6 +76,12 @@ typedef struct {
     int32_t deterministic;/* 1: no cross-band threshold sharing             */
     int64_t row_base;     /* global row index of row 0 (row-band sharding)  */
     int64_t ws_bytes;     /* required workspace bytes                       */
+    int32_t team;         /* threads per band team (sub-warp for batches)   */
+    int32_t teams_per_cta;
+    int32_t tile_rows_l;  /* rows per tile once the threshold is >= tl      */
+    int32_t tl;           /* threshold where the word-level filter takes over */
+    int32_t grid;         /* pass-1 CTAs                                    */
+    int32_t reserved;
 } msq_plan;
 
 /* Build a plan.  nbands <= 0 picks a default (one band per SM, bands of

@@ -38,7 +38,9 @@ class MsqPlan(ctypes.Structure):
                 ("nstage", ctypes.c_int32), ("row_stage_bytes", ctypes.c_int32),
                 ("smem_pass1", ctypes.c_int32), ("smem_fixup", ctypes.c_int32),
                 ("deterministic", ctypes.c_int32), ("row_base", ctypes.c_int64),
-                ("ws_bytes", ctypes.c_int64)]
+                ("ws_bytes", ctypes.c_int64), ("team", ctypes.c_int32),
+                ("teams_per_cta", ctypes.c_int32), ("tile_rows_l", ctypes.c_int32),
+                ("tl", ctypes.c_int32), ("grid", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 _lib = None

@@ -16,7 +16,7 @@
 namespace {
 
 constexpr int kSmemMax = 232448;  // 227 KB opt-in dynamic shared memory per CTA (sm_100)
-constexpr int kTileRows = 2;
+constexpr int kModeLThreshold = 96;  // >= 63 (see msq_engine.cuh)
 constexpr int kMaxWords = 2048;   // 65536 columns
 
 thread_local int32_t g_last_launches = 0;
@@ -62,33 +62,34 @@ WsLayout ws_layout(const msq_plan* p) {
 }
 
 // ------------------------------------------------------------- dispatch
-template <int WPT, bool U8, bool TMA>
-cudaError_t launch_pass1_t(const msq_plan* pl, const msq::Pass1Params& prm, cudaStream_t st) {
-    auto kern = msq::pass1_kernel<WPT, kTileRows, U8, TMA>;
-    static bool attr_set[64] = {false};
+template <class K>
+cudaError_t set_smem_attr(K kern, bool* done) {
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 64 && !attr_set[dev]) {
+    if (dev < 64 && !done[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
         if (e != cudaSuccess) return e;
-        attr_set[dev] = true;
+        done[dev] = true;
     }
-    dim3 grid((unsigned)pl->nbands * (unsigned)pl->batch);
-    kern<<<grid, pl->threads, pl->smem_pass1, st>>>(prm);
+    return cudaSuccess;
+}
+
+template <int WPT, bool U8, bool TMA, bool SUB>
+cudaError_t launch_pass1_t(const msq_plan* pl, const msq::Pass1Params& prm, cudaStream_t st) {
+    auto kern = msq::pass1_kernel<WPT, U8, TMA, SUB>;
+    static bool attr_set[64] = {false};
+    cudaError_t e = set_smem_attr(kern, attr_set);
+    if (e != cudaSuccess) return e;
+    kern<<<pl->grid, pl->threads, pl->smem_pass1, st>>>(prm);
     return cudaGetLastError();
 }
 
 template <int WPT>
 cudaError_t launch_fixup_t(const msq_plan* pl, const msq::FixParams& prm, int nblocks, cudaStream_t st) {
-    auto kern = msq::fixup_kernel<WPT, kTileRows>;
+    auto kern = msq::fixup_kernel<WPT>;
     static bool attr_set[64] = {false};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 64 && !attr_set[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
-        if (e != cudaSuccess) return e;
-        attr_set[dev] = true;
-    }
+    cudaError_t e = set_smem_attr(kern, attr_set);
+    if (e != cudaSuccess) return e;
     kern<<<nblocks, pl->threads, pl->smem_fixup, st>>>(prm);
     return cudaGetLastError();
 }
@@ -96,11 +97,17 @@ cudaError_t launch_fixup_t(const msq_plan* pl, const msq::FixParams& prm, int nb
 cudaError_t launch_pass1(const msq_plan* pl, const msq::Pass1Params& prm, cudaStream_t st) {
     const bool u8 = pl->fmt == MSQ_FMT_U8;
     const bool tma = pl->nstage > 0;
-#define MSQ_P1(W_, U_, T_) \
-    if (pl->wpt == W_ && u8 == U_ && tma == T_) return launch_pass1_t<W_, U_, T_>(pl, prm, st);
-    MSQ_P1(1, true, true) MSQ_P1(1, true, false) MSQ_P1(1, false, true) MSQ_P1(1, false, false)
-    MSQ_P1(2, true, true) MSQ_P1(2, true, false) MSQ_P1(2, false, true) MSQ_P1(2, false, false)
-    MSQ_P1(4, true, true) MSQ_P1(4, true, false) MSQ_P1(4, false, true) MSQ_P1(4, false, false)
+    const bool sub = pl->team < pl->threads || pl->teams_per_cta > 1;
+#define MSQ_P1(W_, U_, T_, S_) \
+    if (pl->wpt == W_ && u8 == U_ && tma == T_ && sub == S_) return launch_pass1_t<W_, U_, T_, S_>(pl, prm, st);
+    MSQ_P1(1, true, true, true) MSQ_P1(1, true, false, true) MSQ_P1(1, false, true, true)
+    MSQ_P1(1, false, false, true)
+    MSQ_P1(1, true, true, false) MSQ_P1(1, true, false, false) MSQ_P1(1, false, true, false)
+    MSQ_P1(1, false, false, false)
+    MSQ_P1(2, true, true, false) MSQ_P1(2, true, false, false) MSQ_P1(2, false, true, false)
+    MSQ_P1(2, false, false, false)
+    MSQ_P1(4, true, true, false) MSQ_P1(4, true, false, false) MSQ_P1(4, false, true, false)
+    MSQ_P1(4, false, false, false)
 #undef MSQ_P1
     return cudaErrorInvalidValue;
 }
@@ -113,6 +120,10 @@ cudaError_t launch_fixup(const msq_plan* pl, const msq::FixParams& prm, int nblo
         case 4: return launch_fixup_t<4>(pl, prm, nblocks, st);
         default: return cudaErrorInvalidValue;
     }
+}
+
+int team_layout_bytes(const msq_plan* pl) {
+    return msq::p1_layout(pl->team, pl->wpt, pl->nstage, pl->row_stage_bytes, pl->tile_rows, pl->nstage > 0).total;
 }
 
 msq::Pass1Params make_pass1(const msq_plan* pl, const void* src, void* ws, msq_devresult* res,
@@ -133,8 +144,14 @@ msq::Pass1Params make_pass1(const msq_plan* pl, const void* src, void* ws, msq_d
     p.nstage = pl->nstage;
     p.rs = pl->row_stage_bytes;
     p.row_bytes = pl->row_stage_bytes;
+    p.bs = pl->tile_rows;
+    p.bl = pl->tile_rows_l;
+    p.tl = pl->tl;
     p.share = (pl->deterministic || pl->nbands == 1) ? 0 : 1;
     p.write_summaries = summaries ? 1 : 0;
+    p.team = pl->team;
+    p.units = pl->nbands * pl->batch;
+    p.layout_bytes = team_layout_bytes(pl);
     p.e_out = summaries ? (uint16_t*)(w + L.e) : nullptr;
     p.b_out = summaries ? (uint16_t*)(w + L.b) : nullptr;
     p.ao_out = summaries ? (uint32_t*)(w + L.ao) : nullptr;
@@ -154,6 +171,8 @@ msq::FixParams make_fix(const msq_plan* pl, void* ws, const uint32_t* base, msq_
     f.cols_pad = pl->words * 32;
     f.row_base = pl->row_base;
     f.band_begin = base ? 0 : 1;
+    f.bs = pl->tile_rows;
+    f.bl = pl->tile_rows_l;
     f.e_in = (const uint16_t*)(w + L.e);
     f.b_in = (const uint16_t*)(w + L.b);
     f.ao_in = (const uint32_t*)(w + L.ao);
@@ -252,41 +271,77 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
     p.cols = cols;
     p.ld = ld;
     p.words = (int32_t)words;
+    p.deterministic = deterministic ? 1 : 0;
+    p.row_base = 0;
+    p.tl = kModeLThreshold;
+    const long long row_bytes = fmt == MSQ_FMT_U8 ? cols : words * 4;
+    const long long ld_bytes = fmt == MSQ_FMT_U8 ? ld : ld * 4;
+    p.row_stage_bytes = (int32_t)row_bytes;
+    const bool tma_ok = (row_bytes % 16 == 0) && (ld_bytes % 16 == 0) && row_bytes <= 65536;
+    const int sms = num_sms();
+    if (batch > 1 && words <= 32) {
+        // ---- sub-warp teams: one small matrix per team, several teams per CTA
+        p.wpt = 1;
+        int ts = 1;
+        while (ts < words) ts *= 2;
+        p.team = ts;
+        p.nbands = 1;
+        p.tile_rows = msq::BMAX;
+        p.tile_rows_l = msq::BMAX;
+        long long tpc = std::max<long long>(1, ceil_div(batch, sms));
+        const long long gran = std::max(1, 32 / ts);  // teams per warp
+        tpc = round_up(tpc, gran);
+        tpc = std::min<long long>(tpc, 512 / ts);
+        p.nstage = tma_ok ? 6 : 0;
+        for (;;) {
+            const long long per = msq::p1_layout(ts, 1, p.nstage, (int)row_bytes, p.tile_rows, p.nstage > 0).total;
+            if (per * tpc <= kSmemMax) break;
+            if (p.nstage > 2) {
+                --p.nstage;
+            } else if (p.nstage > 0) {
+                p.nstage = 0;
+            } else {
+                tpc -= gran;
+                if (tpc < gran) return MSQ_EINVAL;
+            }
+        }
+        p.teams_per_cta = (int32_t)tpc;
+        p.threads = (int32_t)round_up(tpc * ts, 32);
+        p.grid = (int32_t)ceil_div(batch, tpc);
+        p.smem_pass1 = (int32_t)(tpc * msq::p1_layout(ts, 1, p.nstage, (int)row_bytes, p.tile_rows, p.nstage > 0).total);
+        p.smem_fixup = 0;
+        p.ws_bytes = (int64_t)ws_layout(&p).total;
+        *plan = p;
+        return MSQ_OK;
+    }
+    // ---- CTA teams: one band of one matrix per CTA
     p.wpt = words <= 512 ? 1 : (words <= 1024 ? 2 : 4);
     p.threads = (int32_t)std::max<long long>(32, round_up(ceil_div(words, p.wpt), 32));
-    p.tile_rows = kTileRows;
-    // bands: one per SM for large single matrices; none for batches
+    p.team = p.threads;
+    p.teams_per_cta = 1;
     int nb = nbands;
     if (batch > 1) {
         nb = 1;
     } else if (nb <= 0) {
-        nb = (int)std::min<long long>(num_sms(), std::max<long long>(1, rows / 64));
+        nb = (int)std::min<long long>(sms, std::max<long long>(1, rows / 64));
     }
     nb = (int)std::max<long long>(nb, ceil_div(rows, 65535));
     if (nb > rows) nb = (int)rows;
     if (batch > 1 && nb != 1) return MSQ_EINVAL;
     p.nbands = nb;
-    p.deterministic = deterministic ? 1 : 0;
-    p.row_base = 0;
-    const long long wpad = (long long)p.threads * p.wpt;
-    const long long zbytes = wpad * 32 * 2;
-    const long long hbytes = (long long)kTileRows * wpad * 4;
-    const long long misc = 64;
-    const long long row_bytes = fmt == MSQ_FMT_U8 ? cols : words * 4;
-    const long long ld_bytes = fmt == MSQ_FMT_U8 ? ld : ld * 4;
-    p.row_stage_bytes = (int32_t)row_bytes;
+    p.grid = nb * batch;
+    p.tile_rows = 2;
+    p.tile_rows_l = msq::BMAX;
     p.nstage = 0;
-    const bool tma_ok = (row_bytes % 16 == 0) && (ld_bytes % 16 == 0) && row_bytes <= 65536;
     if (tma_ok) {
-        const long long avail = kSmemMax - zbytes - hbytes - misc - 128;
-        long long ns = avail / ((long long)kTileRows * row_bytes);
-        ns = std::min<long long>(ns, batch > 1 ? 3 : 8);
-        if (ns >= 2) p.nstage = (int32_t)ns;
+        const int base = msq::p1_layout(p.threads, p.wpt, 0, (int)row_bytes, p.tile_rows, true).total;
+        long long ns = (kSmemMax - base - 256) / row_bytes;
+        ns = std::min<long long>(ns, 16);
+        if (ns < p.tile_rows_l + 2) p.tile_rows_l = 2;
+        if (ns >= p.tile_rows_l + 2) p.nstage = (int32_t)ns;
     }
-    long long s1 = zbytes + hbytes + misc;
-    if (p.nstage) s1 += (long long)p.nstage * kTileRows * row_bytes + round_up(p.nstage * 8, 16);
-    p.smem_pass1 = (int32_t)s1;
-    p.smem_fixup = (int32_t)(wpad * 32 * 3 + hbytes + misc);
+    p.smem_pass1 = msq::p1_layout(p.threads, p.wpt, p.nstage, (int)row_bytes, p.tile_rows, p.nstage > 0).total;
+    p.smem_fixup = msq::fix_layout(p.threads, p.wpt, p.tile_rows).total;
     if (p.smem_pass1 > kSmemMax || p.smem_fixup > kSmemMax) return MSQ_EINVAL;
     p.ws_bytes = (int64_t)ws_layout(&p).total;
     *plan = p;

@@ -2,29 +2,32 @@
 //
 // Reference semantics: /root/reference/pkg/src/squarelab/squares.py:68-114
 // (Algorithm 1 / _freq_core): per row, column one-run heights ("freq") are
-// updated and ONE threshold test is made: do t consecutive columns have
+// updated and ONE threshold test is made -- do t consecutive columns have
 // height >= t, t = best side so far + 1.  On success the side grows by one and
 // the location is the cell where the t-run closes (squares.py:93-97).
 //
-// B200 design (DESIGN.md has the full argument):
-//  * A matrix is cut into row bands, one CTA per band (<= one per SM).  Each
-//    CTA streams its rows through a TMA bulk-copy ring in shared memory and
-//    keeps, per 32-column word, the eligibility mask E = {j : h_j >= t} as a
-//    bit-set in registers.  Heights are never stored: smem holds u_j, the row
-//    of column j's last zero, and a column becomes eligible exactly when
-//    rho - u_j >= t.  Per word we keep TRIG = min u over ineligible columns,
-//    so a word is only revisited when a column can actually become eligible
-//    (event-driven: ~3% of word-rows at p = 0.999).
-//  * The threshold test runs on bit-sets with clz/ffs word walks; after the
-//    first row only words that gained eligible bits can create a new run, so
-//    the test is incremental.  B rows are tested per barrier ("tile"); a raise
-//    inside a tile re-tests later rows at t+1 with E_b(t+1) = E_b(t) & E_{b-1}(t)
-//    from the tile's E history.
-//  * Bands run standalone (local heights); squares crossing a band's top are
-//    recovered by a data-free fix-up on virtual heights c_j + d for columns
-//    whose leading run from the band top is >= d.  The fix-up
-//    reads no matrix data: only per-band (bottom run, leading depth, all-ones)
-//    column summaries written by pass 1.
+// B200 design (DESIGN.md has the full argument and the measurements):
+//  * One CTA ("team") per row band of one matrix; for batches of small
+//    matrices a team is a sub-warp (8/16/32 lanes) and one matrix is one band.
+//    Thread tau owns WPT consecutive 32-column words.  Rows stream through a
+//    TMA bulk-copy ring in shared memory (one cp.async.bulk per row).
+//  * Work per word-row is divergence free.  Two regimes, switched per tile:
+//      mode S (t < tl): heights kept as 7-plane bit-sliced saturating
+//        counters (min(h,127)); the eligibility mask E = {h >= t} is a
+//        bit-sliced compare against the warp-uniform t.  The row test walks
+//        E words (clz/ffs) from the smem E history.
+//      mode L (t >= tl >= 63): a run of >= t eligible columns must contain a
+//        whole word whose 32 columns are all eligible.  Per word we keep only
+//        Zw = last row with any zero; F = {rho - Zw >= t} is one compare.  The
+//        test scans the tile's F bitmap (rare runs) and checks the two
+//        boundary words exactly from per-column last-zero rows in smem.
+//    Per-column last-zero rows are written in a deferred per-tile phase (C)
+//    from the rows still resident in the TMA ring, so the hot loop never
+//    branches per bit.
+//  * B rows are tested per barrier; a raise inside a tile re-tests later rows
+//    at t+1 with X_b(t+1) = X_b(t) & X_{b-1}(t) (X = E or F).
+//  * Bands run standalone; squares crossing a band top are recovered by a
+//    data-free fix-up on virtual heights c_j + d while d <= e_j (P5/P6).
 //  * Result: one 64-bit key per unit, (side, -bottom, -right), max-reduced.
 #pragma once
 #include <cuda_runtime.h>
@@ -34,9 +37,11 @@ namespace msq {
 
 constexpr int KEY_DIM_BITS = 21;
 constexpr unsigned long long KEY_DIM_MASK = (1ull << KEY_DIM_BITS) - 1ull;
-constexpr int TRIG_INF = 1 << 29;
 constexpr uint32_t RES_INF = 0xFFFFFFFFu;
-constexpr int OFF_FIX = 65535;  // fix-up height offset: h = d + OFF - u, u = OFF - min(c, OFF)
+constexpr int NPLANES = 7;   // mode S counters saturate at 127
+constexpr int BMAX = 4;      // max rows per tile
+constexpr int FIX_XPL = 6;   // fix-up mode X planes (c, e clamped at 63)
+constexpr int FIX_TL = 63;   // fix-up mode L threshold (runs then contain a full word)
 
 __host__ __device__ __forceinline__ unsigned long long pack_key(long long side, long long bottom,
                                                                 long long right) {
@@ -48,6 +53,56 @@ __host__ __device__ __forceinline__ unsigned long long pack_key(long long side, 
 
 __host__ __device__ __forceinline__ int band_row0(int rows, int nbands, int band) {
     return (int)(((long long)rows * band) / nbands);
+}
+
+__host__ __device__ __forceinline__ int r16(int x) { return (x + 15) & ~15; }
+
+// ------------------------------------------------------------ smem layouts
+struct P1Layout {
+    int ring, bars, zs, za, hist, fmap, misc, total;
+};
+// per team; hist holds bs rows of E words, fmap 2 x BMAX rows of F bits
+__host__ __device__ inline P1Layout p1_layout(int NT, int WPT, int nstage, int rs, int bs, bool tma) {
+    P1Layout L;
+    const int wpad = NT * WPT, nfw = (wpad + 31) / 32;
+    int off = 0;
+    L.ring = off;
+    if (tma) off += nstage * rs;
+    L.bars = off;
+    if (tma) off += r16(nstage * 8);
+    L.zs = off;
+    off += wpad * 32 * 2;
+    L.za = off;
+    off += r16(wpad * 2);
+    L.hist = off;
+    off += bs * wpad * 4;
+    L.fmap = off;
+    off += 2 * BMAX * r16(nfw * 4);
+    L.misc = off;
+    off += 64;
+    L.total = (off + 127) & ~127;
+    return L;
+}
+
+struct FixLayout {
+    int us, e8, hist, fmap, misc, total;
+};
+__host__ __device__ inline FixLayout fix_layout(int NT, int WPT, int bs) {
+    FixLayout L;
+    const int wpad = NT * WPT, nfw = (wpad + 31) / 32;
+    int off = 0;
+    L.us = off;
+    off += wpad * 32 * 2;
+    L.e8 = off;
+    off += wpad * 32;
+    L.hist = off;
+    off += bs * wpad * 4;
+    L.fmap = off;
+    off += 2 * BMAX * r16(nfw * 4);
+    L.misc = off;
+    off += 64;
+    L.total = (off + 127) & ~127;
+    return L;
 }
 
 // ---------------------------------------------------------------- PTX helpers
@@ -88,8 +143,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ int ld_volatile(const int* p) { return *(const volatile int*)p; }
 
-// 4 bytes in {0,1} -> 4 bits (byte i -> bit i).  Terms of the product land on
-// distinct bit positions, so no carries ("u8 ingest").
+template <bool SUB>
+__device__ __forceinline__ void tsync(unsigned mask) {
+    if (SUB)
+        __syncwarp(mask);
+    else
+        __syncthreads();
+}
+
+// 4 bytes in {0,1} -> 4 bits (byte i -> bit i).  The partial products of
+// x * 0x01020408 land on distinct bit positions, so there are no carries.
 __device__ __forceinline__ uint32_t nib4(uint32_t x) { return ((x * 0x01020408u) >> 24) & 0xFu; }
 __device__ __forceinline__ uint32_t bits16(uint4 v) {
     return nib4(v.x) | (nib4(v.y) << 4) | (nib4(v.z) << 8) | (nib4(v.w) << 12);
@@ -109,18 +172,17 @@ __device__ __forceinline__ uint32_t windows_in_word(uint32_t x, int t) {
 
 __device__ __forceinline__ uint32_t enc_res(int b, int col) { return ((uint32_t)b << 20) | (uint32_t)col; }
 
-// eligibility of word x at tile row b at threshold t + m (P7 AND-history)
-__device__ __forceinline__ uint32_t e_at(const uint32_t* hist, int Wpad, int b, int m, int x) {
-    uint32_t v = hist[b * Wpad + x];
-    for (int q = 1; q <= m; ++q) v &= hist[(b - q) * Wpad + x];
+// X word at tile row b for threshold t+m: AND of rows b-m..b (P7)
+__device__ __forceinline__ uint32_t x_at(const uint32_t* hist, int stride, int b, int m, int x) {
+    uint32_t v = hist[b * stride + x];
+    for (int q = 1; q <= m; ++q) v &= hist[(b - q) * stride + x];
     return v;
 }
 
-// length of the run continuing rightwards from word y (full words then a prefix)
 __device__ __forceinline__ int run_right(const uint32_t* hist, int Wpad, int W, int b, int m, int y,
                                          int L, int t) {
     while (L < t && y < W) {
-        uint32_t nx = e_at(hist, Wpad, b, m, y);
+        const uint32_t nx = x_at(hist, Wpad, b, m, y);
         if (nx == 0xFFFFFFFFu) {
             L += 32;
             ++y;
@@ -132,35 +194,35 @@ __device__ __forceinline__ int run_right(const uint32_t* hist, int Wpad, int W, 
     return L;
 }
 
-// FULL test: every run that STARTS in word a (each maximal run is walked once)
+// E test, every run that STARTS in word a
 __device__ __forceinline__ void test_word_full(const uint32_t* hist, int Wpad, int W, int b, int m,
                                                int a, int t, uint32_t& best) {
-    uint32_t x = e_at(hist, Wpad, b, m, a);
+    const uint32_t x = x_at(hist, Wpad, b, m, a);
     if (x == 0) return;
     if (t <= 32) {
-        uint32_t y = windows_in_word(x, t);
+        const uint32_t y = windows_in_word(x, t);
         if (y) best = min(best, enc_res(b, 32 * a + __ffs(y) - 1));
     }
-    int s = __clz(~x);  // suffix run (from bit 31 down); 32 if full
+    const int s = __clz(~x);
     if (s == 0) return;
-    if (s == 32 && a > 0 && (e_at(hist, Wpad, b, m, a - 1) >> 31)) return;  // continuation
-    int L = run_right(hist, Wpad, W, b, m, a + 1, s, t);
+    if (s == 32 && a > 0 && (x_at(hist, Wpad, b, m, a - 1) >> 31)) return;  // continuation
+    const int L = run_right(hist, Wpad, W, b, m, a + 1, s, t);
     if (L >= t) best = min(best, enc_res(b, 32 * a + 32 - s));
 }
 
-// INCREMENTAL test: every run intersecting word a (a gained eligible bits)
+// E test, every run intersecting word a (a gained eligible bits this row)
 __device__ __forceinline__ void test_word_incr(const uint32_t* hist, int Wpad, int W, int b, int m,
                                                int a, int t, uint32_t& best) {
-    uint32_t x = e_at(hist, Wpad, b, m, a);
+    const uint32_t x = x_at(hist, Wpad, b, m, a);
     if (x == 0) return;
     if (t <= 32) {
-        uint32_t y = windows_in_word(x, t);
+        const uint32_t y = windows_in_word(x, t);
         if (y) best = min(best, enc_res(b, 32 * a + __ffs(y) - 1));
     }
-    if (x & 1u) {  // run through bit 0: find its start on the left
+    if (x & 1u) {
         int start = 32 * a;
         for (int y = a - 1; y >= 0; --y) {
-            uint32_t px = e_at(hist, Wpad, b, m, y);
+            const uint32_t px = x_at(hist, Wpad, b, m, y);
             if (px == 0xFFFFFFFFu) {
                 start -= 32;
             } else {
@@ -176,48 +238,91 @@ __device__ __forceinline__ void test_word_incr(const uint32_t* hist, int Wpad, i
         if (L >= t) best = min(best, enc_res(b, start));
     }
     if (x != 0xFFFFFFFFu) {
-        int s = __clz(~x);
+        const int s = __clz(~x);
         if (s > 0) {
-            int L = run_right(hist, Wpad, W, b, m, a + 1, s, t);
+            const int L = run_right(hist, Wpad, W, b, m, a + 1, s, t);
             if (L >= t) best = min(best, enc_res(b, 32 * a + 32 - s));
         }
     }
 }
 
+// F-bitmap scan of one bitmap word (32 words of the row) at tile row b,
+// threshold T = t+m.  A qualifying run = suffix(a) + 32*len + prefix(c) with
+// the full words a+1..c-1 = one maximal F run; boundary words are checked
+// exactly through `ex`.
+template <class Exact>
+__device__ __forceinline__ void scan_fword(const uint32_t* fm, int nfw, int W, int b, int m, int fw,
+                                           int T, const Exact& ex, uint32_t& best) {
+    const uint32_t x = x_at(fm, nfw, b, m, fw);
+    if (!x) return;
+    const uint32_t prev = fw > 0 ? (x_at(fm, nfw, b, m, fw - 1) >> 31) : 0u;
+    uint32_t starts = x & ~((x << 1) | prev);
+    const int nwords_f = (W + 31) / 32;
+    while (starts) {
+        const int i = __ffs(starts) - 1;
+        starts &= starts - 1;
+        const uint32_t rest = x >> i;
+        int len = (~rest == 0u) ? 32 : (__ffs(~rest) - 1);
+        if (i + len == 32) {
+            for (int y = fw + 1; y < nwords_f; ++y) {
+                const uint32_t nx = x_at(fm, nfw, b, m, y);
+                if (nx == 0xFFFFFFFFu) {
+                    len += 32;
+                } else {
+                    len += __ffs(~nx) - 1;
+                    break;
+                }
+            }
+        }
+        const int a0 = fw * 32 + i;  // first full word of the run
+        const int a = a0 - 1, c = a0 + len;
+        const int ub = 32 * len + (a >= 0 ? 31 : 0) + (c < W ? 32 : 0);
+        if (ub < T) continue;
+        const int suf = a >= 0 ? __clz(~ex.mask(a, b, T)) : 0;
+        int pre = 0;
+        if (c < W) {
+            const uint32_t mk = ex.mask(c, b, T);
+            pre = (mk == 0xFFFFFFFFu) ? 32 : __ffs(~mk) - 1;
+        }
+        if (suf + 32 * len + pre >= T) best = min(best, enc_res(b, 32 * a0 - suf));
+    }
+}
+
 // ------------------------------------------------------------------ params
 struct Pass1Params {
-    const uint8_t* src;         // matrix base (bytes)
-    long long ld_bytes;         // row stride in bytes
-    long long batch_stride;     // bytes between stacked matrices
-    int rows, cols, W, nbands;  // per matrix
-    int cols_pad;               // W * 32
-    long long row_base;         // global row of row 0 (row-band sharding)
-    int nstage;                 // TMA ring depth (tiles); 0 = direct loads
-    int rs;                     // row stage bytes (16-B multiple)
-    int row_bytes;              // bytes copied per row
-    int share;                  // cross-band threshold sharing
-    int write_summaries;        // e/b/allones outputs
+    const uint8_t* src;
+    long long ld_bytes;
+    long long batch_stride;
+    int rows, cols, W, nbands, cols_pad;
+    long long row_base;
+    int nstage, rs, row_bytes;  // TMA ring: one row per stage
+    int bs, bl;                 // rows per tile in mode S / mode L
+    int tl;                     // mode L threshold
+    int share, write_summaries;
+    int team;                   // threads per team
+    int units;                  // nbands * batch
+    int layout_bytes;           // per-team smem bytes
     uint16_t* e_out;
     uint16_t* b_out;
     uint32_t* ao_out;
-    unsigned long long* band_keys;  // [batch][nbands]
-    unsigned char* results;         // msq_devresult blocks (32 B each)
+    unsigned long long* band_keys;
+    unsigned char* results;
 };
 
 struct FixParams {
     int rows, cols, W, nbands, cols_pad;
     long long row_base;
-    int band_begin;             // first band fixed by this launch
+    int band_begin;
+    int bs, bl;
     const uint16_t* e_in;
     const uint16_t* b_in;
     const uint32_t* ao_in;
-    const uint32_t* base_carry;  // carry into band 0 (row-band sharding) or null
+    const uint32_t* base_carry;
     int share;
-    unsigned long long* fix_keys;  // [nbands]
+    unsigned long long* fix_keys;
     unsigned char* results;
 };
 
-// msq_devresult field access (layout fixed in msq.h)
 __device__ __forceinline__ unsigned long long* res_key1(unsigned char* r) {
     return (unsigned long long*)(r + 0);
 }
@@ -229,59 +334,217 @@ __device__ __forceinline__ int* res_best(unsigned char* r) { return (int*)(r + 2
 
 struct Misc {
     uint32_t res[3];
-    int g;      // polled shared best side
-    int flag;
-    int pad[3];
+    int g;
+    int pad[12];
+};
+
+// bit-sliced saturating increment (reset on zero): planes h[0..P-1]
+template <int P>
+__device__ __forceinline__ void planes_step(uint32_t (&h)[P], uint32_t w) {
+    uint32_t c = w;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        const uint32_t tmp = h[p] & c;
+        h[p] ^= c;
+        c = tmp;
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) h[p] = (h[p] | c) & w;
+}
+
+// bit-sliced compare h >= t for a warp-uniform t in [0, 2^P)
+template <int P>
+__device__ __forceinline__ uint32_t planes_ge(const uint32_t (&h)[P], int t) {
+    uint32_t ge = 0, eq = 0xFFFFFFFFu;
+#pragma unroll
+    for (int p = P - 1; p >= 0; --p) {
+        if ((t >> p) & 1)
+            eq &= h[p];
+        else
+            ge |= eq & h[p];
+    }
+    return ge | eq;
+}
+
+__device__ __forceinline__ uint32_t valid_mask(int a, int W, int cols) {
+    if (a >= W) return 0u;
+    const int rem = cols - 32 * a;
+    return rem >= 32 ? 0xFFFFFFFFu : ((1u << rem) - 1u);
+}
+
+// row words for the thread's WPT words from a staged row (TMA) or global
+template <int WPT, bool U8, bool TMA>
+__device__ __forceinline__ void fetch_words(const uint8_t* stage_row, const uint8_t* grow, int tau, int W,
+                                            int cols, int rs, const uint32_t (&VAL)[WPT], uint32_t (&w)[WPT],
+                                            uint32_t& bad_or) {
+    if (U8) {
+#pragma unroll
+        for (int k = 0; k < WPT; ++k) {
+            const int a = tau * WPT + k;
+            uint32_t word = 0;
+            if (a < W) {
+                if (TMA) {
+                    const uint8_t* rp = stage_row + (size_t)a * 32;
+                    const uint4 v0 = *(const uint4*)rp;
+                    uint4 v1 = make_uint4(0, 0, 0, 0);
+                    if (a * 32 + 16 < rs) v1 = *(const uint4*)(rp + 16);
+                    bad_or |= v0.x | v0.y | v0.z | v0.w | v1.x | v1.y | v1.z | v1.w;
+                    word = bits16(v0) | (bits16(v1) << 16);
+                } else {
+                    const int c0 = 32 * a;
+                    const int n = min(32, cols - c0);
+                    for (int j = 0; j < n; ++j) {
+                        const uint32_t cb = grow[c0 + j];
+                        bad_or |= cb;
+                        word |= (cb & 1u) << j;
+                    }
+                }
+            }
+            w[k] = word & VAL[k];
+        }
+    } else {
+        if (TMA) {
+            const uint32_t* rp = (const uint32_t*)stage_row + tau * WPT;
+            if (tau * WPT < W) {
+                if (WPT == 4) {
+                    const uint4 v = *(const uint4*)rp;
+                    w[0] = v.x;
+                    w[1 % WPT] = v.y;
+                    w[2 % WPT] = v.z;
+                    w[3 % WPT] = v.w;
+                } else if (WPT == 2) {
+                    const uint2 v = *(const uint2*)rp;
+                    w[0] = v.x;
+                    w[1 % WPT] = v.y;
+                } else {
+                    w[0] = rp[0];
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < WPT; ++k) w[k] = 0;
+            }
+        } else {
+            const uint32_t* rp = (const uint32_t*)grow;
+#pragma unroll
+            for (int k = 0; k < WPT; ++k) {
+                const int a = tau * WPT + k;
+                w[k] = a < W ? rp[a] : 0u;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < WPT; ++k) w[k] &= VAL[k];
+    }
+}
+
+// one word of one staged/global row (any owner), for phase C / exact checks
+template <bool U8, bool TMA>
+__device__ __forceinline__ uint32_t word_of_row(const uint8_t* stage_row, const uint8_t* grow, int a,
+                                                int cols, int rs) {
+    if (U8) {
+        uint32_t word = 0;
+        if (TMA) {
+            const uint8_t* rp = stage_row + (size_t)a * 32;
+            const uint4 v0 = *(const uint4*)rp;
+            uint4 v1 = make_uint4(0, 0, 0, 0);
+            if (a * 32 + 16 < rs) v1 = *(const uint4*)(rp + 16);
+            word = bits16(v0) | (bits16(v1) << 16);
+        } else {
+            const int c0 = 32 * a;
+            const int n = min(32, cols - c0);
+            for (int j = 0; j < n; ++j) word |= ((uint32_t)grow[c0 + j] & 1u) << j;
+        }
+        return word;
+    }
+    if (TMA) return ((const uint32_t*)stage_row)[a];
+    return ((const uint32_t*)grow)[a];
+}
+
+// exact eligibility of a word inside a pass-1 tile (mode L boundary check)
+template <bool U8, bool TMA>
+struct Pass1Exact {
+    const uint16_t* zs;
+    const uint16_t* za;
+    const uint8_t* ring;
+    const uint8_t* mbase;
+    long long ld_bytes;
+    int NT, WPT, W, cols, rs, nstage;
+    int tile_row0;  // band-relative 0-based row of tile row 0
+    int r0;         // band top row (matrix)
+    __device__ __forceinline__ const uint8_t* srow(int b) const {
+        return TMA ? ring + (size_t)((tile_row0 + b) % nstage) * rs : nullptr;
+    }
+    __device__ __forceinline__ const uint8_t* grow(int b) const {
+        return mbase + (size_t)(r0 + tile_row0 + b) * ld_bytes;
+    }
+    __device__ uint32_t mask(int a, int b, int T) const {
+        const uint32_t val = valid_mask(a, W, cols);
+        const int rho_b = tile_row0 + b + 1;
+        const int lim = rho_b - T;  // last zero must be <= lim (T > BMAX: any zero in the tile kills)
+        if ((int)za[a] > lim) return 0u;
+        uint32_t zin = 0;
+        for (int q = 0; q <= b; ++q) zin |= ~word_of_row<U8, TMA>(srow(q), grow(q), a, cols, rs);
+        uint32_t cand = val & ~zin, m = 0;
+        const int tau = a / WPT, k = a - tau * WPT;
+        while (cand) {
+            const int j = __ffs(cand) - 1;
+            cand &= cand - 1;
+            if ((int)zs[(k * 32 + j) * NT + tau] <= lim) m |= 1u << j;
+        }
+        return m;
+    }
 };
 
 // ============================================================= pass 1 kernel
-// One CTA = one band of one matrix.  Thread tau owns words [tau*WPT, tau*WPT+WPT).
-template <int WPT, int B, bool U8, bool TMA>
+template <int WPT, bool U8, bool TMA, bool SUB>
 __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     extern __shared__ __align__(128) uint8_t smem[];
-    const int NT = blockDim.x;
-    const int tau = threadIdx.x;
-    const int band = (int)(blockIdx.x % (unsigned)p.nbands);
-    const int mat = (int)(blockIdx.x / (unsigned)p.nbands);
+    const int NT = p.team;
+    const int tid = threadIdx.x;
+    const int team_idx = SUB ? tid / NT : 0;
+    const int tau = SUB ? tid - team_idx * NT : tid;
+    const unsigned tmask =
+        SUB ? (unsigned)((NT >= 32 ? 0xFFFFFFFFull : ((1ull << NT) - 1ull)) << ((tid & 31) - tau)) : 0xFFFFFFFFu;
+    const int teams_per_cta = SUB ? (int)blockDim.x / NT : 1;
+    const int unit = blockIdx.x * teams_per_cta + team_idx;
+    if (unit >= p.units) return;  // whole idle team (sub-warp teams only)
+    const int band = unit % p.nbands;
+    const int mat = unit / p.nbands;
     const int W = p.W;
     const int Wpad = NT * WPT;
+    const int nfw = (Wpad + 31) / 32;
+    const int fstride = r16(nfw * 4) / 4;
     const int r0 = band_row0(p.rows, p.nbands, band);
     const int H = band_row0(p.rows, p.nbands, band + 1) - r0;
     unsigned char* result = p.results + (size_t)mat * 32;
 
-    // ---- shared memory carve-up (must match host plan)
-    size_t off = 0;
-    uint8_t* ring = smem + off;
-    if (TMA) off += (size_t)p.nstage * B * p.rs;
-    uint64_t* bars = (uint64_t*)(smem + off);
-    if (TMA) off += ((size_t)p.nstage * 8 + 15) / 16 * 16;
-    uint16_t* zs = (uint16_t*)(smem + off);
-    off += (size_t)Wpad * 32 * 2;
-    uint32_t* hist = (uint32_t*)(smem + off);
-    off += (size_t)B * Wpad * 4;
-    Misc* misc = (Misc*)(smem + off);
+    const P1Layout Lo = p1_layout(NT, WPT, p.nstage, p.rs, p.bs, TMA);
+    uint8_t* tsm = smem + (size_t)team_idx * p.layout_bytes;
+    uint8_t* ring = tsm + Lo.ring;
+    uint64_t* bars = (uint64_t*)(tsm + Lo.bars);
+    uint16_t* zs = (uint16_t*)(tsm + Lo.zs);
+    uint16_t* za = (uint16_t*)(tsm + Lo.za);
+    uint32_t* hist = (uint32_t*)(tsm + Lo.hist);
+    uint32_t* fmap = (uint32_t*)(tsm + Lo.fmap);
+    Misc* misc = (Misc*)(tsm + Lo.misc);
 
     const uint8_t* mbase = p.src + (size_t)mat * p.batch_stride;
     const size_t sum_base = (size_t)band * p.cols_pad;
 
-    // ---- per-thread word state
-    uint32_t E[WPT], NZ[WPT], VAL[WPT];
-    int ZA[WPT], TRIG[WPT];
+    uint32_t VAL[WPT], NZ[WPT], EPREV[WPT];
+    uint32_t HC[WPT][NPLANES];
+    int ZW[WPT];
 #pragma unroll
     for (int k = 0; k < WPT; ++k) {
-        const int a = tau * WPT + k;
-        uint32_t v = 0;
-        if (a < W) {
-            const int rem = p.cols - 32 * a;
-            v = rem >= 32 ? 0xFFFFFFFFu : ((1u << rem) - 1u);
-        }
-        VAL[k] = v;
-        E[k] = 0;
-        NZ[k] = v;
-        ZA[k] = 0;
-        TRIG[k] = v ? 0 : TRIG_INF;
+        VAL[k] = valid_mask(tau * WPT + k, W, p.cols);
+        NZ[k] = VAL[k];
+        EPREV[k] = 0;
+        ZW[k] = 0;
+#pragma unroll
+        for (int q = 0; q < NPLANES; ++q) HC[k][q] = 0;
     }
     for (int i = tau; i < Wpad * 16; i += NT) ((uint32_t*)zs)[i] = 0u;
+    for (int i = tau; i < Wpad; i += NT) za[i] = 0;
+    for (int i = tau; i < 2 * BMAX * fstride; i += NT) fmap[i] = 0u;
     if (tau == 0) {
         misc->res[0] = misc->res[1] = misc->res[2] = RES_INF;
         misc->g = p.share ? ld_volatile(res_best(result)) : 0;
@@ -290,17 +553,15 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
             fence_mbar_init();
         }
     }
-    __syncthreads();
+    tsync<SUB>(tmask);
 
-    const int ntiles = (H + B - 1) / B;
+    int issued = 0;  // next band row to stage (meaningful in the producer thread)
     if (TMA && tau == 0) {
-        for (int tl = 0; tl < p.nstage && tl < ntiles; ++tl) {
-            const int nr = min(B, H - tl * B);
-            uint8_t* dst = ring + (size_t)(tl % p.nstage) * B * p.rs;
-            mbar_expect_tx(&bars[tl % p.nstage], (uint32_t)(nr * p.row_bytes));
-            for (int b = 0; b < nr; ++b)
-                tma_row(dst + (size_t)b * p.rs, mbase + (size_t)(r0 + tl * B + b) * p.ld_bytes,
-                        (uint32_t)p.row_bytes, &bars[tl % p.nstage]);
+        for (; issued < min(p.nstage, H); ++issued) {
+            const int s = issued % p.nstage;
+            mbar_expect_tx(&bars[s], (uint32_t)p.row_bytes);
+            tma_row(ring + (size_t)s * p.rs, mbase + (size_t)(r0 + issued) * p.ld_bytes, (uint32_t)p.row_bytes,
+                    &bars[s]);
         }
     }
 
@@ -308,535 +569,79 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     bool full_next = false;
     unsigned long long bandkey = 0ull;
     int round_ctr = 0;
-    uint32_t bad_or = 0;  // u8 validation accumulator
+    uint32_t bad_or = 0;
+    int tile = 0;
 
-    for (int tile = 0; tile < ntiles; ++tile) {
-        const int rho0 = tile * B + 1;
-        const uint8_t* stage = nullptr;
-        if (TMA) {
-            const int s = tile % p.nstage;
-            mbar_wait(&bars[s], (uint32_t)((tile / p.nstage) & 1));
-            stage = ring + (size_t)s * B * p.rs;
-        }
+    for (int row0 = 0; row0 < H; ++tile) {
+        const bool modeL = t >= p.tl;
+        const int nrows = min(modeL ? p.bl : p.bs, H - row0);
+        uint32_t* fm = fmap + (tile & 1) * BMAX * fstride;
         int polled = 0;
         if (p.share && tau == 0 && (tile & 7) == 7) polled = ld_volatile(res_best(result));
 
-        uint32_t dirty = 0;
+        // ---------------------------------------------------- phase A
+        uint32_t dirty = 0, zflag = 0;
 #pragma unroll
-        for (int b = 0; b < B; ++b) {
-            const int rho = rho0 + b;
-            uint32_t w[WPT];
-            if (rho <= H) {
-                // ------------------------------------------------ fetch row words
-                if (U8) {
-#pragma unroll
-                    for (int k = 0; k < WPT; ++k) {
-                        const int a = tau * WPT + k;
-                        uint32_t word = 0;
-                        if (a < W) {
-                            if (TMA) {
-                                const uint8_t* rp = stage + (size_t)b * p.rs + (size_t)a * 32;
-                                uint4 v0 = *(const uint4*)rp;
-                                uint4 v1 = make_uint4(0, 0, 0, 0);
-                                if (a * 32 + 16 < p.rs) v1 = *(const uint4*)(rp + 16);
-                                bad_or |= v0.x | v0.y | v0.z | v0.w | v1.x | v1.y | v1.z | v1.w;
-                                word = bits16(v0) | (bits16(v1) << 16);
-                            } else {
-                                const uint8_t* rp = mbase + (size_t)(r0 + rho - 1) * p.ld_bytes;
-                                const int c0 = 32 * a;
-                                const int n = min(32, p.cols - c0);
-                                for (int j = 0; j < n; ++j) {
-                                    uint32_t cb = rp[c0 + j];
-                                    bad_or |= cb;
-                                    word |= (cb & 1u) << j;
-                                }
-                            }
-                        }
-                        w[k] = word & VAL[k];
-                    }
-                } else {
-                    if (TMA) {
-                        const uint32_t* rp = (const uint32_t*)(stage + (size_t)b * p.rs) + tau * WPT;
-                        if (tau * WPT < W) {
-                            if (WPT == 4) {
-                                uint4 v = *(const uint4*)rp;
-                                w[0] = v.x;
-                                if (WPT > 1) w[1 % WPT] = v.y;
-                                if (WPT > 2) w[2 % WPT] = v.z;
-                                if (WPT > 3) w[3 % WPT] = v.w;
-                            } else if (WPT == 2) {
-                                uint2 v = *(const uint2*)rp;
-                                w[0] = v.x;
-                                w[1 % WPT] = v.y;
-                            } else {
-                                w[0] = rp[0];
-                            }
-                        } else {
-#pragma unroll
-                            for (int k = 0; k < WPT; ++k) w[k] = 0;
-                        }
-                    } else {
-                        const uint32_t* rp =
-                            (const uint32_t*)(mbase + (size_t)(r0 + rho - 1) * p.ld_bytes);
-#pragma unroll
-                        for (int k = 0; k < WPT; ++k) {
-                            const int a = tau * WPT + k;
-                            w[k] = a < W ? rp[a] : 0u;
-                        }
-                    }
-#pragma unroll
-                    for (int k = 0; k < WPT; ++k) w[k] &= VAL[k];
+        for (int b = 0; b < BMAX; ++b) {
+            if (b < nrows) {
+                const int r = row0 + b;
+                const int rho = r + 1;
+                const uint8_t* srow = nullptr;
+                if (TMA) {
+                    mbar_wait(&bars[r % p.nstage], (uint32_t)((r / p.nstage) & 1));
+                    srow = ring + (size_t)(r % p.nstage) * p.rs;
                 }
-                // ------------------------------------------------ update state
+                uint32_t w[WPT];
+                fetch_words<WPT, U8, TMA>(srow, mbase + (size_t)(r0 + r) * p.ld_bytes, tau, W, p.cols, p.rs,
+                                          VAL, w, bad_or);
+                uint32_t fnib = 0;
 #pragma unroll
                 for (int k = 0; k < WPT; ++k) {
-                    const uint32_t zeros = VAL[k] & ~w[k];
-                    if (zeros) {
-                        if (zeros == VAL[k]) {
-                            ZA[k] = rho;  // whole word zero: lazy last-zero row
-                        } else {
-                            uint32_t zz = zeros;
-                            while (zz) {
-                                const int bit = __ffs(zz) - 1;
-                                zz &= zz - 1;
-                                zs[(k * 32 + bit) * NT + tau] = (uint16_t)rho;
-                            }
-                        }
-                        uint32_t newly = NZ[k] & zeros;
-                        if (newly && p.write_summaries) {
-                            const size_t cb = sum_base + (size_t)(tau * WPT + k) * 32;
-                            while (newly) {
-                                const int bit = __ffs(newly) - 1;
-                                newly &= newly - 1;
-                                p.e_out[cb + bit] = (uint16_t)(rho - 1);
-                            }
-                        }
-                        NZ[k] &= ~zeros;
-                        E[k] &= ~zeros;
-                        TRIG[k] = min(TRIG[k], rho);
-                    }
-                    if (rho >= TRIG[k] + t) {  // a column may have reached height t
-                        uint32_t cand = VAL[k] & ~E[k] & w[k];
-                        int nt = zeros ? rho : TRIG_INF;
-                        uint32_t added = 0;
-                        while (cand) {
-                            const int bit = __ffs(cand) - 1;
-                            cand &= cand - 1;
-                            const int u = max((int)zs[(k * 32 + bit) * NT + tau], ZA[k]);
-                            if (u + t <= rho)
-                                added |= 1u << bit;
-                            else
-                                nt = min(nt, u);
-                        }
-                        E[k] |= added;
-                        TRIG[k] = nt;
-                        if (added) dirty |= 1u << (b * WPT + k);
+                    const bool z = w[k] != VAL[k];
+                    ZW[k] = z ? rho : ZW[k];
+                    zflag |= (z ? 1u : 0u) << (b * WPT + k);
+                    if (modeL) {
+                        fnib |= ((VAL[k] == 0xFFFFFFFFu && ZW[k] <= rho - t) ? 1u : 0u) << k;
+                    } else {
+                        planes_step<NPLANES>(HC[k], w[k]);
+                        const uint32_t e = planes_ge<NPLANES>(HC[k], t) & VAL[k];
+                        if (e & ~EPREV[k]) dirty |= 1u << (b * WPT + k);
+                        EPREV[k] = e;
+                        hist[b * Wpad + tau * WPT + k] = e;
                     }
                 }
-            } else {
-#pragma unroll
-                for (int k = 0; k < WPT; ++k) w[k] = 0;
-            }
-            // ------------------------------------------------ E history
-            if (WPT == 4) {
-                *(uint4*)(hist + b * Wpad + tau * 4) = rho <= H ? make_uint4(E[0], E[1 % WPT], E[2 % WPT], E[3 % WPT])
-                                                                : make_uint4(0, 0, 0, 0);
-            } else if (WPT == 2) {
-                *(uint2*)(hist + b * Wpad + tau * 2) = rho <= H ? make_uint2(E[0], E[1 % WPT]) : make_uint2(0, 0);
-            } else {
-                hist[b * Wpad + tau] = rho <= H ? E[0] : 0u;
+                if (modeL && fnib) {
+                    const int a0 = tau * WPT;
+                    atomicOr(&fm[b * fstride + (a0 >> 5)], fnib << (a0 & 31));
+                }
             }
         }
         if (tau == 0 && (tile & 7) == 7) misc->g = polled;
-        __syncthreads();  // (A) E history complete; stage consumed
-
-        if (TMA && tau == 0) {
-            const int tl = tile + p.nstage;
-            if (tl < ntiles) {
-                const int s = tl % p.nstage;
-                const int nr = min(B, H - tl * B);
-                uint8_t* dst = ring + (size_t)s * B * p.rs;
-                mbar_expect_tx(&bars[s], (uint32_t)(nr * p.row_bytes));
-                for (int b = 0; b < nr; ++b)
-                    tma_row(dst + (size_t)b * p.rs, mbase + (size_t)(r0 + tl * B + b) * p.ld_bytes,
-                            (uint32_t)p.row_bytes, &bars[s]);
+        tsync<SUB>(tmask);  // (A)
+        if (TMA && tau == 0) {  // stages of the previous tile are free now
+            const int upto = min(row0 + p.nstage, H);
+            for (; issued < upto; ++issued) {
+                const int s = issued % p.nstage;
+                mbar_expect_tx(&bars[s], (uint32_t)p.row_bytes);
+                tma_row(ring + (size_t)s * p.rs, mbase + (size_t)(r0 + issued) * p.ld_bytes,
+                        (uint32_t)p.row_bytes, &bars[s]);
             }
         }
 
-        // ---------------------------------------------------- test rounds
-        const int lastb = min(B - 1, H - rho0);
-        int cur_t = t, start_b = 0, full_from = full_next ? 0 : B, last_raise = -1;
+        // ---------------------------------------------------- phase B
+        const int lastb = nrows - 1;
+        int cur_t = t, start_b = 0, full_from = full_next ? 0 : BMAX;
+        const Pass1Exact<U8, TMA> ex{zs, za, ring, mbase, p.ld_bytes, NT, WPT, W, p.cols, p.rs, p.nstage, row0, r0};
         for (;;) {
             uint32_t best = RES_INF;
             const int m = cur_t - t;
-            for (int b = start_b; b <= lastb; ++b) {
-                const bool full = b >= full_from;
-#pragma unroll
-                for (int k = 0; k < WPT; ++k) {
-                    const int a = tau * WPT + k;
-                    if (a < W) {
-                        if (full)
-                            test_word_full(hist, Wpad, W, b, m, a, cur_t, best);
-                        else if ((dirty >> (b * WPT + k)) & 1u)
-                            test_word_incr(hist, Wpad, W, b, m, a, cur_t, best);
-                    }
+            if (modeL) {
+                const int n = (lastb - start_b + 1) * nfw;
+                for (int idx = tau; idx < n; idx += NT) {
+                    const int b = start_b + idx / nfw, fw = idx % nfw;
+                    scan_fword(fm, fstride, W, b, m, fw, cur_t, ex, best);
                 }
-            }
-            const int slot = round_ctr % 3;
-            if (best != RES_INF) atomicMin(&misc->res[slot], best);
-            if (tau == 0) misc->res[(round_ctr + 1) % 3] = RES_INF;
-            __syncthreads();  // (B)
-            const uint32_t r = misc->res[slot];
-            ++round_ctr;
-            if (r == RES_INF) break;
-            const int bs = (int)(r >> 20), col = (int)(r & 0xFFFFFu);
-            if (tau == 0) {
-                bandkey = pack_key(cur_t, p.row_base + r0 + rho0 + bs - 1, col + cur_t - 1);
-                if (p.share) atomicMax(res_best(result), cur_t);
-            }
-            last_raise = bs;
-            ++cur_t;
-            start_b = bs + 1;
-            full_from = bs + 1;
-            if (start_b > lastb) break;
-        }
-        // ---------------------------------------------------- state correction
-        const int nraise = cur_t - t;
-        const int meff = nraise - (last_raise == lastb ? 1 : 0);
-        const int rho_last = rho0 + lastb;
-        if (meff > 0) {
-#pragma unroll
-            for (int k = 0; k < WPT; ++k) {
-                const int a = tau * WPT + k;
-                if (a < W) {
-                    const uint32_t en = e_at(hist, Wpad, lastb, meff, a);
-                    const uint32_t removed = E[k] & ~en;
-                    E[k] = en;
-                    if (removed) TRIG[k] = min(TRIG[k], rho_last - t - meff + 1);
-                }
-            }
-        }
-        full_next = nraise > 0 && last_raise == lastb;
-        t = cur_t;
-        // ---------------------------------------------------- shared best jump
-        if (p.share) {
-            const int g = misc->g;
-            if (g > t) {
-#pragma unroll
-                for (int k = 0; k < WPT; ++k) {
-                    uint32_t ee = E[k];
-                    while (ee) {
-                        const int bit = __ffs(ee) - 1;
-                        ee &= ee - 1;
-                        const int u = max((int)zs[(k * 32 + bit) * NT + tau], ZA[k]);
-                        if (u + g > rho_last) {
-                            E[k] &= ~(1u << bit);
-                            TRIG[k] = min(TRIG[k], u);
-                        }
-                    }
-                }
-                t = g;
-            }
-        }
-    }
-
-    // ---------------------------------------------------------- band outputs
-    if (p.write_summaries) {
-#pragma unroll
-        for (int k = 0; k < WPT; ++k) {
-            const int a = tau * WPT + k;
-            if (a < W) {
-                const size_t cb = sum_base + (size_t)a * 32;
-                uint32_t nz = NZ[k];
-                while (nz) {
-                    const int bit = __ffs(nz) - 1;
-                    nz &= nz - 1;
-                    p.e_out[cb + bit] = (uint16_t)H;
-                }
-                uint16_t bb[32];
-#pragma unroll
-                for (int bit = 0; bit < 32; ++bit) {
-                    const int u = max((int)zs[(k * 32 + bit) * NT + tau], ZA[k]);
-                    bb[bit] = (uint16_t)(H - u);
-                }
-                uint4* dst = (uint4*)(p.b_out + cb);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    uint4 v;
-                    v.x = (uint32_t)bb[8 * q + 0] | ((uint32_t)bb[8 * q + 1] << 16);
-                    v.y = (uint32_t)bb[8 * q + 2] | ((uint32_t)bb[8 * q + 3] << 16);
-                    v.z = (uint32_t)bb[8 * q + 4] | ((uint32_t)bb[8 * q + 5] << 16);
-                    v.w = (uint32_t)bb[8 * q + 6] | ((uint32_t)bb[8 * q + 7] << 16);
-                    dst[q] = v;
-                }
-                p.ao_out[(size_t)band * W + a] = NZ[k];
-            }
-        }
-    }
-    if (U8 && (bad_or & 0xFEFEFEFEu)) atomicOr(res_status(result), 1u);
-    if (tau == 0) {
-        if (p.band_keys) p.band_keys[(size_t)mat * p.nbands + band] = bandkey;
-        if (bandkey) atomicMax(res_key1(result), bandkey);
-    }
-}
-
-// ============================================================ fix-up kernel
-// Data-free: virtual rows d = 1..min(H, t-1) of band `band`, height of column j
-// at depth d is c_j + d while d <= e_j (leading ones of the band top), else 0.
-template <int WPT, int B>
-__global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    const int NT = blockDim.x;
-    const int tau = threadIdx.x;
-    const int band = p.band_begin + blockIdx.x;
-    const int W = p.W;
-    const int Wpad = NT * WPT;
-    const int r0 = band_row0(p.rows, p.nbands, band);
-    const int H = band_row0(p.rows, p.nbands, band + 1) - r0;
-    unsigned char* result = p.results;
-
-    size_t off = 0;
-    uint16_t* us = (uint16_t*)(smem + off);
-    off += (size_t)Wpad * 32 * 2;
-    uint8_t* e8 = smem + off;
-    off += (size_t)Wpad * 32;
-    uint32_t* hist = (uint32_t*)(smem + off);
-    off += (size_t)B * Wpad * 4;
-    Misc* misc = (Misc*)(smem + off);
-
-    // starting threshold: best side known after the band passes
-    if (tau == 0) {
-        misc->res[0] = misc->res[1] = misc->res[2] = RES_INF;
-        int g = (int)(*(volatile unsigned long long*)res_key1(result) >> (2 * KEY_DIM_BITS));
-        if (p.share) g = max(g, ld_volatile(res_best(result)));
-        misc->g = g;
-    }
-
-    uint32_t E[WPT], ALIVE[WPT], VAL[WPT];
-    int TRIG[WPT], ND[WPT];
-    const size_t eb = (size_t)band * p.cols_pad;
-#pragma unroll
-    for (int k = 0; k < WPT; ++k) {
-        const int a = tau * WPT + k;
-        uint32_t v = 0;
-        if (a < W) {
-            const int rem = p.cols - 32 * a;
-            v = rem >= 32 ? 0xFFFFFFFFu : ((1u << rem) - 1u);
-        }
-        VAL[k] = v;
-        ALIVE[k] = 0;
-        ND[k] = TRIG_INF;
-        if (!v) continue;
-        // ---- carry-in heights by look-back over the bands above (P5)
-        uint32_t pending = v;
-        long long acc = 0;
-        for (int q = band - 1; q >= 0 && pending; --q) {
-            const uint32_t m = p.ao_in[(size_t)q * W + a];
-            uint32_t res = pending & ~m;
-            while (res) {
-                const int bit = __ffs(res) - 1;
-                res &= res - 1;
-                const long long c = acc + p.b_in[(size_t)q * p.cols_pad + 32 * a + bit];
-                us[(k * 32 + bit) * NT + tau] = (uint16_t)(OFF_FIX - (int)min(c, (long long)OFF_FIX));
-            }
-            pending &= m;
-            acc += band_row0(p.rows, p.nbands, q + 1) - band_row0(p.rows, p.nbands, q);
-        }
-        while (pending) {
-            const int bit = __ffs(pending) - 1;
-            pending &= pending - 1;
-            const long long c = acc + (p.base_carry ? (long long)p.base_carry[32 * a + bit] : 0ll);
-            us[(k * 32 + bit) * NT + tau] = (uint16_t)(OFF_FIX - (int)min(c, (long long)OFF_FIX));
-        }
-        // ---- leading-ones depth of the band top
-        const uint4* ep = (const uint4*)(p.e_in + eb + (size_t)32 * a);
-        uint32_t alive = 0;
-        int nd = TRIG_INF;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint4 v4 = ep[q];
-            const uint32_t pr[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-#pragma unroll
-                for (int s = 0; s < 2; ++s) {
-                    const int bit = 8 * q + 2 * h + s;
-                    const int e = (int)((pr[h] >> (16 * s)) & 0xFFFFu);
-                    e8[(k * 32 + bit) * NT + tau] = (uint8_t)min(e, 255);
-                    if (((v >> bit) & 1u) && e >= 1) {
-                        alive |= 1u << bit;
-                        nd = min(nd, e + 1);
-                    }
-                }
-            }
-        }
-        ALIVE[k] = alive;
-        ND[k] = nd;
-    }
-    __syncthreads();
-    int t = max(1, misc->g);
-
-    // eligibility of word k at depth d, threshold tt; also returns TRIG
-    auto eval_word = [&](int k, int d, int tt, uint32_t& e_out, int& trig_out) {
-        uint32_t al = ALIVE[k], e = 0;
-        int tr = TRIG_INF;
-        while (al) {
-            const int bit = __ffs(al) - 1;
-            al &= al - 1;
-            const int u = us[(k * 32 + bit) * NT + tau];
-            if (u + tt <= d + OFF_FIX)
-                e |= 1u << bit;
-            else
-                tr = min(tr, u);
-        }
-        e_out = e;
-        trig_out = tr;
-    };
-    auto store_hist0 = [&](const uint32_t* ev) {
-#pragma unroll
-        for (int k = 0; k < WPT; ++k) hist[tau * WPT + k] = ev[k];
-    };
-    int round_ctr = 0;
-    // full test of tile row 0 at threshold tt; returns packed result or RES_INF
-    auto full_test_row0 = [&](int tt) -> uint32_t {
-        uint32_t best = RES_INF;
-#pragma unroll
-        for (int k = 0; k < WPT; ++k) {
-            const int a = tau * WPT + k;
-            if (a < W) test_word_full(hist, Wpad, W, 0, 0, a, tt, best);
-        }
-        const int slot = round_ctr % 3;
-        if (best != RES_INF) atomicMin(&misc->res[slot], best);
-        if (tau == 0) misc->res[(round_ctr + 1) % 3] = RES_INF;
-        __syncthreads();
-        const uint32_t r = misc->res[slot];
-        ++round_ctr;
-        return r;
-    };
-
-    unsigned long long fixkey = 0ull;
-    if (H >= 1) {
-        // ---------------------------------------------- depth 1, exact seeding
-#pragma unroll
-        for (int k = 0; k < WPT; ++k) eval_word(k, 1, t, E[k], TRIG[k]);
-        store_hist0(E);
-        __syncthreads();
-        uint32_t r = full_test_row0(t);
-        if (r != RES_INF) {
-            // P3: the window test is monotone in k -> exponential + binary search
-            int lo = t, hi = -1;
-            uint32_t rlo = r;
-            int step = 1;
-            while (hi < 0) {
-                const int kk = lo + step;
-                if (kk > p.cols) {
-                    hi = kk;
-                    break;
-                }
-                uint32_t ev[WPT];
-                int dummy;
-#pragma unroll
-                for (int k = 0; k < WPT; ++k) eval_word(k, 1, kk, ev[k], dummy);
-                __syncthreads();
-                store_hist0(ev);
-                __syncthreads();
-                const uint32_t rk = full_test_row0(kk);
-                if (rk != RES_INF) {
-                    lo = kk;
-                    rlo = rk;
-                    step *= 2;
-                } else {
-                    hi = kk;
-                }
-            }
-            while (hi - lo > 1) {
-                const int mid = lo + (hi - lo) / 2;
-                uint32_t ev[WPT];
-                int dummy;
-#pragma unroll
-                for (int k = 0; k < WPT; ++k) eval_word(k, 1, mid, ev[k], dummy);
-                __syncthreads();
-                store_hist0(ev);
-                __syncthreads();
-                const uint32_t rk = full_test_row0(mid);
-                if (rk != RES_INF) {
-                    lo = mid;
-                    rlo = rk;
-                } else {
-                    hi = mid;
-                }
-            }
-            if (tau == 0) {
-                fixkey = pack_key(lo, p.row_base + r0, (int)(rlo & 0xFFFFFu) + lo - 1);
-                if (p.share) atomicMax(res_best(result), lo);
-            }
-            t = lo + 1;
-#pragma unroll
-            for (int k = 0; k < WPT; ++k) eval_word(k, 1, t, E[k], TRIG[k]);
-        }
-        __syncthreads();
-
-        // ---------------------------------------------- depths 2.. (tiles of B)
-        bool full_next = false;
-        int tile = 0;
-        for (int d0 = 2; d0 <= H && d0 < t; d0 += B, ++tile) {
-            int polled = 0;
-            if (p.share && tau == 0 && (tile & 7) == 7) polled = ld_volatile(res_best(result));
-            uint32_t dirty = 0;
-#pragma unroll
-            for (int b = 0; b < B; ++b) {
-                const int d = d0 + b;
-                if (d <= H) {
-#pragma unroll
-                    for (int k = 0; k < WPT; ++k) {
-                        if (d >= ND[k]) {  // deaths: leading run of the band top ended
-                            uint32_t al = ALIVE[k];
-                            int nd = TRIG_INF;
-                            while (al) {
-                                const int bit = __ffs(al) - 1;
-                                al &= al - 1;
-                                int e = e8[(k * 32 + bit) * NT + tau];
-                                if (e == 255 && d >= 256)
-                                    e = p.e_in[eb + (size_t)32 * (tau * WPT + k) + bit];
-                                if (e < d) {
-                                    ALIVE[k] &= ~(1u << bit);
-                                } else {
-                                    nd = min(nd, e == 255 && d < 256 ? 256 : e + 1);
-                                }
-                            }
-                            ND[k] = nd;
-                            E[k] &= ALIVE[k];
-                        }
-                        if (d + OFF_FIX >= TRIG[k] + t) {  // entries: c_j + d reached t
-                            uint32_t cand = ALIVE[k] & ~E[k];
-                            int nt = TRIG_INF;
-                            uint32_t added = 0;
-                            while (cand) {
-                                const int bit = __ffs(cand) - 1;
-                                cand &= cand - 1;
-                                const int u = us[(k * 32 + bit) * NT + tau];
-                                if (u + t <= d + OFF_FIX)
-                                    added |= 1u << bit;
-                                else
-                                    nt = min(nt, u);
-                            }
-                            E[k] |= added;
-                            TRIG[k] = nt;
-                            if (added) dirty |= 1u << (b * WPT + k);
-                        }
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < WPT; ++k) hist[b * Wpad + tau * WPT + k] = d <= H ? E[k] : 0u;
-            }
-            if (tau == 0 && (tile & 7) == 7) misc->g = polled;
-            __syncthreads();
-
-            const int lastb = min(B - 1, H - d0);
-            int cur_t = t, start_b = 0, full_from = full_next ? 0 : B, last_raise = -1;
-            for (;;) {
-                uint32_t best = RES_INF;
-                const int m = cur_t - t;
+            } else {
                 for (int b = start_b; b <= lastb; ++b) {
                     const bool full = b >= full_from;
 #pragma unroll
@@ -850,60 +655,392 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
                         }
                     }
                 }
-                const int slot = round_ctr % 3;
-                if (best != RES_INF) atomicMin(&misc->res[slot], best);
-                if (tau == 0) misc->res[(round_ctr + 1) % 3] = RES_INF;
-                __syncthreads();
-                const uint32_t rr = misc->res[slot];
-                ++round_ctr;
-                if (rr == RES_INF) break;
-                const int bs = (int)(rr >> 20), col = (int)(rr & 0xFFFFFu);
-                if (tau == 0) {
-                    fixkey = pack_key(cur_t, p.row_base + r0 + d0 + bs - 1, col + cur_t - 1);
-                    if (p.share) atomicMax(res_best(result), cur_t);
-                }
-                last_raise = bs;
-                ++cur_t;
-                start_b = bs + 1;
-                full_from = bs + 1;
-                if (start_b > lastb) break;
             }
-            const int nraise = cur_t - t;
-            const int meff = nraise - (last_raise == lastb ? 1 : 0);
-            const int d_last = d0 + lastb;
-            if (meff > 0) {
+            const int slot = round_ctr % 3;
+            if (best != RES_INF) atomicMin(&misc->res[slot], best);
+            if (tau == 0) misc->res[(round_ctr + 1) % 3] = RES_INF;
+            tsync<SUB>(tmask);  // (B)
+            const uint32_t rr = misc->res[slot];
+            ++round_ctr;
+            if (rr == RES_INF) break;
+            const int bs_ = (int)(rr >> 20), col = (int)(rr & 0xFFFFFu);
+            if (tau == 0) {
+                bandkey = pack_key(cur_t, p.row_base + r0 + row0 + bs_, col + cur_t - 1);
+                if (p.share) atomicMax(res_best(result), cur_t);
+            }
+            ++cur_t;
+            start_b = bs_ + 1;
+            full_from = bs_ + 1;
+            if (start_b > lastb) break;
+        }
+        const bool raised = cur_t != t;
+        t = cur_t;
+        bool jumped = false;
+        if (p.share) {
+            const int g = misc->g;
+            if (g > t) {
+                t = g;
+                jumped = true;
+            }
+        }
+        full_next = raised || jumped;
+
+        // ---------------------------------------------------- phase C
+        uint32_t zf = zflag;
+        while (zf) {
+            const int bit = __ffs(zf) - 1;
+            zf &= zf - 1;
+            const int b = bit / WPT, k = bit - b * WPT;
+            const int r = row0 + b, rho = r + 1;
+            const int a = tau * WPT + k;
+            const uint8_t* srow = TMA ? ring + (size_t)(r % p.nstage) * p.rs : nullptr;
+            const uint32_t wv =
+                word_of_row<U8, TMA>(srow, mbase + (size_t)(r0 + r) * p.ld_bytes, a, p.cols, p.rs);
+            const uint32_t zeros = VAL[k] & ~wv;
+            if (zeros == VAL[k]) {
+                za[a] = (uint16_t)rho;
+            } else {
+                uint32_t zz = zeros;
+                while (zz) {
+                    const int j = __ffs(zz) - 1;
+                    zz &= zz - 1;
+                    zs[(k * 32 + j) * NT + tau] = (uint16_t)rho;
+                }
+            }
+            uint32_t newly = NZ[k] & zeros;
+            if (newly && p.write_summaries) {
+                const size_t cb = sum_base + (size_t)a * 32;
+                while (newly) {
+                    const int j = __ffs(newly) - 1;
+                    newly &= newly - 1;
+                    p.e_out[cb + j] = (uint16_t)(rho - 1);
+                }
+            }
+            NZ[k] &= ~zeros;
+        }
+        if (modeL)
+            for (int i = tau; i < BMAX * fstride; i += NT) fm[i] = 0u;
+        row0 += nrows;
+    }
+    tsync<SUB>(tmask);
+
+    // ---------------------------------------------------------- band outputs
+    if (p.write_summaries) {
 #pragma unroll
-                for (int k = 0; k < WPT; ++k) {
-                    const int a = tau * WPT + k;
-                    if (a < W) {
-                        const uint32_t en = e_at(hist, Wpad, lastb, meff, a);
-                        const uint32_t removed = E[k] & ~en;
-                        E[k] = en;
-                        if (removed) TRIG[k] = min(TRIG[k], d_last + OFF_FIX - t - meff + 1);
+        for (int k = 0; k < WPT; ++k) {
+            const int a = tau * WPT + k;
+            if (a < W) {
+                const size_t cb = sum_base + (size_t)a * 32;
+                uint32_t nz = NZ[k];
+                while (nz) {
+                    const int j = __ffs(nz) - 1;
+                    nz &= nz - 1;
+                    p.e_out[cb + j] = (uint16_t)H;
+                }
+                const int zaa = za[a];
+                uint4* dst = (uint4*)(p.b_out + cb);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint32_t v[4];
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const int j0 = 8 * q + 2 * h;
+                        const int u0 = max((int)zs[(k * 32 + j0) * NT + tau], zaa);
+                        const int u1 = max((int)zs[(k * 32 + j0 + 1) * NT + tau], zaa);
+                        v[h] = (uint32_t)(H - u0) | ((uint32_t)(H - u1) << 16);
                     }
+                    dst[q] = make_uint4(v[0], v[1], v[2], v[3]);
+                }
+                p.ao_out[(size_t)band * W + a] = NZ[k];
+            }
+        }
+    }
+    if (U8 && (bad_or & 0xFEFEFEFEu)) atomicOr(res_status(result), 1u);
+    if (tau == 0) {
+        if (p.band_keys) p.band_keys[unit] = bandkey;
+        if (bandkey) atomicMax(res_key1(result), bandkey);
+    }
+}
+
+// ============================================================ fix-up kernel
+// virtual band top: column j has height c_j + d at depth d while d <= e_j.
+struct FixExact {
+    const uint16_t* us;   // c clamped to 65535
+    const uint8_t* e8;    // e clamped to 255
+    const uint16_t* e_g;  // exact e (global) for this band
+    int NT, WPT, W, cols;
+    int d0;               // depth of tile row 0
+    __device__ __forceinline__ bool elig(int a, int j, int d, int T) const {
+        const int tau = a / WPT, k = a - tau * WPT;
+        const int idx = (k * 32 + j) * NT + tau;
+        int e = e8[idx];
+        if (e == 255 && d > 255) e = e_g[32 * a + j];
+        return e >= d && (int)us[idx] + d >= T;
+    }
+    __device__ uint32_t mask(int a, int b, int T) const {
+        const uint32_t val = valid_mask(a, W, cols);
+        const int d = d0 + b;
+        uint32_t m = 0, cand = val;
+        while (cand) {
+            const int j = __ffs(cand) - 1;
+            cand &= cand - 1;
+            if (elig(a, j, d, T)) m |= 1u << j;
+        }
+        return m;
+    }
+};
+
+template <int WPT>
+__global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int NT = blockDim.x;
+    const int tau = threadIdx.x;
+    const int band = p.band_begin + blockIdx.x;
+    const int W = p.W;
+    const int Wpad = NT * WPT;
+    const int nfw = (Wpad + 31) / 32;
+    const int fstride = r16(nfw * 4) / 4;
+    const int r0 = band_row0(p.rows, p.nbands, band);
+    const int H = band_row0(p.rows, p.nbands, band + 1) - r0;
+    unsigned char* result = p.results;
+
+    const FixLayout Lo = fix_layout(NT, WPT, p.bs);
+    uint16_t* us = (uint16_t*)(smem + Lo.us);
+    uint8_t* e8 = smem + Lo.e8;
+    uint32_t* hist = (uint32_t*)(smem + Lo.hist);
+    uint32_t* fmap = (uint32_t*)(smem + Lo.fmap);
+    Misc* misc = (Misc*)(smem + Lo.misc);
+    const uint16_t* e_g = p.e_in + (size_t)band * p.cols_pad;
+
+    if (tau == 0) {
+        misc->res[0] = misc->res[1] = misc->res[2] = RES_INF;
+        int g = (int)(*(volatile unsigned long long*)res_key1(result) >> (2 * KEY_DIM_BITS));
+        if (p.share) g = max(g, ld_volatile(res_best(result)));
+        misc->g = g;
+    }
+    for (int i = tau; i < 2 * BMAX * fstride; i += NT) fmap[i] = 0u;
+
+    uint32_t VAL[WPT];
+    int MINC[WPT], MINE[WPT];
+    uint32_t CP[WPT][FIX_XPL], EP[WPT][FIX_XPL];  // mode X planes: min(c,63), min(e,63)
+#pragma unroll
+    for (int k = 0; k < WPT; ++k) {
+        const int a = tau * WPT + k;
+        const uint32_t v = valid_mask(a, W, p.cols);
+        VAL[k] = v;
+        MINC[k] = -0x3FFFFFFF;
+        MINE[k] = -1;
+#pragma unroll
+        for (int q = 0; q < FIX_XPL; ++q) CP[k][q] = EP[k][q] = 0;
+        if (!v) continue;
+        int minc = 0x7FFFFFFF, mine = 0x7FFFFFFF;
+        // ---- carry-in heights by look-back over the bands above (P5), 8 bands per step
+        uint32_t pending = v;
+        long long acc = 0;
+        for (int q0 = band - 1; q0 >= 0 && pending; q0 -= 8) {
+            uint32_t mq[8];
+#pragma unroll
+            for (int s = 0; s < 8; ++s) mq[s] = (q0 - s >= 0) ? p.ao_in[(size_t)(q0 - s) * W + a] : 0u;
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+                const int q = q0 - s;
+                if (q >= 0 && pending) {
+                    uint32_t res = pending & ~mq[s];
+                    while (res) {
+                        const int j = __ffs(res) - 1;
+                        res &= res - 1;
+                        const long long c = acc + p.b_in[(size_t)q * p.cols_pad + 32 * a + j];
+                        us[(k * 32 + j) * NT + tau] = (uint16_t)min(c, 65535ll);
+                    }
+                    pending &= mq[s];
+                    acc += band_row0(p.rows, p.nbands, q + 1) - band_row0(p.rows, p.nbands, q);
                 }
             }
-            full_next = nraise > 0 && last_raise == lastb;
-            t = cur_t;
-            if (p.share) {
-                const int g = misc->g;
-                if (g > t) {
+        }
+        while (pending) {
+            const int j = __ffs(pending) - 1;
+            pending &= pending - 1;
+            const long long c = acc + (p.base_carry ? (long long)p.base_carry[32 * a + j] : 0ll);
+            us[(k * 32 + j) * NT + tau] = (uint16_t)min(c, 65535ll);
+        }
+        // ---- leading-ones depth of the band top, per-word minima, mode X planes
+        const uint4* ep = (const uint4*)(e_g + (size_t)32 * a);
 #pragma unroll
-                    for (int k = 0; k < WPT; ++k) {
-                        uint32_t ee = E[k];
-                        while (ee) {
-                            const int bit = __ffs(ee) - 1;
-                            ee &= ee - 1;
-                            const int u = us[(k * 32 + bit) * NT + tau];
-                            if (u + g > d_last + OFF_FIX) {
-                                E[k] &= ~(1u << bit);
-                                TRIG[k] = min(TRIG[k], u);
-                            }
+        for (int q = 0; q < 4; ++q) {
+            const uint4 v4 = ep[q];
+            const uint32_t pr[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+#pragma unroll
+                for (int s = 0; s < 2; ++s) {
+                    const int j = 8 * q + 2 * h + s;
+                    if ((v >> j) & 1u) {
+                        const int e = (int)((pr[h] >> (16 * s)) & 0xFFFFu);
+                        const int idx = (k * 32 + j) * NT + tau;
+                        e8[idx] = (uint8_t)min(e, 255);
+                        const int c = us[idx];
+                        mine = min(mine, e);
+                        minc = min(minc, c);
+                        const int e63 = min(e, 63), c63 = min(c, 63);
+#pragma unroll
+                        for (int pl = 0; pl < FIX_XPL; ++pl) {
+                            EP[k][pl] |= (uint32_t)((e63 >> pl) & 1) << j;
+                            CP[k][pl] |= (uint32_t)((c63 >> pl) & 1) << j;
                         }
                     }
-                    t = g;
                 }
             }
+        }
+        if (v == 0xFFFFFFFFu) {  // a partial word is never F
+            MINC[k] = minc;
+            MINE[k] = mine;
+        }
+    }
+    __syncthreads();
+    int t = max(1, misc->g);
+    FixExact ex{us, e8, e_g, NT, WPT, W, p.cols, 1};
+
+    int round_ctr = 0;
+    auto round_result = [&](uint32_t best) -> uint32_t {
+        const int slot = round_ctr % 3;
+        if (best != RES_INF) atomicMin(&misc->res[slot], best);
+        if (tau == 0) misc->res[(round_ctr + 1) % 3] = RES_INF;
+        __syncthreads();
+        const uint32_t r = misc->res[slot];
+        ++round_ctr;
+        return r;
+    };
+    auto probe = [&](int T) -> uint32_t {  // full test of depth 1 at threshold T
+        uint32_t ev[WPT];
+        ex.d0 = 1;
+#pragma unroll
+        for (int k = 0; k < WPT; ++k) {
+            const int a = tau * WPT + k;
+            ev[k] = a < W ? ex.mask(a, 0, T) : 0u;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < WPT; ++k) hist[tau * WPT + k] = ev[k];
+        __syncthreads();
+        uint32_t best = RES_INF;
+#pragma unroll
+        for (int k = 0; k < WPT; ++k) {
+            const int a = tau * WPT + k;
+            if (a < W) test_word_full(hist, Wpad, W, 0, 0, a, T, best);
+        }
+        return round_result(best);
+    };
+
+    unsigned long long fixkey = 0ull;
+    if (H >= 1) {
+        // ---------------------------------------------- depth 1, exact seeding
+        const uint32_t r = probe(t);
+        if (r != RES_INF) {
+            int lo = t, hi = -1;
+            uint32_t rlo = r;
+            int step = 1;
+            while (hi < 0) {
+                const int kk = lo + step;
+                if (kk > p.cols) {
+                    hi = kk;
+                    break;
+                }
+                const uint32_t rk = probe(kk);
+                if (rk != RES_INF) {
+                    lo = kk;
+                    rlo = rk;
+                    step *= 2;
+                } else {
+                    hi = kk;
+                }
+            }
+            while (hi - lo > 1) {
+                const int mid = lo + (hi - lo) / 2;
+                const uint32_t rk = probe(mid);
+                if (rk != RES_INF) {
+                    lo = mid;
+                    rlo = rk;
+                } else {
+                    hi = mid;
+                }
+            }
+            if (tau == 0) {
+                fixkey = pack_key(lo, p.row_base + r0, (int)(rlo & 0xFFFFFu) + lo - 1);
+                if (p.share) atomicMax(res_best(result), lo);
+            }
+            t = lo + 1;
+        }
+        __syncthreads();
+
+        // ---------------------------------------------- depths 2.. in tiles
+        int tile = 0;
+        for (int d0 = 2; d0 <= H && d0 < t; ++tile) {
+            const bool modeL = t >= FIX_TL;
+            const int nrows = min(modeL ? p.bl : p.bs, H - d0 + 1);
+            uint32_t* fm = fmap + (tile & 1) * BMAX * fstride;
+            int polled = 0;
+            if (p.share && tau == 0 && (tile & 7) == 7) polled = ld_volatile(res_best(result));
+#pragma unroll
+            for (int b = 0; b < BMAX; ++b) {
+                if (b < nrows) {
+                    const int d = d0 + b;
+                    uint32_t fnib = 0;
+#pragma unroll
+                    for (int k = 0; k < WPT; ++k) {
+                        if (modeL) {
+                            fnib |= ((d <= MINE[k] && MINC[k] + d >= t) ? 1u : 0u) << k;
+                        } else {  // t <= 62: exact E from the clamped planes
+                            const uint32_t e = planes_ge<FIX_XPL>(CP[k], max(t - d, 0)) &
+                                               planes_ge<FIX_XPL>(EP[k], d) & VAL[k];
+                            hist[b * Wpad + tau * WPT + k] = e;
+                        }
+                    }
+                    if (modeL && fnib) {
+                        const int a0 = tau * WPT;
+                        atomicOr(&fm[b * fstride + (a0 >> 5)], fnib << (a0 & 31));
+                    }
+                }
+            }
+            if (tau == 0 && (tile & 7) == 7) misc->g = polled;
+            __syncthreads();
+
+            const int lastb = nrows - 1;
+            int cur_t = t, start_b = 0;
+            ex.d0 = d0;
+            for (;;) {
+                uint32_t best = RES_INF;
+                const int m = cur_t - t;
+                if (modeL) {
+                    const int n = (lastb - start_b + 1) * nfw;
+                    for (int idx = tau; idx < n; idx += NT) {
+                        const int b = start_b + idx / nfw, fw = idx % nfw;
+                        scan_fword(fm, fstride, W, b, m, fw, cur_t, ex, best);
+                    }
+                } else {
+                    for (int b = start_b; b <= lastb; ++b) {
+#pragma unroll
+                        for (int k = 0; k < WPT; ++k) {
+                            const int a = tau * WPT + k;
+                            if (a < W) test_word_full(hist, Wpad, W, b, m, a, cur_t, best);
+                        }
+                    }
+                }
+                const uint32_t rr = round_result(best);
+                if (rr == RES_INF) break;
+                const int bs_ = (int)(rr >> 20), col = (int)(rr & 0xFFFFFu);
+                if (tau == 0) {
+                    fixkey = pack_key(cur_t, p.row_base + r0 + d0 + bs_ - 1, col + cur_t - 1);
+                    if (p.share) atomicMax(res_best(result), cur_t);
+                }
+                ++cur_t;
+                start_b = bs_ + 1;
+                if (start_b > lastb) break;
+            }
+            t = cur_t;
+            if (p.share) t = max(t, misc->g);
+            if (modeL)
+                for (int i = tau; i < BMAX * fstride; i += NT) fm[i] = 0u;
+            d0 += nrows;
         }
     }
     if (tau == 0) {
@@ -913,7 +1050,6 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
 }
 
 // ======================================================= row-band sharding
-// per column: bottom run of the whole local slice (P5 fold of all bands)
 __global__ void rank_summary_kernel(int rows, int cols, int W, int nbands, int cols_pad,
                                     const uint16_t* b_in, const uint32_t* ao_in, uint32_t* out) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -930,7 +1066,7 @@ __global__ void rank_summary_kernel(int rows, int cols, int W, int nbands, int c
         }
         acc += band_row0(rows, nbands, q + 1) - band_row0(rows, nbands, q);
     }
-    out[j] = done ? s : (uint32_t)acc;  // == rows: all ones
+    out[j] = done ? s : (uint32_t)acc;
 }
 
 struct RankRows {

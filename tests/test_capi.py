@@ -35,7 +35,10 @@ def test_plan_shapes(lib):
     assert (p.words, p.wpt, p.threads) == (1024, 2, 512)
     assert p.nstage >= 2
     p = N.plan(N.FMT_U8, 4096, 256, 256, 256)
-    assert (p.nbands, p.threads, p.batch) == (1, 32, 4096)
+    assert (p.nbands, p.team, p.batch) == (1, 8, 4096)  # sub-warp teams of 8 lanes
+    assert p.teams_per_cta * p.team == p.threads and p.threads % 32 == 0
+    assert p.grid * p.teams_per_cta >= 4096
+    assert p.smem_pass1 <= 232448
     # odd width: no TMA staging (rows are not 16-byte multiples)
     p = N.plan(N.FMT_U8, 1, 7, 13, 13)
     assert p.nstage == 0 and p.nbands == 1
