@@ -292,13 +292,11 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
         const long long gran = std::max(1, 32 / ts);  // teams per warp
         tpc = round_up(tpc, gran);
         tpc = std::min<long long>(tpc, 512 / ts);
-        p.nstage = tma_ok ? 6 : 0;
+        p.nstage = tma_ok ? 2 * msq::BMAX : 0;  // ring holds the previous and the current tile
         for (;;) {
             const long long per = msq::p1_layout(ts, 1, p.nstage, (int)row_bytes, p.tile_rows, p.nstage > 0).total;
             if (per * tpc <= kSmemMax) break;
-            if (p.nstage > 2) {
-                --p.nstage;
-            } else if (p.nstage > 0) {
+            if (p.nstage > 0) {
                 p.nstage = 0;
             } else {
                 tpc -= gran;
@@ -337,8 +335,10 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
         const int base = msq::p1_layout(p.threads, p.wpt, 0, (int)row_bytes, p.tile_rows, true).total;
         long long ns = (kSmemMax - base - 256) / row_bytes;
         ns = std::min<long long>(ns, 16);
-        if (ns < p.tile_rows_l + 2) p.tile_rows_l = 2;
-        if (ns >= p.tile_rows_l + 2) p.nstage = (int32_t)ns;
+        // the ring must hold the previous tile (freed only after the next
+        // tile's first barrier) plus the current one
+        if (ns < 2 * p.tile_rows_l) p.tile_rows_l = p.tile_rows;
+        if (ns >= 2 * p.tile_rows_l) p.nstage = (int32_t)ns;
     }
     p.smem_pass1 = msq::p1_layout(p.threads, p.wpt, p.nstage, (int)row_bytes, p.tile_rows, p.nstage > 0).total;
     p.smem_fixup = msq::fix_layout(p.threads, p.wpt, p.tile_rows).total;

@@ -246,48 +246,6 @@ __device__ __forceinline__ void test_word_incr(const uint32_t* hist, int Wpad, i
     }
 }
 
-// F-bitmap scan of one bitmap word (32 words of the row) at tile row b,
-// threshold T = t+m.  A qualifying run = suffix(a) + 32*len + prefix(c) with
-// the full words a+1..c-1 = one maximal F run; boundary words are checked
-// exactly through `ex`.
-template <class Exact>
-__device__ __forceinline__ void scan_fword(const uint32_t* fm, int nfw, int W, int b, int m, int fw,
-                                           int T, const Exact& ex, uint32_t& best) {
-    const uint32_t x = x_at(fm, nfw, b, m, fw);
-    if (!x) return;
-    const uint32_t prev = fw > 0 ? (x_at(fm, nfw, b, m, fw - 1) >> 31) : 0u;
-    uint32_t starts = x & ~((x << 1) | prev);
-    const int nwords_f = (W + 31) / 32;
-    while (starts) {
-        const int i = __ffs(starts) - 1;
-        starts &= starts - 1;
-        const uint32_t rest = x >> i;
-        int len = (~rest == 0u) ? 32 : (__ffs(~rest) - 1);
-        if (i + len == 32) {
-            for (int y = fw + 1; y < nwords_f; ++y) {
-                const uint32_t nx = x_at(fm, nfw, b, m, y);
-                if (nx == 0xFFFFFFFFu) {
-                    len += 32;
-                } else {
-                    len += __ffs(~nx) - 1;
-                    break;
-                }
-            }
-        }
-        const int a0 = fw * 32 + i;  // first full word of the run
-        const int a = a0 - 1, c = a0 + len;
-        const int ub = 32 * len + (a >= 0 ? 31 : 0) + (c < W ? 32 : 0);
-        if (ub < T) continue;
-        const int suf = a >= 0 ? __clz(~ex.mask(a, b, T)) : 0;
-        int pre = 0;
-        if (c < W) {
-            const uint32_t mk = ex.mask(c, b, T);
-            pre = (mk == 0xFFFFFFFFu) ? 32 : __ffs(~mk) - 1;
-        }
-        if (suf + 32 * len + pre >= T) best = min(best, enc_res(b, 32 * a0 - suf));
-    }
-}
-
 // ------------------------------------------------------------------ params
 struct Pass1Params {
     const uint8_t* src;
@@ -459,7 +417,47 @@ __device__ __forceinline__ uint32_t word_of_row(const uint8_t* stage_row, const 
     return ((const uint32_t*)grow)[a];
 }
 
-// exact eligibility of a word inside a pass-1 tile (mode L boundary check)
+// scan one F-bitmap word (32 words of the row) at tile row b, threshold T =
+// t+m: every maximal F run that STARTS here and whose upper bound
+// 32*len + 31 + 32 reaches T is handed to on_cand(b, a0, len).  A qualifying
+// run = suffix(a0-1) + 32*len + prefix(a0+len); the boundary words are checked
+// exactly by the caller.
+template <class OnCand>
+__device__ __forceinline__ void scan_fword(const uint32_t* fm, int nfw, int W, int b, int m, int fw,
+                                           int T, OnCand&& on_cand) {
+    const uint32_t x = x_at(fm, nfw, b, m, fw);
+    if (!x) return;
+    const uint32_t prev = fw > 0 ? (x_at(fm, nfw, b, m, fw - 1) >> 31) : 0u;
+    uint32_t starts = x & ~((x << 1) | prev);
+    const int nwords_f = (W + 31) / 32;
+    while (starts) {
+        const int i = __ffs(starts) - 1;
+        starts &= starts - 1;
+        const uint32_t rest = x >> i;
+        int len = (~rest == 0u) ? 32 : (__ffs(~rest) - 1);
+        if (i + len == 32) {
+            for (int y = fw + 1; y < nwords_f; ++y) {
+                const uint32_t nx = x_at(fm, nfw, b, m, y);
+                if (nx == 0xFFFFFFFFu) {
+                    len += 32;
+                } else {
+                    len += __ffs(~nx) - 1;
+                    break;
+                }
+            }
+        }
+        const int a0 = fw * 32 + i;
+        const int ub = 32 * len + (a0 > 0 ? 31 : 0) + (a0 + len < W ? 32 : 0);
+        if (ub >= T) on_cand(b, a0, len);
+    }
+}
+
+__device__ __forceinline__ int suffix_ones(uint32_t m) { return __clz(~m); }
+__device__ __forceinline__ int prefix_ones(uint32_t m) { return m == 0xFFFFFFFFu ? 32 : __ffs(~m) - 1; }
+
+// pass-1 exact eligibility of word a at tile row b, threshold T (T > BMAX):
+// column j eligible iff no zero in the tile rows <= b and its last zero before
+// the tile (max(zs, za)) is <= rho_b - T.  zs is word-major: zs[a*32 + j].
 template <bool U8, bool TMA>
 struct Pass1Exact {
     const uint16_t* zs;
@@ -467,7 +465,7 @@ struct Pass1Exact {
     const uint8_t* ring;
     const uint8_t* mbase;
     long long ld_bytes;
-    int NT, WPT, W, cols, rs, nstage;
+    int W, cols, rs, nstage;
     int tile_row0;  // band-relative 0-based row of tile row 0
     int r0;         // band top row (matrix)
     __device__ __forceinline__ const uint8_t* srow(int b) const {
@@ -476,34 +474,104 @@ struct Pass1Exact {
     __device__ __forceinline__ const uint8_t* grow(int b) const {
         return mbase + (size_t)(r0 + tile_row0 + b) * ld_bytes;
     }
+    // one thread computes the whole mask (sub-warp teams, overflow path)
     __device__ uint32_t mask(int a, int b, int T) const {
         const uint32_t val = valid_mask(a, W, cols);
-        const int rho_b = tile_row0 + b + 1;
-        const int lim = rho_b - T;  // last zero must be <= lim (T > BMAX: any zero in the tile kills)
+        const int lim = tile_row0 + b + 1 - T;
         if ((int)za[a] > lim) return 0u;
         uint32_t zin = 0;
         for (int q = 0; q <= b; ++q) zin |= ~word_of_row<U8, TMA>(srow(q), grow(q), a, cols, rs);
-        uint32_t cand = val & ~zin, m = 0;
-        const int tau = a / WPT, k = a - tau * WPT;
-        while (cand) {
-            const int j = __ffs(cand) - 1;
-            cand &= cand - 1;
-            if ((int)zs[(k * 32 + j) * NT + tau] <= lim) m |= 1u << j;
+        const uint4* zp = (const uint4*)(zs + (size_t)a * 32);
+        uint32_t m = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint4 v = zp[q];
+            const uint32_t pr[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                m |= ((int)(pr[h] & 0xFFFFu) <= lim ? 1u : 0u) << (8 * q + 2 * h);
+                m |= ((int)(pr[h] >> 16) <= lim ? 1u : 0u) << (8 * q + 2 * h + 1);
+            }
         }
-        return m;
+        return m & val & ~zin;
+    }
+    // one full warp, lane = column
+    __device__ uint32_t coop_mask(int a, int b, int T, int lane) const {
+        const uint32_t val = valid_mask(a, W, cols);
+        const int lim = tile_row0 + b + 1 - T;
+        bool el = ((val >> lane) & 1u) && (int)za[a] <= lim && (int)zs[(size_t)a * 32 + lane] <= lim;
+        for (int q = 0; q <= b; ++q) {
+            uint32_t one;
+            if (U8) {
+                one = TMA ? srow(q)[(size_t)a * 32 + lane] : ((a * 32 + lane < cols) ? grow(q)[a * 32 + lane] : 0);
+                one = one != 0;
+            } else {
+                one = (word_of_row<U8, TMA>(srow(q), grow(q), a, cols, rs) >> lane) & 1u;
+            }
+            el = el && one;
+        }
+        return __ballot_sync(0xFFFFFFFFu, el);
     }
 };
 
+// leftmost window of T consecutive ones in row X (smem, W words) starting at
+// column >= s0; one full warp; returns the start column or -1.  Segmented
+// warp scan of run lengths (R = full ? R_prev + 32 : suffix), chunk by chunk.
+__device__ int warp_first_window(const uint32_t* X, int W, int s0, int T, int lane) {
+    int carry = 0;
+    const int w0 = s0 >> 5;
+    const uint32_t first_mask = ~((1u << (s0 & 31)) - 1u);
+    for (int base = w0; base < W; base += 32) {
+        const int w = base + lane;
+        uint32_t x = (w < W) ? X[w] : 0u;
+        if (w == w0) x &= first_mask;
+        const bool full = x == 0xFFFFFFFFu;
+        const int pre = prefix_ones(x);
+        int v = full ? 32 : suffix_ones(x);
+        int f = full ? 1 : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v2 = __shfl_up_sync(0xFFFFFFFFu, v, o);
+            const int f2 = __shfl_up_sync(0xFFFFFFFFu, f, o);
+            if (lane >= o) {
+                if (f) v = v2 + v;
+                f = f & f2;
+            }
+        }
+        const int R = f ? carry + v : v;  // run ending at bit 31 of my word
+        int Rin = __shfl_up_sync(0xFFFFFFFFu, R, 1);
+        if (lane == 0) Rin = carry;
+        int end = 64;
+        if (Rin < T && Rin + pre >= T) end = T - Rin - 1;
+        if (T <= 32 && x) {
+            const uint32_t y = windows_in_word(x, T);
+            if (y) end = min(end, __ffs(y) - 1 + T - 1);
+        }
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, end < 64);
+        if (bal) {
+            const int src = __ffs(bal) - 1;
+            const int e = __shfl_sync(0xFFFFFFFFu, end, src);
+            return 32 * (base + src) + e - T + 1;
+        }
+        carry = __shfl_sync(0xFFFFFFFFu, R, 31);
+    }
+    return -1;
+}
+
 // ============================================================= pass 1 kernel
+// Tile kinds: CLIMB (t >= rho: heights <= rho, so E = prefix-AND of the band
+// top when t == rho; 1 row per tile, one warp finds the leftmost window),
+// S (t < tl: bit-sliced counters), L (t >= tl: word-level F filter).
 template <int WPT, bool U8, bool TMA, bool SUB>
 __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int NT = p.team;
     const int tid = threadIdx.x;
+    const int lane = tid & 31;
     const int team_idx = SUB ? tid / NT : 0;
     const int tau = SUB ? tid - team_idx * NT : tid;
     const unsigned tmask =
-        SUB ? (unsigned)((NT >= 32 ? 0xFFFFFFFFull : ((1ull << NT) - 1ull)) << ((tid & 31) - tau)) : 0xFFFFFFFFu;
+        SUB ? (unsigned)((NT >= 32 ? 0xFFFFFFFFull : ((1ull << NT) - 1ull)) << (lane - (tau & 31))) : 0xFFFFFFFFu;
     const int teams_per_cta = SUB ? (int)blockDim.x / NT : 1;
     const int unit = blockIdx.x * teams_per_cta + team_idx;
     if (unit >= p.units) return;  // whole idle team (sub-warp teams only)
@@ -521,7 +589,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     uint8_t* tsm = smem + (size_t)team_idx * p.layout_bytes;
     uint8_t* ring = tsm + Lo.ring;
     uint64_t* bars = (uint64_t*)(tsm + Lo.bars);
-    uint16_t* zs = (uint16_t*)(tsm + Lo.zs);
+    uint16_t* zs = (uint16_t*)(tsm + Lo.zs);  // word-major: zs[a*32 + j]
     uint16_t* za = (uint16_t*)(tsm + Lo.za);
     uint32_t* hist = (uint32_t*)(tsm + Lo.hist);
     uint32_t* fmap = (uint32_t*)(tsm + Lo.fmap);
@@ -530,13 +598,14 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     const uint8_t* mbase = p.src + (size_t)mat * p.batch_stride;
     const size_t sum_base = (size_t)band * p.cols_pad;
 
-    uint32_t VAL[WPT], NZ[WPT], EPREV[WPT];
+    uint32_t VAL[WPT], NZ[WPT], EPREV[WPT], AL[WPT];
     uint32_t HC[WPT][NPLANES];
     int ZW[WPT];
 #pragma unroll
     for (int k = 0; k < WPT; ++k) {
         VAL[k] = valid_mask(tau * WPT + k, W, p.cols);
         NZ[k] = VAL[k];
+        AL[k] = VAL[k];
         EPREV[k] = 0;
         ZW[k] = 0;
 #pragma unroll
@@ -555,7 +624,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     }
     tsync<SUB>(tmask);
 
-    int issued = 0;  // next band row to stage (meaningful in the producer thread)
+    int issued = 0;  // next band row to stage (producer thread)
     if (TMA && tau == 0) {
         for (; issued < min(p.nstage, H); ++issued) {
             const int s = issued % p.nstage;
@@ -567,15 +636,41 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 
     int t = max(1, misc->g);
     bool full_next = false;
+    bool counters_ok = true;  // counters track heights since the band top
+    int climb_s = 0;          // leftmost window start of the last successful climb test
     unsigned long long bandkey = 0ull;
     int round_ctr = 0;
     uint32_t bad_or = 0;
     int tile = 0;
 
     for (int row0 = 0; row0 < H; ++tile) {
-        const bool modeL = t >= p.tl;
-        const int nrows = min(modeL ? p.bl : p.bs, H - row0);
+        const int rho0 = row0 + 1;
+        const bool climb = t >= rho0;
+        const bool modeL = !climb && t >= p.tl;
+        const bool modeS = !climb && !modeL;
+        const int nrows = climb ? 1 : min(modeL ? p.bl : p.bs, H - row0);
         uint32_t* fm = fmap + (tile & 1) * BMAX * fstride;
+        if (modeS && !counters_ok) {
+            // (re)build the counters from the last-zero rows: h = rho0-1 - lastzero
+#pragma unroll
+            for (int k = 0; k < WPT; ++k) {
+                const int a = tau * WPT + k;
+#pragma unroll
+                for (int q = 0; q < NPLANES; ++q) HC[k][q] = 0;
+                if (a < W) {
+                    const int zaa = za[a];
+                    for (int j = 0; j < 32; ++j) {
+                        const int h = min(rho0 - 1 - max((int)zs[(size_t)a * 32 + j], zaa), 127);
+#pragma unroll
+                        for (int q = 0; q < NPLANES; ++q) HC[k][q] |= (uint32_t)((h >> q) & 1) << j;
+                    }
+#pragma unroll
+                    for (int q = 0; q < NPLANES; ++q) HC[k][q] &= VAL[k];
+                }
+            }
+            counters_ok = true;
+            full_next = true;
+        }
         int polled = 0;
         if (p.share && tau == 0 && (tile & 7) == 7) polled = ld_volatile(res_best(result));
 
@@ -600,7 +695,10 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     const bool z = w[k] != VAL[k];
                     ZW[k] = z ? rho : ZW[k];
                     zflag |= (z ? 1u : 0u) << (b * WPT + k);
-                    if (modeL) {
+                    AL[k] &= w[k];
+                    if (climb) {
+                        hist[b * Wpad + tau * WPT + k] = AL[k];
+                    } else if (modeL) {
                         fnib |= ((VAL[k] == 0xFFFFFFFFu && ZW[k] <= rho - t) ? 1u : 0u) << k;
                     } else {
                         planes_step<NPLANES>(HC[k], w[k]);
@@ -630,48 +728,111 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 
         // ---------------------------------------------------- phase B
         const int lastb = nrows - 1;
-        int cur_t = t, start_b = 0, full_from = full_next ? 0 : BMAX;
-        const Pass1Exact<U8, TMA> ex{zs, za, ring, mbase, p.ld_bytes, NT, WPT, W, p.cols, p.rs, p.nstage, row0, r0};
-        for (;;) {
-            uint32_t best = RES_INF;
-            const int m = cur_t - t;
-            if (modeL) {
-                const int n = (lastb - start_b + 1) * nfw;
-                for (int idx = tau; idx < n; idx += NT) {
-                    const int b = start_b + idx / nfw, fw = idx % nfw;
-                    scan_fword(fm, fstride, W, b, m, fw, cur_t, ex, best);
-                }
-            } else {
-                for (int b = start_b; b <= lastb; ++b) {
-                    const bool full = b >= full_from;
+        int cur_t = t;
+        const Pass1Exact<U8, TMA> ex{zs, za, ring, mbase, p.ld_bytes, W, p.cols, p.rs, p.nstage, row0, r0};
+        if (climb) {
+            if (t == rho0) {  // E = prefix-AND of the band top; find the leftmost t-window
+                int start = -1;
+                if (!SUB) {
+                    if (tid < 32) {
+                        start = warp_first_window(hist, W, climb_s, t, lane);
+                        if (lane == 0) misc->res[0] = (uint32_t)start;
+                    }
+                } else {
+                    uint32_t best = RES_INF;
 #pragma unroll
                     for (int k = 0; k < WPT; ++k) {
                         const int a = tau * WPT + k;
-                        if (a < W) {
-                            if (full)
-                                test_word_full(hist, Wpad, W, b, m, a, cur_t, best);
-                            else if ((dirty >> (b * WPT + k)) & 1u)
-                                test_word_incr(hist, Wpad, W, b, m, a, cur_t, best);
+                        if (a < W) test_word_full(hist, Wpad, W, 0, 0, a, t, best);
+                    }
+                    if (best != RES_INF) atomicMin(&misc->res[0], best);
+                }
+                tsync<SUB>(tmask);  // (B)
+                const uint32_t rr = misc->res[0];
+                tsync<SUB>(tmask);
+                if (tau == 0) misc->res[0] = RES_INF;
+                start = (rr == RES_INF) ? -1 : (int)(rr & 0xFFFFFu);
+                if (!SUB && rr == 0xFFFFFFFFu) start = -1;
+                if (start >= 0) {
+                    if (tau == 0) {
+                        bandkey = pack_key(t, p.row_base + r0 + row0, start + t - 1);
+                        if (p.share) atomicMax(res_best(result), t);
+                    }
+                    climb_s = start;
+                    cur_t = t + 1;
+                }
+            }
+        } else {
+            int start_b = 0, full_from = full_next ? 0 : BMAX;
+            for (;;) {
+                uint32_t best = RES_INF;
+                const int m = cur_t - t;
+                if (modeL) {
+                    const int n = (lastb - start_b + 1) * nfw;
+                    int nc = 0, cb0 = 0, ca0 = 0, cl0 = 0, cb1 = 0, ca1 = 0, cl1 = 0;
+                    for (int idx = tau; idx < n; idx += NT) {
+                        const int b = start_b + idx / nfw, fw = idx % nfw;
+                        scan_fword(fm, fstride, W, b, m, fw, cur_t, [&](int cb, int a0, int len) {
+                            if (!SUB && nc < 2) {
+                                if (nc == 0) { cb0 = cb; ca0 = a0; cl0 = len; }
+                                else { cb1 = cb; ca1 = a0; cl1 = len; }
+                                ++nc;
+                            } else {  // serial exact check
+                                const int suf = a0 > 0 ? suffix_ones(ex.mask(a0 - 1, cb, cur_t)) : 0;
+                                const int pre = a0 + len < W ? prefix_ones(ex.mask(a0 + len, cb, cur_t)) : 0;
+                                if (suf + 32 * len + pre >= cur_t) best = min(best, enc_res(cb, 32 * a0 - suf));
+                            }
+                        });
+                    }
+                    if (!SUB) {  // warp-cooperative exact checks: lane = column
+                        for (;;) {
+                            const unsigned mk = __ballot_sync(0xFFFFFFFFu, nc > 0);
+                            if (!mk) break;
+                            const int src = __ffs(mk) - 1;
+                            const int mb = nc == 2 ? cb1 : cb0, ma = nc == 2 ? ca1 : ca0, ml = nc == 2 ? cl1 : cl0;
+                            const int b = __shfl_sync(0xFFFFFFFFu, mb, src);
+                            const int a0 = __shfl_sync(0xFFFFFFFFu, ma, src);
+                            const int len = __shfl_sync(0xFFFFFFFFu, ml, src);
+                            const int suf = a0 > 0 ? suffix_ones(ex.coop_mask(a0 - 1, b, cur_t, lane)) : 0;
+                            const int pre = a0 + len < W ? prefix_ones(ex.coop_mask(a0 + len, b, cur_t, lane)) : 0;
+                            if (lane == src) {
+                                if (suf + 32 * len + pre >= cur_t) best = min(best, enc_res(b, 32 * a0 - suf));
+                                --nc;
+                            }
+                        }
+                    }
+                } else {
+                    for (int b = start_b; b <= lastb; ++b) {
+                        const bool full = b >= full_from;
+#pragma unroll
+                        for (int k = 0; k < WPT; ++k) {
+                            const int a = tau * WPT + k;
+                            if (a < W) {
+                                if (full)
+                                    test_word_full(hist, Wpad, W, b, m, a, cur_t, best);
+                                else if ((dirty >> (b * WPT + k)) & 1u)
+                                    test_word_incr(hist, Wpad, W, b, m, a, cur_t, best);
+                            }
                         }
                     }
                 }
+                const int slot = round_ctr % 3;
+                if (best != RES_INF) atomicMin(&misc->res[slot], best);
+                if (tau == 0) misc->res[(round_ctr + 1) % 3] = RES_INF;
+                tsync<SUB>(tmask);  // (B)
+                const uint32_t rr = misc->res[slot];
+                ++round_ctr;
+                if (rr == RES_INF) break;
+                const int bs_ = (int)(rr >> 20), col = (int)(rr & 0xFFFFFu);
+                if (tau == 0) {
+                    bandkey = pack_key(cur_t, p.row_base + r0 + row0 + bs_, col + cur_t - 1);
+                    if (p.share) atomicMax(res_best(result), cur_t);
+                }
+                ++cur_t;
+                start_b = bs_ + 1;
+                full_from = bs_ + 1;
+                if (start_b > lastb) break;
             }
-            const int slot = round_ctr % 3;
-            if (best != RES_INF) atomicMin(&misc->res[slot], best);
-            if (tau == 0) misc->res[(round_ctr + 1) % 3] = RES_INF;
-            tsync<SUB>(tmask);  // (B)
-            const uint32_t rr = misc->res[slot];
-            ++round_ctr;
-            if (rr == RES_INF) break;
-            const int bs_ = (int)(rr >> 20), col = (int)(rr & 0xFFFFFu);
-            if (tau == 0) {
-                bandkey = pack_key(cur_t, p.row_base + r0 + row0 + bs_, col + cur_t - 1);
-                if (p.share) atomicMax(res_best(result), cur_t);
-            }
-            ++cur_t;
-            start_b = bs_ + 1;
-            full_from = bs_ + 1;
-            if (start_b > lastb) break;
         }
         const bool raised = cur_t != t;
         t = cur_t;
@@ -684,6 +845,8 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
             }
         }
         full_next = raised || jumped;
+        if (!modeS) counters_ok = false;
+        if (!climb || !raised) climb_s = 0;
 
         // ---------------------------------------------------- phase C
         uint32_t zf = zflag;
@@ -704,7 +867,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 while (zz) {
                     const int j = __ffs(zz) - 1;
                     zz &= zz - 1;
-                    zs[(k * 32 + j) * NT + tau] = (uint16_t)rho;
+                    zs[(size_t)a * 32 + j] = (uint16_t)rho;
                 }
             }
             uint32_t newly = NZ[k] & zeros;
@@ -738,15 +901,17 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     p.e_out[cb + j] = (uint16_t)H;
                 }
                 const int zaa = za[a];
+                const uint4* zp = (const uint4*)(zs + (size_t)a * 32);
                 uint4* dst = (uint4*)(p.b_out + cb);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
+                    const uint4 zv = zp[q];
+                    const uint32_t pr[4] = {zv.x, zv.y, zv.z, zv.w};
                     uint32_t v[4];
 #pragma unroll
                     for (int h = 0; h < 4; ++h) {
-                        const int j0 = 8 * q + 2 * h;
-                        const int u0 = max((int)zs[(k * 32 + j0) * NT + tau], zaa);
-                        const int u1 = max((int)zs[(k * 32 + j0 + 1) * NT + tau], zaa);
+                        const int u0 = max((int)(pr[h] & 0xFFFFu), zaa);
+                        const int u1 = max((int)(pr[h] >> 16), zaa);
                         v[h] = (uint32_t)(H - u0) | ((uint32_t)(H - u1) << 16);
                     }
                     dst[q] = make_uint4(v[0], v[1], v[2], v[3]);
@@ -764,29 +929,48 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 
 // ============================================================ fix-up kernel
 // virtual band top: column j has height c_j + d at depth d while d <= e_j.
+// us/e8 are word-major (us[a*32 + j]).
 struct FixExact {
     const uint16_t* us;   // c clamped to 65535
     const uint8_t* e8;    // e clamped to 255
     const uint16_t* e_g;  // exact e (global) for this band
-    int NT, WPT, W, cols;
+    int W, cols;
     int d0;               // depth of tile row 0
-    __device__ __forceinline__ bool elig(int a, int j, int d, int T) const {
-        const int tau = a / WPT, k = a - tau * WPT;
-        const int idx = (k * 32 + j) * NT + tau;
+    __device__ __forceinline__ bool elig(int idx, int d, int T) const {
         int e = e8[idx];
-        if (e == 255 && d > 255) e = e_g[32 * a + j];
+        if (e == 255 && d > 255) e = e_g[idx];
         return e >= d && (int)us[idx] + d >= T;
     }
     __device__ uint32_t mask(int a, int b, int T) const {
         const uint32_t val = valid_mask(a, W, cols);
         const int d = d0 + b;
-        uint32_t m = 0, cand = val;
-        while (cand) {
-            const int j = __ffs(cand) - 1;
-            cand &= cand - 1;
-            if (elig(a, j, d, T)) m |= 1u << j;
+        uint32_t m = 0;
+        const uint4* up = (const uint4*)(us + (size_t)a * 32);
+        const uint4* ep = (const uint4*)(e8 + (size_t)a * 32);
+        const uint4 e0 = ep[0], e1 = ep[1];
+        const uint32_t ew[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint4 v = up[q];
+            const uint32_t pr[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+#pragma unroll
+                for (int s = 0; s < 2; ++s) {
+                    const int j = 8 * q + 2 * h + s;
+                    int e = (int)((ew[j >> 2] >> (8 * (j & 3))) & 0xFFu);
+                    if (e == 255 && d > 255) e = e_g[(size_t)a * 32 + j];
+                    const int c = (int)((pr[h] >> (16 * s)) & 0xFFFFu);
+                    m |= ((e >= d && c + d >= T) ? 1u : 0u) << j;
+                }
+            }
         }
-        return m;
+        return m & val;
+    }
+    __device__ uint32_t coop_mask(int a, int b, int T, int lane) const {
+        const uint32_t val = valid_mask(a, W, cols);
+        const bool el = ((val >> lane) & 1u) && elig(a * 32 + lane, d0 + b, T);
+        return __ballot_sync(0xFFFFFFFFu, el);
     }
 };
 
@@ -795,6 +979,7 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int NT = blockDim.x;
     const int tau = threadIdx.x;
+    const int lane = tau & 31;
     const int band = p.band_begin + blockIdx.x;
     const int W = p.W;
     const int Wpad = NT * WPT;
@@ -833,7 +1018,7 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
 #pragma unroll
         for (int q = 0; q < FIX_XPL; ++q) CP[k][q] = EP[k][q] = 0;
         if (!v) continue;
-        int minc = 0x7FFFFFFF, mine = 0x7FFFFFFF;
+        uint16_t* uw = us + (size_t)a * 32;
         // ---- carry-in heights by look-back over the bands above (P5), 8 bands per step
         uint32_t pending = v;
         long long acc = 0;
@@ -845,26 +1030,29 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
             for (int s = 0; s < 8; ++s) {
                 const int q = q0 - s;
                 if (q >= 0 && pending) {
-                    uint32_t res = pending & ~mq[s];
-                    while (res) {
-                        const int j = __ffs(res) - 1;
-                        res &= res - 1;
-                        const long long c = acc + p.b_in[(size_t)q * p.cols_pad + 32 * a + j];
-                        us[(k * 32 + j) * NT + tau] = (uint16_t)min(c, 65535ll);
+                    const uint32_t res = pending & ~mq[s];
+                    if (res) {
+                        const uint16_t* bq = p.b_in + (size_t)q * p.cols_pad + (size_t)32 * a;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if ((res >> j) & 1u) uw[j] = (uint16_t)min(acc + bq[j], 65535ll);
                     }
                     pending &= mq[s];
                     acc += band_row0(p.rows, p.nbands, q + 1) - band_row0(p.rows, p.nbands, q);
                 }
             }
         }
-        while (pending) {
-            const int j = __ffs(pending) - 1;
-            pending &= pending - 1;
-            const long long c = acc + (p.base_carry ? (long long)p.base_carry[32 * a + j] : 0ll);
-            us[(k * 32 + j) * NT + tau] = (uint16_t)min(c, 65535ll);
+        if (pending) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if ((pending >> j) & 1u) {
+                    const long long c = acc + (p.base_carry ? (long long)p.base_carry[32 * a + j] : 0ll);
+                    uw[j] = (uint16_t)min(c, 65535ll);
+                }
         }
         // ---- leading-ones depth of the band top, per-word minima, mode X planes
         const uint4* ep = (const uint4*)(e_g + (size_t)32 * a);
+        int minc = 0x7FFFFFFF, mine = 0x7FFFFFFF;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const uint4 v4 = ep[q];
@@ -876,9 +1064,8 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
                     const int j = 8 * q + 2 * h + s;
                     if ((v >> j) & 1u) {
                         const int e = (int)((pr[h] >> (16 * s)) & 0xFFFFu);
-                        const int idx = (k * 32 + j) * NT + tau;
-                        e8[idx] = (uint8_t)min(e, 255);
-                        const int c = us[idx];
+                        e8[(size_t)a * 32 + j] = (uint8_t)min(e, 255);
+                        const int c = uw[j];
                         mine = min(mine, e);
                         minc = min(minc, c);
                         const int e63 = min(e, 63), c63 = min(c, 63);
@@ -887,6 +1074,8 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
                             EP[k][pl] |= (uint32_t)((e63 >> pl) & 1) << j;
                             CP[k][pl] |= (uint32_t)((c63 >> pl) & 1) << j;
                         }
+                    } else {
+                        e8[(size_t)a * 32 + j] = 0;
                     }
                 }
             }
@@ -898,7 +1087,7 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
     }
     __syncthreads();
     int t = max(1, misc->g);
-    FixExact ex{us, e8, e_g, NT, WPT, W, p.cols, 1};
+    FixExact ex{us, e8, e_g, W, p.cols, 1};
 
     int round_ctr = 0;
     auto round_result = [&](uint32_t best) -> uint32_t {
@@ -1012,9 +1201,35 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
                 const int m = cur_t - t;
                 if (modeL) {
                     const int n = (lastb - start_b + 1) * nfw;
+                    int nc = 0, cb0 = 0, ca0 = 0, cl0 = 0, cb1 = 0, ca1 = 0, cl1 = 0;
                     for (int idx = tau; idx < n; idx += NT) {
                         const int b = start_b + idx / nfw, fw = idx % nfw;
-                        scan_fword(fm, fstride, W, b, m, fw, cur_t, ex, best);
+                        scan_fword(fm, fstride, W, b, m, fw, cur_t, [&](int cb, int a0, int len) {
+                            if (nc < 2) {
+                                if (nc == 0) { cb0 = cb; ca0 = a0; cl0 = len; }
+                                else { cb1 = cb; ca1 = a0; cl1 = len; }
+                                ++nc;
+                            } else {
+                                const int suf = a0 > 0 ? suffix_ones(ex.mask(a0 - 1, cb, cur_t)) : 0;
+                                const int pre = a0 + len < W ? prefix_ones(ex.mask(a0 + len, cb, cur_t)) : 0;
+                                if (suf + 32 * len + pre >= cur_t) best = min(best, enc_res(cb, 32 * a0 - suf));
+                            }
+                        });
+                    }
+                    for (;;) {
+                        const unsigned mk = __ballot_sync(0xFFFFFFFFu, nc > 0);
+                        if (!mk) break;
+                        const int src = __ffs(mk) - 1;
+                        const int mb = nc == 2 ? cb1 : cb0, ma = nc == 2 ? ca1 : ca0, ml = nc == 2 ? cl1 : cl0;
+                        const int b = __shfl_sync(0xFFFFFFFFu, mb, src);
+                        const int a0 = __shfl_sync(0xFFFFFFFFu, ma, src);
+                        const int len = __shfl_sync(0xFFFFFFFFu, ml, src);
+                        const int suf = a0 > 0 ? suffix_ones(ex.coop_mask(a0 - 1, b, cur_t, lane)) : 0;
+                        const int pre = a0 + len < W ? prefix_ones(ex.coop_mask(a0 + len, b, cur_t, lane)) : 0;
+                        if (lane == src) {
+                            if (suf + 32 * len + pre >= cur_t) best = min(best, enc_res(b, 32 * a0 - suf));
+                            --nc;
+                        }
                     }
                 } else {
                     for (int b = start_b; b <= lastb; ++b) {
