@@ -38,7 +38,7 @@ int num_sms() {
 }
 
 struct WsLayout {
-    size_t band_keys, fix_keys, e, b, ao, total;
+    size_t band_keys, fix_keys, zb, e, ao, carry, total;
 };
 
 WsLayout ws_layout(const msq_plan* p) {
@@ -54,9 +54,11 @@ WsLayout ws_layout(const msq_plan* p) {
     L.band_keys = take((size_t)p->batch * nb * 8);
     L.fix_keys = take(nb * 8);
     const bool summaries = p->batch == 1;
+    // per unit: last-zero rows during pass 1 (global scratch), bottom runs after
+    L.zb = take((size_t)p->batch * nb * cols_pad * 2);
     L.e = take(summaries ? nb * cols_pad * 2 : 0);
-    L.b = take(summaries ? nb * cols_pad * 2 : 0);
     L.ao = take(summaries ? nb * (size_t)p->words * 4 : 0);
+    L.carry = take(summaries ? nb * cols_pad * 2 : 0);
     L.total = off;
     return L;
 }
@@ -152,8 +154,8 @@ msq::Pass1Params make_pass1(const msq_plan* pl, const void* src, void* ws, msq_d
     p.team = pl->team;
     p.units = pl->nbands * pl->batch;
     p.layout_bytes = team_layout_bytes(pl);
+    p.zb = (uint16_t*)(w + L.zb);
     p.e_out = summaries ? (uint16_t*)(w + L.e) : nullptr;
-    p.b_out = summaries ? (uint16_t*)(w + L.b) : nullptr;
     p.ao_out = summaries ? (uint32_t*)(w + L.ao) : nullptr;
     p.band_keys = (unsigned long long*)(w + L.band_keys);
     p.results = (unsigned char*)res;
@@ -174,9 +176,7 @@ msq::FixParams make_fix(const msq_plan* pl, void* ws, const uint32_t* base, msq_
     f.bs = pl->tile_rows;
     f.bl = pl->tile_rows_l;
     f.e_in = (const uint16_t*)(w + L.e);
-    f.b_in = (const uint16_t*)(w + L.b);
-    f.ao_in = (const uint32_t*)(w + L.ao);
-    f.base_carry = base;
+    f.carry_in = (const uint16_t*)(w + L.carry);
     f.share = pl->deterministic ? 0 : 1;
     f.fix_keys = (unsigned long long*)(w + L.fix_keys);
     f.results = (unsigned char*)res;
@@ -184,6 +184,16 @@ msq::FixParams make_fix(const msq_plan* pl, void* ws, const uint32_t* base, msq_
 }
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? MSQ_OK : MSQ_ECUDA; }
+
+cudaError_t launch_carry(const msq_plan* pl, void* ws, const uint32_t* base, cudaStream_t st) {
+    WsLayout L = ws_layout(pl);
+    uint8_t* w = (uint8_t*)ws;
+    const int threads = 256;
+    msq::carry_scan_kernel<<<(int)ceil_div(pl->cols, threads), threads, 0, st>>>(
+        (int)pl->rows, (int)pl->cols, pl->words, pl->nbands, pl->words * 32, (const uint16_t*)(w + L.zb),
+        (const uint32_t*)(w + L.ao), base, (uint16_t*)(w + L.carry));
+    return cudaGetLastError();
+}
 
 // --------------------------------------------------- internal workspace
 struct DevCache {
@@ -325,6 +335,7 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
     }
     nb = (int)std::max<long long>(nb, ceil_div(rows, 65535));
     if (nb > rows) nb = (int)rows;
+    if (nb > 2048) return MSQ_EINVAL;
     if (batch > 1 && nb != 1) return MSQ_EINVAL;
     p.nbands = nb;
     p.grid = nb * batch;
@@ -334,7 +345,7 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
     if (tma_ok) {
         const int base = msq::p1_layout(p.threads, p.wpt, 0, (int)row_bytes, p.tile_rows, true).total;
         long long ns = (kSmemMax - base - 256) / row_bytes;
-        ns = std::min<long long>(ns, 16);
+        ns = std::min<long long>(ns, 24);
         // the ring must hold the previous tile (freed only after the next
         // tile's first barrier) plus the current one
         if (ns < 2 * p.tile_rows_l) p.tile_rows_l = p.tile_rows;
@@ -365,10 +376,12 @@ int msq_launch(const msq_plan* pl, const void* d_src, void* d_ws, msq_devresult*
     if (e != cudaSuccess) return MSQ_ECUDA;
     g_last_launches = 1;
     if (multi) {
+        e = launch_carry(pl, d_ws, nullptr, st);
+        if (e != cudaSuccess) return MSQ_ECUDA;
         msq::FixParams f = make_fix(pl, d_ws, nullptr, d_result);
         e = launch_fixup(pl, f, pl->nbands - 1, st);
         if (e != cudaSuccess) return MSQ_ECUDA;
-        g_last_launches = 2;
+        g_last_launches = 3;
     }
     return MSQ_OK;
 }
@@ -454,7 +467,7 @@ int msq_rank_summary(const msq_plan* pl, const void* d_ws, uint32_t* d_summary, 
     const int threads = 256;
     const int blocks = (int)ceil_div(pl->cols, threads);
     msq::rank_summary_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
-        (int)pl->rows, (int)pl->cols, pl->words, pl->nbands, pl->words * 32, (const uint16_t*)(w + L.b),
+        (int)pl->rows, (int)pl->cols, pl->words, pl->nbands, pl->words * 32, (const uint16_t*)(w + L.zb),
         (const uint32_t*)(w + L.ao), d_summary);
     return cuda_status(cudaGetLastError());
 }
@@ -475,6 +488,8 @@ int msq_compose_carry(const uint32_t* d_summaries, const int64_t* h_rank_rows, i
 int msq_rank_fixup(const msq_plan* pl, void* d_ws, const uint32_t* d_base_carry, msq_devresult* d_result,
                    void* stream) {
     if (!pl || !d_ws || !d_result || pl->batch != 1) return MSQ_EINVAL;
+    cudaError_t e = launch_carry(pl, d_ws, d_base_carry, (cudaStream_t)stream);
+    if (e != cudaSuccess) return MSQ_ECUDA;
     msq::FixParams f = make_fix(pl, d_ws, d_base_carry, d_result);
     const int nblocks = pl->nbands - f.band_begin;
     return cuda_status(launch_fixup(pl, f, nblocks, (cudaStream_t)stream));
@@ -486,7 +501,7 @@ int msq_ws_views(const msq_plan* pl, void* d_ws, uint16_t** e, uint16_t** b, uin
     WsLayout L = ws_layout(pl);
     uint8_t* w = (uint8_t*)d_ws;
     if (e) *e = (uint16_t*)(w + L.e);
-    if (b) *b = (uint16_t*)(w + L.b);
+    if (b) *b = (uint16_t*)(w + L.zb);
     if (allones) *allones = (uint32_t*)(w + L.ao);
     if (band_keys) *band_keys = (uint64_t*)(w + L.band_keys);
     return MSQ_OK;

@@ -51,15 +51,16 @@ __host__ __device__ __forceinline__ unsigned long long pack_key(long long side, 
            (KEY_DIM_MASK - (unsigned long long)right);
 }
 
+// rows < 2^21 and nbands <= 2048, so the product fits in 32 unsigned bits
 __host__ __device__ __forceinline__ int band_row0(int rows, int nbands, int band) {
-    return (int)(((long long)rows * band) / nbands);
+    return (int)(((unsigned)rows * (unsigned)band) / (unsigned)nbands);
 }
 
 __host__ __device__ __forceinline__ int r16(int x) { return (x + 15) & ~15; }
 
 // ------------------------------------------------------------ smem layouts
 struct P1Layout {
-    int ring, bars, zs, za, hist, fmap, misc, total;
+    int ring, bars, nz, za, hist, fmap, misc, total;
 };
 // per team; hist holds bs rows of E words, fmap 2 x BMAX rows of F bits
 __host__ __device__ inline P1Layout p1_layout(int NT, int WPT, int nstage, int rs, int bs, bool tma) {
@@ -70,8 +71,8 @@ __host__ __device__ inline P1Layout p1_layout(int NT, int WPT, int nstage, int r
     if (tma) off += nstage * rs;
     L.bars = off;
     if (tma) off += r16(nstage * 8);
-    L.zs = off;
-    off += wpad * 32 * 2;
+    L.nz = off;
+    off += r16(wpad * 4);
     L.za = off;
     off += r16(wpad * 2);
     L.hist = off;
@@ -121,11 +122,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                  "r"(bytes)
                  : "memory");
 }
-__device__ __forceinline__ void tma_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+// streaming rows are read once: evict them first so the band summaries stay in L2
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
             smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
         : "memory");
 }
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
@@ -260,8 +267,8 @@ struct Pass1Params {
     int team;                   // threads per team
     int units;                  // nbands * batch
     int layout_bytes;           // per-team smem bytes
+    uint16_t* zb;               // [units][cols_pad] last-zero rows during the pass, bottom runs after
     uint16_t* e_out;
-    uint16_t* b_out;
     uint32_t* ao_out;
     unsigned long long* band_keys;
     unsigned char* results;
@@ -273,9 +280,7 @@ struct FixParams {
     int band_begin;
     int bs, bl;
     const uint16_t* e_in;
-    const uint16_t* b_in;
-    const uint32_t* ao_in;
-    const uint32_t* base_carry;
+    const uint16_t* carry_in;  // [nbands][cols_pad] carry-in heights (clamped 65535)
     int share;
     unsigned long long* fix_keys;
     unsigned char* results;
@@ -457,10 +462,13 @@ __device__ __forceinline__ int prefix_ones(uint32_t m) { return m == 0xFFFFFFFFu
 
 // pass-1 exact eligibility of word a at tile row b, threshold T (T > BMAX):
 // column j eligible iff no zero in the tile rows <= b and its last zero before
-// the tile (max(zs, za)) is <= rho_b - T.  zs is word-major: zs[a*32 + j].
+// the tile (max(z, za)) is <= rho_b - T.  z lives in global scratch (word-major
+// zs[a*32 + j], L2-resident) and is valid only where the never-zeroed mask
+// nz[a] is clear (no initialisation needed).
 template <bool U8, bool TMA>
 struct Pass1Exact {
     const uint16_t* zs;
+    const uint32_t* nz;
     const uint16_t* za;
     const uint8_t* ring;
     const uint8_t* mbase;
@@ -482,7 +490,7 @@ struct Pass1Exact {
         uint32_t zin = 0;
         for (int q = 0; q <= b; ++q) zin |= ~word_of_row<U8, TMA>(srow(q), grow(q), a, cols, rs);
         const uint4* zp = (const uint4*)(zs + (size_t)a * 32);
-        uint32_t m = 0;
+        uint32_t m = nz[a];  // never zeroed in the band: eligible (lim >= 0 here)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const uint4 v = zp[q];
@@ -499,7 +507,8 @@ struct Pass1Exact {
     __device__ uint32_t coop_mask(int a, int b, int T, int lane) const {
         const uint32_t val = valid_mask(a, W, cols);
         const int lim = tile_row0 + b + 1 - T;
-        bool el = ((val >> lane) & 1u) && (int)za[a] <= lim && (int)zs[(size_t)a * 32 + lane] <= lim;
+        const bool never = (nz[a] >> lane) & 1u;
+        bool el = ((val >> lane) & 1u) && (int)za[a] <= lim && (never || (int)zs[(size_t)a * 32 + lane] <= lim);
         for (int q = 0; q <= b; ++q) {
             uint32_t one;
             if (U8) {
@@ -589,7 +598,8 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     uint8_t* tsm = smem + (size_t)team_idx * p.layout_bytes;
     uint8_t* ring = tsm + Lo.ring;
     uint64_t* bars = (uint64_t*)(tsm + Lo.bars);
-    uint16_t* zs = (uint16_t*)(tsm + Lo.zs);  // word-major: zs[a*32 + j]
+    uint16_t* zs = p.zb + (size_t)unit * p.cols_pad;  // global, word-major: zs[a*32 + j]
+    uint32_t* nzs = (uint32_t*)(tsm + Lo.nz);          // never-zeroed masks (mirror of NZ)
     uint16_t* za = (uint16_t*)(tsm + Lo.za);
     uint32_t* hist = (uint32_t*)(tsm + Lo.hist);
     uint32_t* fmap = (uint32_t*)(tsm + Lo.fmap);
@@ -611,7 +621,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 #pragma unroll
         for (int q = 0; q < NPLANES; ++q) HC[k][q] = 0;
     }
-    for (int i = tau; i < Wpad * 16; i += NT) ((uint32_t*)zs)[i] = 0u;
+    for (int i = tau; i < Wpad; i += NT) nzs[i] = valid_mask(i, W, p.cols);
     for (int i = tau; i < Wpad; i += NT) za[i] = 0;
     for (int i = tau; i < 2 * BMAX * fstride; i += NT) fmap[i] = 0u;
     if (tau == 0) {
@@ -625,12 +635,13 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     tsync<SUB>(tmask);
 
     int issued = 0;  // next band row to stage (producer thread)
+    const uint64_t pol = TMA ? l2_evict_first_policy() : 0ull;
     if (TMA && tau == 0) {
         for (; issued < min(p.nstage, H); ++issued) {
             const int s = issued % p.nstage;
             mbar_expect_tx(&bars[s], (uint32_t)p.row_bytes);
             tma_row(ring + (size_t)s * p.rs, mbase + (size_t)(r0 + issued) * p.ld_bytes, (uint32_t)p.row_bytes,
-                    &bars[s]);
+                    &bars[s], pol);
         }
     }
 
@@ -660,7 +671,8 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 if (a < W) {
                     const int zaa = za[a];
                     for (int j = 0; j < 32; ++j) {
-                        const int h = min(rho0 - 1 - max((int)zs[(size_t)a * 32 + j], zaa), 127);
+                        const int zj = ((NZ[k] >> j) & 1u) ? 0 : (int)zs[(size_t)a * 32 + j];
+                        const int h = min(rho0 - 1 - max(zj, zaa), 127);
 #pragma unroll
                         for (int q = 0; q < NPLANES; ++q) HC[k][q] |= (uint32_t)((h >> q) & 1) << j;
                     }
@@ -722,14 +734,14 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 const int s = issued % p.nstage;
                 mbar_expect_tx(&bars[s], (uint32_t)p.row_bytes);
                 tma_row(ring + (size_t)s * p.rs, mbase + (size_t)(r0 + issued) * p.ld_bytes,
-                        (uint32_t)p.row_bytes, &bars[s]);
+                        (uint32_t)p.row_bytes, &bars[s], pol);
             }
         }
 
         // ---------------------------------------------------- phase B
         const int lastb = nrows - 1;
         int cur_t = t;
-        const Pass1Exact<U8, TMA> ex{zs, za, ring, mbase, p.ld_bytes, W, p.cols, p.rs, p.nstage, row0, r0};
+        const Pass1Exact<U8, TMA> ex{zs, nzs, za, ring, mbase, p.ld_bytes, W, p.cols, p.rs, p.nstage, row0, r0};
         if (climb) {
             if (t == rho0) {  // E = prefix-AND of the band top; find the leftmost t-window
                 int start = -1;
@@ -871,15 +883,26 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 }
             }
             uint32_t newly = NZ[k] & zeros;
-            if (newly && p.write_summaries) {
-                const size_t cb = sum_base + (size_t)a * 32;
-                while (newly) {
-                    const int j = __ffs(newly) - 1;
-                    newly &= newly - 1;
-                    p.e_out[cb + j] = (uint16_t)(rho - 1);
+            if (newly) {
+                if (zeros == VAL[k]) {  // the lazy all-zero row is the first zero of these columns
+                    uint32_t nn = newly;
+                    while (nn) {
+                        const int j = __ffs(nn) - 1;
+                        nn &= nn - 1;
+                        zs[(size_t)a * 32 + j] = 0;
+                    }
                 }
+                if (p.write_summaries) {
+                    const size_t cb = sum_base + (size_t)a * 32;
+                    while (newly) {
+                        const int j = __ffs(newly) - 1;
+                        newly &= newly - 1;
+                        p.e_out[cb + j] = (uint16_t)(rho - 1);
+                    }
+                }
+                NZ[k] &= ~zeros;
+                nzs[a] = NZ[k];
             }
-            NZ[k] &= ~zeros;
         }
         if (modeL)
             for (int i = tau; i < BMAX * fstride; i += NT) fm[i] = 0u;
@@ -901,8 +924,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     p.e_out[cb + j] = (uint16_t)H;
                 }
                 const int zaa = za[a];
-                const uint4* zp = (const uint4*)(zs + (size_t)a * 32);
-                uint4* dst = (uint4*)(p.b_out + cb);
+                uint4* zp = (uint4*)(zs + (size_t)a * 32);  // bottom runs overwrite the last-zero rows
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const uint4 zv = zp[q];
@@ -910,11 +932,12 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     uint32_t v[4];
 #pragma unroll
                     for (int h = 0; h < 4; ++h) {
-                        const int u0 = max((int)(pr[h] & 0xFFFFu), zaa);
-                        const int u1 = max((int)(pr[h] >> 16), zaa);
+                        const int j0 = 8 * q + 2 * h;
+                        const int u0 = ((NZ[k] >> j0) & 1u) ? 0 : max((int)(pr[h] & 0xFFFFu), zaa);
+                        const int u1 = ((NZ[k] >> (j0 + 1)) & 1u) ? 0 : max((int)(pr[h] >> 16), zaa);
                         v[h] = (uint32_t)(H - u0) | ((uint32_t)(H - u1) << 16);
                     }
-                    dst[q] = make_uint4(v[0], v[1], v[2], v[3]);
+                    zp[q] = make_uint4(v[0], v[1], v[2], v[3]);
                 }
                 p.ao_out[(size_t)band * W + a] = NZ[k];
             }
@@ -1019,36 +1042,12 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
         for (int q = 0; q < FIX_XPL; ++q) CP[k][q] = EP[k][q] = 0;
         if (!v) continue;
         uint16_t* uw = us + (size_t)a * 32;
-        // ---- carry-in heights by look-back over the bands above (P5), 8 bands per step
-        uint32_t pending = v;
-        long long acc = 0;
-        for (int q0 = band - 1; q0 >= 0 && pending; q0 -= 8) {
-            uint32_t mq[8];
+        // ---- carry-in heights (carry_scan_kernel) for this band
+        {
+            const uint4* cp4 = (const uint4*)(p.carry_in + (size_t)band * p.cols_pad + (size_t)32 * a);
+            uint4* up4 = (uint4*)uw;
 #pragma unroll
-            for (int s = 0; s < 8; ++s) mq[s] = (q0 - s >= 0) ? p.ao_in[(size_t)(q0 - s) * W + a] : 0u;
-#pragma unroll
-            for (int s = 0; s < 8; ++s) {
-                const int q = q0 - s;
-                if (q >= 0 && pending) {
-                    const uint32_t res = pending & ~mq[s];
-                    if (res) {
-                        const uint16_t* bq = p.b_in + (size_t)q * p.cols_pad + (size_t)32 * a;
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if ((res >> j) & 1u) uw[j] = (uint16_t)min(acc + bq[j], 65535ll);
-                    }
-                    pending &= mq[s];
-                    acc += band_row0(p.rows, p.nbands, q + 1) - band_row0(p.rows, p.nbands, q);
-                }
-            }
-        }
-        if (pending) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-                if ((pending >> j) & 1u) {
-                    const long long c = acc + (p.base_carry ? (long long)p.base_carry[32 * a + j] : 0ll);
-                    uw[j] = (uint16_t)min(c, 65535ll);
-                }
+            for (int q = 0; q < 4; ++q) up4[q] = cp4[q];
         }
         // ---- leading-ones depth of the band top, per-word minima, mode X planes
         const uint4* ep = (const uint4*)(e_g + (size_t)32 * a);
@@ -1261,6 +1260,38 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
     if (tau == 0) {
         if (p.fix_keys) p.fix_keys[band] = fixkey;
         if (fixkey) atomicMax(res_keyfix(result), fixkey);
+    }
+}
+
+// ======================================================= carries (P5 fold)
+// carry[k][j] = true height of column j at the row above band k (clamped to
+// 65535; exact for cols <= 65536): fold (b, all-ones) of the
+// bands above, starting from base[j] (rows above this rank; 0 on one GPU).
+__global__ void carry_scan_kernel(int rows, int cols, int W, int nbands, int cols_pad, const uint16_t* b_in,
+                                  const uint32_t* ao_in, const uint32_t* base, uint16_t* carry_out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= cols) return;
+    unsigned c = base ? base[j] : 0u;
+    carry_out[j] = (uint16_t)min(c, 65535u);
+    constexpr int U = 8;
+    for (int q0 = 0; q0 < nbands - 1; q0 += U) {
+        uint32_t fw[U];
+        uint16_t bv[U];
+#pragma unroll
+        for (int s = 0; s < U; ++s) {
+            const int q = q0 + s;
+            fw[s] = q < nbands - 1 ? ao_in[(size_t)q * W + (j >> 5)] : 0u;
+            bv[s] = q < nbands - 1 ? b_in[(size_t)q * cols_pad + j] : (uint16_t)0;
+        }
+#pragma unroll
+        for (int s = 0; s < U; ++s) {
+            const int q = q0 + s;
+            if (q < nbands - 1) {
+                const unsigned hq = (unsigned)(band_row0(rows, nbands, q + 1) - band_row0(rows, nbands, q));
+                c = ((fw[s] >> (j & 31)) & 1u) ? min(c + hq, 0x7FFFFFFFu) : (unsigned)bv[s];
+                carry_out[(size_t)(q + 1) * cols_pad + j] = (uint16_t)min(c, 65535u);
+            }
+        }
     }
 }
 
