@@ -149,6 +149,10 @@ int msq_gen_hash(int32_t fmt, uint64_t seed, uint64_t thr53, int64_t row0, int64
 /* Number of kernel launches the last msq_launch enqueued (instrumentation). */
 int32_t msq_last_launch_count(void);
 
+/* Debug instrumentation: when set, each pass-1 unit writes 16 uint64 phase
+ * cycle counters to d_counters[unit*16..] (NULL disables; tools only). */
+void msq_debug_set_profile(void* d_counters);
+
 const char* msq_strerror(int code);
 const char* msq_version(void);
 

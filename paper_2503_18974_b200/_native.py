@@ -82,6 +82,7 @@ def load():
         "msq_ws_views": ([PP, P, P, P, P, P], ctypes.c_int),
         "msq_gen_hash": ([I32, U64, U64, I64, I64, I64, I64, P, P], ctypes.c_int),
         "msq_last_launch_count": ([], I32),
+        "msq_debug_set_profile": ([P], None),
         "msq_strerror": ([ctypes.c_int], ctypes.c_char_p),
         "msq_version": ([], ctypes.c_char_p),
     }

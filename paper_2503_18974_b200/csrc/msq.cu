@@ -20,6 +20,7 @@ constexpr int kModeLThreshold = 96;  // >= 63 (see msq_engine.cuh)
 constexpr int kMaxWords = 2048;   // 65536 columns
 
 thread_local int32_t g_last_launches = 0;
+unsigned long long* g_prof = nullptr;  // debug: per-unit phase counters
 
 inline long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
 inline long long round_up(long long a, long long b) { return ceil_div(a, b) * b; }
@@ -64,6 +65,16 @@ WsLayout ws_layout(const msq_plan* p) {
 }
 
 // ------------------------------------------------------------- dispatch
+int zplanes_for(const msq_plan* pl) {
+    const long long hmax = ceil_div(pl->rows, pl->nbands);
+    int P = 1;
+    while ((1ll << P) <= hmax) ++P;
+    return P;
+}
+
+bool uses_producer_warp(const msq_plan* pl) { return pl->teams_per_cta == 1 && pl->team == pl->threads - 32; }
+
+
 template <class K>
 cudaError_t set_smem_attr(K kern, bool* done) {
     int dev = 0;
@@ -99,7 +110,7 @@ cudaError_t launch_fixup_t(const msq_plan* pl, const msq::FixParams& prm, int nb
 cudaError_t launch_pass1(const msq_plan* pl, const msq::Pass1Params& prm, cudaStream_t st) {
     const bool u8 = pl->fmt == MSQ_FMT_U8;
     const bool tma = pl->nstage > 0;
-    const bool sub = pl->team < pl->threads || pl->teams_per_cta > 1;
+    const bool sub = pl->teams_per_cta > 1 || (pl->team < pl->threads && !uses_producer_warp(pl));
 #define MSQ_P1(W_, U_, T_, S_) \
     if (pl->wpt == W_ && u8 == U_ && tma == T_ && sub == S_) return launch_pass1_t<W_, U_, T_, S_>(pl, prm, st);
     MSQ_P1(1, true, true, true) MSQ_P1(1, true, false, true) MSQ_P1(1, false, true, true)
@@ -125,7 +136,9 @@ cudaError_t launch_fixup(const msq_plan* pl, const msq::FixParams& prm, int nblo
 }
 
 int team_layout_bytes(const msq_plan* pl) {
-    return msq::p1_layout(pl->team, pl->wpt, pl->nstage, pl->row_stage_bytes, pl->tile_rows, pl->nstage > 0).total;
+    return msq::p1_layout(pl->team, pl->wpt, pl->nstage, pl->row_stage_bytes, pl->tile_rows, zplanes_for(pl),
+                          pl->nstage > 0, uses_producer_warp(pl))
+        .total;
 }
 
 msq::Pass1Params make_pass1(const msq_plan* pl, const void* src, void* ws, msq_devresult* res,
@@ -152,6 +165,8 @@ msq::Pass1Params make_pass1(const msq_plan* pl, const void* src, void* ws, msq_d
     p.share = (pl->deterministic || pl->nbands == 1) ? 0 : 1;
     p.write_summaries = summaries ? 1 : 0;
     p.team = pl->team;
+    p.teams_per_cta = pl->teams_per_cta;
+    p.zplanes = zplanes_for(pl);
     p.units = pl->nbands * pl->batch;
     p.layout_bytes = team_layout_bytes(pl);
     p.zb = (uint16_t*)(w + L.zb);
@@ -159,6 +174,7 @@ msq::Pass1Params make_pass1(const msq_plan* pl, const void* src, void* ws, msq_d
     p.ao_out = summaries ? (uint32_t*)(w + L.ao) : nullptr;
     p.band_keys = (unsigned long long*)(w + L.band_keys);
     p.results = (unsigned char*)res;
+    p.prof = g_prof;
     return p;
 }
 
@@ -304,7 +320,9 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
         tpc = std::min<long long>(tpc, 512 / ts);
         p.nstage = tma_ok ? 2 * msq::BMAX : 0;  // ring holds the previous and the current tile
         for (;;) {
-            const long long per = msq::p1_layout(ts, 1, p.nstage, (int)row_bytes, p.tile_rows, p.nstage > 0).total;
+            const long long per = msq::p1_layout(ts, 1, p.nstage, (int)row_bytes, p.tile_rows, zplanes_for(&p),
+                                                 p.nstage > 0, false)
+                                      .total;
             if (per * tpc <= kSmemMax) break;
             if (p.nstage > 0) {
                 p.nstage = 0;
@@ -316,7 +334,7 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
         p.teams_per_cta = (int32_t)tpc;
         p.threads = (int32_t)round_up(tpc * ts, 32);
         p.grid = (int32_t)ceil_div(batch, tpc);
-        p.smem_pass1 = (int32_t)(tpc * msq::p1_layout(ts, 1, p.nstage, (int)row_bytes, p.tile_rows, p.nstage > 0).total);
+        p.smem_pass1 = (int32_t)(tpc * team_layout_bytes(&p));
         p.smem_fixup = 0;
         p.ws_bytes = (int64_t)ws_layout(&p).total;
         *plan = p;
@@ -342,16 +360,20 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
     p.tile_rows = 2;
     p.tile_rows_l = msq::BMAX;
     p.nstage = 0;
+    const int P = zplanes_for(&p);
     if (tma_ok) {
-        const int base = msq::p1_layout(p.threads, p.wpt, 0, (int)row_bytes, p.tile_rows, true).total;
-        long long ns = (kSmemMax - base - 256) / row_bytes;
-        ns = std::min<long long>(ns, 24);
-        // the ring must hold the previous tile (freed only after the next
-        // tile's first barrier) plus the current one
+        // a producer warp streams rows; a stage is refilled as soon as its row
+        // is released, so the ring only has to hold one tile (more = deeper prefetch)
+        const int base = msq::p1_layout(p.threads, p.wpt, 0, (int)row_bytes, p.tile_rows, P, true, true).total;
+        long long ns = (kSmemMax - base - 512) / row_bytes;
+        ns = std::min<long long>(ns, 32);
         if (ns < 2 * p.tile_rows_l) p.tile_rows_l = p.tile_rows;
-        if (ns >= 2 * p.tile_rows_l) p.nstage = (int32_t)ns;
+        if (ns >= 2 * p.tile_rows_l) {
+            p.nstage = (int32_t)ns;
+            p.threads += 32;  // + producer warp (team stays the consumer count)
+        }
     }
-    p.smem_pass1 = msq::p1_layout(p.threads, p.wpt, p.nstage, (int)row_bytes, p.tile_rows, p.nstage > 0).total;
+    p.smem_pass1 = team_layout_bytes(&p);
     p.smem_fixup = msq::fix_layout(p.threads, p.wpt, p.tile_rows).total;
     if (p.smem_pass1 > kSmemMax || p.smem_fixup > kSmemMax) return MSQ_EINVAL;
     p.ws_bytes = (int64_t)ws_layout(&p).total;
@@ -523,6 +545,8 @@ int msq_gen_hash(int32_t fmt, uint64_t seed, uint64_t thr53, int64_t row0, int64
 }
 
 int32_t msq_last_launch_count(void) { return g_last_launches; }
+
+void msq_debug_set_profile(void* d_counters) { g_prof = (unsigned long long*)d_counters; }
 
 const char* msq_strerror(int code) {
     switch (code) {

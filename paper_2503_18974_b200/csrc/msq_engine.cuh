@@ -60,10 +60,13 @@ __host__ __device__ __forceinline__ int r16(int x) { return (x + 15) & ~15; }
 
 // ------------------------------------------------------------ smem layouts
 struct P1Layout {
-    int ring, bars, nz, za, hist, fmap, misc, total;
+    int ring, bars, ebars, zp, hist, fmap, misc, total;
 };
-// per team; hist holds bs rows of E words, fmap 2 x BMAX rows of F bits
-__host__ __device__ inline P1Layout p1_layout(int NT, int WPT, int nstage, int rs, int bs, bool tma) {
+// per team; zp holds P bit-planes of the last-zero rows, hist bs rows of E
+// words, fmap 2 x BMAX rows of F bits; ebars = empty barriers of the
+// producer-warp ring (CTA teams)
+__host__ __device__ inline P1Layout p1_layout(int NT, int WPT, int nstage, int rs, int bs, int P, bool tma,
+                                              bool ebar) {
     P1Layout L;
     const int wpad = NT * WPT, nfw = (wpad + 31) / 32;
     int off = 0;
@@ -71,10 +74,10 @@ __host__ __device__ inline P1Layout p1_layout(int NT, int WPT, int nstage, int r
     if (tma) off += nstage * rs;
     L.bars = off;
     if (tma) off += r16(nstage * 8);
-    L.nz = off;
-    off += r16(wpad * 4);
-    L.za = off;
-    off += r16(wpad * 2);
+    L.ebars = off;
+    if (ebar) off += r16(nstage * 8);
+    L.zp = off;
+    off += P * wpad * 4;
     L.hist = off;
     off += bs * wpad * 4;
     L.fmap = off;
@@ -265,13 +268,16 @@ struct Pass1Params {
     int tl;                     // mode L threshold
     int share, write_summaries;
     int team;                   // threads per team
+    int teams_per_cta;
+    int zplanes;                // bit planes of the last-zero rows (2^P > band height)
     int units;                  // nbands * batch
     int layout_bytes;           // per-team smem bytes
-    uint16_t* zb;               // [units][cols_pad] last-zero rows during the pass, bottom runs after
+    uint16_t* zb;               // [units][cols_pad] bottom runs (band outputs)
     uint16_t* e_out;
     uint32_t* ao_out;
     unsigned long long* band_keys;
     unsigned char* results;
+    unsigned long long* prof;  // optional [units][16] phase-cycle counters (thread 0)
 };
 
 struct FixParams {
@@ -461,19 +467,38 @@ __device__ __forceinline__ int suffix_ones(uint32_t m) { return __clz(~m); }
 __device__ __forceinline__ int prefix_ones(uint32_t m) { return m == 0xFFFFFFFFu ? 32 : __ffs(~m) - 1; }
 
 // pass-1 exact eligibility of word a at tile row b, threshold T (T > BMAX):
-// column j eligible iff no zero in the tile rows <= b and its last zero before
-// the tile (max(z, za)) is <= rho_b - T.  z lives in global scratch (word-major
-// zs[a*32 + j], L2-resident) and is valid only where the never-zeroed mask
-// nz[a] is clear (no initialisation needed).
+// column j is eligible iff no zero in the tile rows <= b and its last zero
+// before the tile, z_j, is <= rho_b - T.  z is kept bit-sliced in smem
+// (zp[p*Wpad + k*NT + tau] = bit p of z for the 32 columns of word
+// a = tau*WPT + k; z = 0 means "no zero in the band yet"), so the test is a
+// bit-sliced compare with a warp-uniform constant.
+__device__ __forceinline__ int zp_index(int a, int p, int WPT, int NT, int Wpad) {
+    const int tau = a / WPT, k = a - tau * WPT;
+    return p * Wpad + k * NT + tau;
+}
+
+// bit-sliced "Z <= c" over P planes (c < 2^P)
+__device__ __forceinline__ uint32_t planes_le(const uint32_t* zp, int base, int stride, int P, int c) {
+    uint32_t lt = 0, eq = 0xFFFFFFFFu;
+    for (int p = P - 1; p >= 0; --p) {
+        const uint32_t zb = zp[base + p * stride];
+        if ((c >> p) & 1) {
+            lt |= eq & ~zb;
+            eq &= zb;
+        } else {
+            eq &= ~zb;
+        }
+    }
+    return lt | eq;
+}
+
 template <bool U8, bool TMA>
 struct Pass1Exact {
-    const uint16_t* zs;
-    const uint32_t* nz;
-    const uint16_t* za;
+    const uint32_t* zp;
     const uint8_t* ring;
     const uint8_t* mbase;
     long long ld_bytes;
-    int W, cols, rs, nstage;
+    int W, cols, rs, nstage, P, WPT, NT, Wpad;
     int tile_row0;  // band-relative 0-based row of tile row 0
     int r0;         // band top row (matrix)
     __device__ __forceinline__ const uint8_t* srow(int b) const {
@@ -482,44 +507,14 @@ struct Pass1Exact {
     __device__ __forceinline__ const uint8_t* grow(int b) const {
         return mbase + (size_t)(r0 + tile_row0 + b) * ld_bytes;
     }
-    // one thread computes the whole mask (sub-warp teams, overflow path)
     __device__ uint32_t mask(int a, int b, int T) const {
         const uint32_t val = valid_mask(a, W, cols);
         const int lim = tile_row0 + b + 1 - T;
-        if ((int)za[a] > lim) return 0u;
+        if (lim < 0) return 0u;
         uint32_t zin = 0;
         for (int q = 0; q <= b; ++q) zin |= ~word_of_row<U8, TMA>(srow(q), grow(q), a, cols, rs);
-        const uint4* zp = (const uint4*)(zs + (size_t)a * 32);
-        uint32_t m = nz[a];  // never zeroed in the band: eligible (lim >= 0 here)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint4 v = zp[q];
-            const uint32_t pr[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                m |= ((int)(pr[h] & 0xFFFFu) <= lim ? 1u : 0u) << (8 * q + 2 * h);
-                m |= ((int)(pr[h] >> 16) <= lim ? 1u : 0u) << (8 * q + 2 * h + 1);
-            }
-        }
-        return m & val & ~zin;
-    }
-    // one full warp, lane = column
-    __device__ uint32_t coop_mask(int a, int b, int T, int lane) const {
-        const uint32_t val = valid_mask(a, W, cols);
-        const int lim = tile_row0 + b + 1 - T;
-        const bool never = (nz[a] >> lane) & 1u;
-        bool el = ((val >> lane) & 1u) && (int)za[a] <= lim && (never || (int)zs[(size_t)a * 32 + lane] <= lim);
-        for (int q = 0; q <= b; ++q) {
-            uint32_t one;
-            if (U8) {
-                one = TMA ? srow(q)[(size_t)a * 32 + lane] : ((a * 32 + lane < cols) ? grow(q)[a * 32 + lane] : 0);
-                one = one != 0;
-            } else {
-                one = (word_of_row<U8, TMA>(srow(q), grow(q), a, cols, rs) >> lane) & 1u;
-            }
-            el = el && one;
-        }
-        return __ballot_sync(0xFFFFFFFFu, el);
+        const uint32_t le = (lim >= (1 << P)) ? 0xFFFFFFFFu : planes_le(zp, zp_index(a, 0, WPT, NT, Wpad), Wpad, P, lim);
+        return le & val & ~zin;
     }
 };
 
@@ -571,8 +566,10 @@ __device__ int warp_first_window(const uint32_t* X, int W, int s0, int T, int la
 // Tile kinds: CLIMB (t >= rho: heights <= rho, so E = prefix-AND of the band
 // top when t == rho; 1 row per tile, one warp finds the leftmost window),
 // S (t < tl: bit-sliced counters), L (t >= tl: word-level F filter).
+// CTA teams: warps 0..NT/32-1 consume; one extra warp streams rows with TMA
+// (full/empty mbarrier ring).  Sub-warp teams: lane 0 of the team streams.
 template <int WPT, bool U8, bool TMA, bool SUB>
-__global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
+__global__ void __maxnreg__(120) pass1_kernel(const Pass1Params p) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int NT = p.team;
     const int tid = threadIdx.x;
@@ -581,9 +578,9 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     const int tau = SUB ? tid - team_idx * NT : tid;
     const unsigned tmask =
         SUB ? (unsigned)((NT >= 32 ? 0xFFFFFFFFull : ((1ull << NT) - 1ull)) << (lane - (tau & 31))) : 0xFFFFFFFFu;
-    const int teams_per_cta = SUB ? (int)blockDim.x / NT : 1;
+    const int teams_per_cta = SUB ? p.teams_per_cta : 1;
     const int unit = blockIdx.x * teams_per_cta + team_idx;
-    if (unit >= p.units) return;  // whole idle team (sub-warp teams only)
+    if (SUB && (team_idx >= teams_per_cta || unit >= p.units)) return;
     const int band = unit % p.nbands;
     const int mat = unit / p.nbands;
     const int W = p.W;
@@ -592,21 +589,77 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     const int fstride = r16(nfw * 4) / 4;
     const int r0 = band_row0(p.rows, p.nbands, band);
     const int H = band_row0(p.rows, p.nbands, band + 1) - r0;
+    const int P = p.zplanes;
     unsigned char* result = p.results + (size_t)mat * 32;
 
-    const P1Layout Lo = p1_layout(NT, WPT, p.nstage, p.rs, p.bs, TMA);
+    const P1Layout Lo = p1_layout(NT, WPT, p.nstage, p.rs, p.bs, P, TMA, !SUB && TMA);
     uint8_t* tsm = smem + (size_t)team_idx * p.layout_bytes;
     uint8_t* ring = tsm + Lo.ring;
     uint64_t* bars = (uint64_t*)(tsm + Lo.bars);
-    uint16_t* zs = p.zb + (size_t)unit * p.cols_pad;  // global, word-major: zs[a*32 + j]
-    uint32_t* nzs = (uint32_t*)(tsm + Lo.nz);          // never-zeroed masks (mirror of NZ)
-    uint16_t* za = (uint16_t*)(tsm + Lo.za);
+    uint64_t* ebars = (uint64_t*)(tsm + Lo.ebars);
+    uint32_t* zp = (uint32_t*)(tsm + Lo.zp);  // bit-sliced last-zero rows
     uint32_t* hist = (uint32_t*)(tsm + Lo.hist);
     uint32_t* fmap = (uint32_t*)(tsm + Lo.fmap);
     Misc* misc = (Misc*)(tsm + Lo.misc);
-
     const uint8_t* mbase = p.src + (size_t)mat * p.batch_stride;
     const size_t sum_base = (size_t)band * p.cols_pad;
+    const uint64_t pol = TMA ? l2_evict_first_policy() : 0ull;
+    const bool producer_warp = !SUB && TMA && tid >= NT;  // CTA teams only
+    const int nconsumer_warps = NT / 32;
+
+    // ---- setup (all threads, including the producer warp)
+    for (int i = tid; i < P * Wpad; i += blockDim.x) {
+        if (!SUB) zp[i] = 0u;
+    }
+    if (SUB)
+        for (int i = tau; i < P * Wpad; i += NT) zp[i] = 0u;
+    for (int i = (SUB ? tau : tid); i < 2 * BMAX * fstride; i += (SUB ? NT : (int)blockDim.x)) fmap[i] = 0u;
+    if (tau == 0) {
+        misc->res[0] = misc->res[1] = misc->res[2] = RES_INF;
+        misc->g = p.share ? ld_volatile(res_best(result)) : 0;
+        if (TMA) {
+            for (int s = 0; s < p.nstage; ++s) {
+                mbar_init(&bars[s], 1);
+                if (!SUB) mbar_init(&ebars[s], nconsumer_warps);
+            }
+            fence_mbar_init();
+        }
+    }
+    if (SUB)
+        tsync<true>(tmask);
+    else
+        __syncthreads();
+
+    if (producer_warp) {  // ------------------------------ TMA producer warp
+        if (lane == 0) {
+            for (int r = 0; r < H; ++r) {
+                const int s = r % p.nstage;
+                if (r >= p.nstage) mbar_wait(&ebars[s], (uint32_t)(((r / p.nstage) - 1) & 1));
+                mbar_expect_tx(&bars[s], (uint32_t)p.row_bytes);
+                tma_row(ring + (size_t)s * p.rs, mbase + (size_t)(r0 + r) * p.ld_bytes, (uint32_t)p.row_bytes,
+                        &bars[s], pol);
+            }
+        }
+        return;
+    }
+    auto csync = [&]() {  // consumer-only barrier
+        if (SUB)
+            __syncwarp(tmask);
+        else if (TMA)
+            asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");
+        else
+            __syncthreads();
+    };
+
+    int issued = 0;  // sub-warp teams: lane 0 streams rows itself
+    if (SUB && TMA && tau == 0) {
+        for (; issued < min(p.nstage, H); ++issued) {
+            const int s = issued % p.nstage;
+            mbar_expect_tx(&bars[s], (uint32_t)p.row_bytes);
+            tma_row(ring + (size_t)s * p.rs, mbase + (size_t)(r0 + issued) * p.ld_bytes, (uint32_t)p.row_bytes,
+                    &bars[s], pol);
+        }
+    }
 
     uint32_t VAL[WPT], NZ[WPT], EPREV[WPT], AL[WPT];
     uint32_t HC[WPT][NPLANES];
@@ -621,38 +674,26 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 #pragma unroll
         for (int q = 0; q < NPLANES; ++q) HC[k][q] = 0;
     }
-    for (int i = tau; i < Wpad; i += NT) nzs[i] = valid_mask(i, W, p.cols);
-    for (int i = tau; i < Wpad; i += NT) za[i] = 0;
-    for (int i = tau; i < 2 * BMAX * fstride; i += NT) fmap[i] = 0u;
-    if (tau == 0) {
-        misc->res[0] = misc->res[1] = misc->res[2] = RES_INF;
-        misc->g = p.share ? ld_volatile(res_best(result)) : 0;
-        if (TMA) {
-            for (int s = 0; s < p.nstage; ++s) mbar_init(&bars[s], 1);
-            fence_mbar_init();
-        }
-    }
-    tsync<SUB>(tmask);
-
-    int issued = 0;  // next band row to stage (producer thread)
-    const uint64_t pol = TMA ? l2_evict_first_policy() : 0ull;
-    if (TMA && tau == 0) {
-        for (; issued < min(p.nstage, H); ++issued) {
-            const int s = issued % p.nstage;
-            mbar_expect_tx(&bars[s], (uint32_t)p.row_bytes);
-            tma_row(ring + (size_t)s * p.rs, mbase + (size_t)(r0 + issued) * p.ld_bytes, (uint32_t)p.row_bytes,
-                    &bars[s], pol);
-        }
-    }
 
     int t = max(1, misc->g);
     bool full_next = false;
-    bool counters_ok = true;  // counters track heights since the band top
-    int climb_s = 0;          // leftmost window start of the last successful climb test
+    bool counters_ok = true;
+    int climb_s = 0;
     unsigned long long bandkey = 0ull;
     int round_ctr = 0;
     uint32_t bad_or = 0;
     int tile = 0;
+    unsigned long long pc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) pc[i] = 0;
+    const bool prof = p.prof != nullptr && tau == 0;
+    long long ck = prof ? clock64() : 0;
+#define MSQ_CK(i)                               \
+    if (prof) {                                 \
+        const long long c1 = clock64();         \
+        pc[i] += (unsigned long long)(c1 - ck); \
+        ck = c1;                                \
+    }
 
     for (int row0 = 0; row0 < H; ++tile) {
         const int rho0 = row0 + 1;
@@ -661,24 +702,24 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         const bool modeS = !climb && !modeL;
         const int nrows = climb ? 1 : min(modeL ? p.bl : p.bs, H - row0);
         uint32_t* fm = fmap + (tile & 1) * BMAX * fstride;
-        if (modeS && !counters_ok) {
-            // (re)build the counters from the last-zero rows: h = rho0-1 - lastzero
+        if (modeS && !counters_ok) {  // counters from the bit-sliced last-zero rows
 #pragma unroll
             for (int k = 0; k < WPT; ++k) {
-                const int a = tau * WPT + k;
+                uint32_t zb[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) zb[q] = q < P ? zp[q * Wpad + k * NT + tau] : 0u;
 #pragma unroll
                 for (int q = 0; q < NPLANES; ++q) HC[k][q] = 0;
-                if (a < W) {
-                    const int zaa = za[a];
-                    for (int j = 0; j < 32; ++j) {
-                        const int zj = ((NZ[k] >> j) & 1u) ? 0 : (int)zs[(size_t)a * 32 + j];
-                        const int h = min(rho0 - 1 - max(zj, zaa), 127);
+                for (int j = 0; j < 32; ++j) {
+                    int z = 0;
 #pragma unroll
-                        for (int q = 0; q < NPLANES; ++q) HC[k][q] |= (uint32_t)((h >> q) & 1) << j;
-                    }
+                    for (int q = 0; q < 16; ++q) z |= (int)((zb[q] >> j) & 1u) << q;
+                    const int h = min(rho0 - 1 - z, 127);
 #pragma unroll
-                    for (int q = 0; q < NPLANES; ++q) HC[k][q] &= VAL[k];
+                    for (int q = 0; q < NPLANES; ++q) HC[k][q] |= (uint32_t)((h >> q) & 1) << j;
                 }
+#pragma unroll
+                for (int q = 0; q < NPLANES; ++q) HC[k][q] &= VAL[k];
             }
             counters_ok = true;
             full_next = true;
@@ -727,8 +768,10 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
             }
         }
         if (tau == 0 && (tile & 7) == 7) misc->g = polled;
-        tsync<SUB>(tmask);  // (A)
-        if (TMA && tau == 0) {  // stages of the previous tile are free now
+        MSQ_CK(0)
+        csync();  // (A)
+        MSQ_CK(1)
+        if (SUB && TMA && tau == 0) {  // stages of the previous tile are free now
             const int upto = min(row0 + p.nstage, H);
             for (; issued < upto; ++issued) {
                 const int s = issued % p.nstage;
@@ -737,17 +780,18 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                         (uint32_t)p.row_bytes, &bars[s], pol);
             }
         }
+        MSQ_CK(2)
 
         // ---------------------------------------------------- phase B
         const int lastb = nrows - 1;
         int cur_t = t;
-        const Pass1Exact<U8, TMA> ex{zs, nzs, za, ring, mbase, p.ld_bytes, W, p.cols, p.rs, p.nstage, row0, r0};
+        const Pass1Exact<U8, TMA> ex{zp, ring, mbase, p.ld_bytes, W, p.cols, p.rs, p.nstage, P, WPT, NT, Wpad,
+                                     row0, r0};
         if (climb) {
-            if (t == rho0) {  // E = prefix-AND of the band top; find the leftmost t-window
-                int start = -1;
+            if (t == rho0) {  // E = prefix-AND of the band top; leftmost t-window
                 if (!SUB) {
                     if (tid < 32) {
-                        start = warp_first_window(hist, W, climb_s, t, lane);
+                        const int start = warp_first_window(hist, W, climb_s, t, lane);
                         if (lane == 0) misc->res[0] = (uint32_t)start;
                     }
                 } else {
@@ -759,12 +803,11 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     }
                     if (best != RES_INF) atomicMin(&misc->res[0], best);
                 }
-                tsync<SUB>(tmask);  // (B)
+                csync();  // (B)
                 const uint32_t rr = misc->res[0];
-                tsync<SUB>(tmask);
+                csync();
                 if (tau == 0) misc->res[0] = RES_INF;
-                start = (rr == RES_INF) ? -1 : (int)(rr & 0xFFFFFu);
-                if (!SUB && rr == 0xFFFFFFFFu) start = -1;
+                const int start = (rr == RES_INF) ? -1 : (int)(rr & 0xFFFFFu);
                 if (start >= 0) {
                     if (tau == 0) {
                         bandkey = pack_key(t, p.row_base + r0 + row0, start + t - 1);
@@ -781,37 +824,13 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 const int m = cur_t - t;
                 if (modeL) {
                     const int n = (lastb - start_b + 1) * nfw;
-                    int nc = 0, cb0 = 0, ca0 = 0, cl0 = 0, cb1 = 0, ca1 = 0, cl1 = 0;
                     for (int idx = tau; idx < n; idx += NT) {
                         const int b = start_b + idx / nfw, fw = idx % nfw;
                         scan_fword(fm, fstride, W, b, m, fw, cur_t, [&](int cb, int a0, int len) {
-                            if (!SUB && nc < 2) {
-                                if (nc == 0) { cb0 = cb; ca0 = a0; cl0 = len; }
-                                else { cb1 = cb; ca1 = a0; cl1 = len; }
-                                ++nc;
-                            } else {  // serial exact check
-                                const int suf = a0 > 0 ? suffix_ones(ex.mask(a0 - 1, cb, cur_t)) : 0;
-                                const int pre = a0 + len < W ? prefix_ones(ex.mask(a0 + len, cb, cur_t)) : 0;
-                                if (suf + 32 * len + pre >= cur_t) best = min(best, enc_res(cb, 32 * a0 - suf));
-                            }
+                            const int suf = a0 > 0 ? suffix_ones(ex.mask(a0 - 1, cb, cur_t)) : 0;
+                            const int pre = a0 + len < W ? prefix_ones(ex.mask(a0 + len, cb, cur_t)) : 0;
+                            if (suf + 32 * len + pre >= cur_t) best = min(best, enc_res(cb, 32 * a0 - suf));
                         });
-                    }
-                    if (!SUB) {  // warp-cooperative exact checks: lane = column
-                        for (;;) {
-                            const unsigned mk = __ballot_sync(0xFFFFFFFFu, nc > 0);
-                            if (!mk) break;
-                            const int src = __ffs(mk) - 1;
-                            const int mb = nc == 2 ? cb1 : cb0, ma = nc == 2 ? ca1 : ca0, ml = nc == 2 ? cl1 : cl0;
-                            const int b = __shfl_sync(0xFFFFFFFFu, mb, src);
-                            const int a0 = __shfl_sync(0xFFFFFFFFu, ma, src);
-                            const int len = __shfl_sync(0xFFFFFFFFu, ml, src);
-                            const int suf = a0 > 0 ? suffix_ones(ex.coop_mask(a0 - 1, b, cur_t, lane)) : 0;
-                            const int pre = a0 + len < W ? prefix_ones(ex.coop_mask(a0 + len, b, cur_t, lane)) : 0;
-                            if (lane == src) {
-                                if (suf + 32 * len + pre >= cur_t) best = min(best, enc_res(b, 32 * a0 - suf));
-                                --nc;
-                            }
-                        }
                     }
                 } else {
                     for (int b = start_b; b <= lastb; ++b) {
@@ -831,7 +850,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 const int slot = round_ctr % 3;
                 if (best != RES_INF) atomicMin(&misc->res[slot], best);
                 if (tau == 0) misc->res[(round_ctr + 1) % 3] = RES_INF;
-                tsync<SUB>(tmask);  // (B)
+                csync();  // (B)
                 const uint32_t rr = misc->res[slot];
                 ++round_ctr;
                 if (rr == RES_INF) break;
@@ -845,6 +864,14 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 full_from = bs_ + 1;
                 if (start_b > lastb) break;
             }
+        }
+        if (prof) {
+            const int kind = climb ? 0 : (modeL ? 2 : 1);
+            pc[8 + kind] += 1;
+            pc[11] += cur_t - t;
+            const long long c1 = clock64();
+            pc[3 + kind] += (unsigned long long)(c1 - ck);
+            ck = c1;
         }
         const bool raised = cur_t != t;
         t = cur_t;
@@ -861,6 +888,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         if (!climb || !raised) climb_s = 0;
 
         // ---------------------------------------------------- phase C
+        // last-zero rows (bit-sliced) and first zeros, in row order per word
         uint32_t zf = zflag;
         while (zf) {
             const int bit = __ffs(zf) - 1;
@@ -872,26 +900,12 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
             const uint32_t wv =
                 word_of_row<U8, TMA>(srow, mbase + (size_t)(r0 + r) * p.ld_bytes, a, p.cols, p.rs);
             const uint32_t zeros = VAL[k] & ~wv;
-            if (zeros == VAL[k]) {
-                za[a] = (uint16_t)rho;
-            } else {
-                uint32_t zz = zeros;
-                while (zz) {
-                    const int j = __ffs(zz) - 1;
-                    zz &= zz - 1;
-                    zs[(size_t)a * 32 + j] = (uint16_t)rho;
-                }
+            for (int q = 0; q < P; ++q) {
+                uint32_t* zq = zp + q * Wpad + k * NT + tau;
+                *zq = (*zq & ~zeros) | (((rho >> q) & 1) ? zeros : 0u);
             }
             uint32_t newly = NZ[k] & zeros;
             if (newly) {
-                if (zeros == VAL[k]) {  // the lazy all-zero row is the first zero of these columns
-                    uint32_t nn = newly;
-                    while (nn) {
-                        const int j = __ffs(nn) - 1;
-                        nn &= nn - 1;
-                        zs[(size_t)a * 32 + j] = 0;
-                    }
-                }
                 if (p.write_summaries) {
                     const size_t cb = sum_base + (size_t)a * 32;
                     while (newly) {
@@ -901,14 +915,27 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     }
                 }
                 NZ[k] &= ~zeros;
-                nzs[a] = NZ[k];
             }
         }
         if (modeL)
             for (int i = tau; i < BMAX * fstride; i += NT) fm[i] = 0u;
+        if (!SUB && TMA) {  // release this tile's rows to the producer
+            __syncwarp();
+            if (lane == 0)
+                for (int b = 0; b < nrows; ++b) {
+                    uint64_t* eb = &ebars[(row0 + b) % p.nstage];
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(eb)) : "memory");
+                }
+        }
+        MSQ_CK(6)
         row0 += nrows;
     }
-    tsync<SUB>(tmask);
+#undef MSQ_CK
+    if (prof) {
+        pc[12] = t;
+        for (int i = 0; i < 16; ++i) p.prof[(size_t)unit * 16 + i] = pc[i];
+    }
+    csync();
 
     // ---------------------------------------------------------- band outputs
     if (p.write_summaries) {
@@ -923,21 +950,25 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     nz &= nz - 1;
                     p.e_out[cb + j] = (uint16_t)H;
                 }
-                const int zaa = za[a];
-                uint4* zp = (uint4*)(zs + (size_t)a * 32);  // bottom runs overwrite the last-zero rows
+                uint32_t zb[16];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint4 zv = zp[q];
-                    const uint32_t pr[4] = {zv.x, zv.y, zv.z, zv.w};
+                for (int q = 0; q < 16; ++q) zb[q] = q < P ? zp[q * Wpad + k * NT + tau] : 0u;
+                uint4* bo = (uint4*)(p.zb + (size_t)unit * p.cols_pad + (size_t)a * 32);
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
                     uint32_t v[4];
 #pragma unroll
                     for (int h = 0; h < 4; ++h) {
-                        const int j0 = 8 * q + 2 * h;
-                        const int u0 = ((NZ[k] >> j0) & 1u) ? 0 : max((int)(pr[h] & 0xFFFFu), zaa);
-                        const int u1 = ((NZ[k] >> (j0 + 1)) & 1u) ? 0 : max((int)(pr[h] >> 16), zaa);
-                        v[h] = (uint32_t)(H - u0) | ((uint32_t)(H - u1) << 16);
+                        const int j0 = 8 * q4 + 2 * h;
+                        int z0 = 0, z1 = 0;
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) {
+                            z0 |= (int)((zb[q] >> j0) & 1u) << q;
+                            z1 |= (int)((zb[q] >> (j0 + 1)) & 1u) << q;
+                        }
+                        v[h] = (uint32_t)(H - z0) | ((uint32_t)(H - z1) << 16);
                     }
-                    zp[q] = make_uint4(v[0], v[1], v[2], v[3]);
+                    bo[q4] = make_uint4(v[0], v[1], v[2], v[3]);
                 }
                 p.ao_out[(size_t)band * W + a] = NZ[k];
             }
