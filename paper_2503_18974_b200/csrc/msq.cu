@@ -103,7 +103,7 @@ cudaError_t launch_fixup_t(const msq_plan* pl, const msq::FixParams& prm, int nb
     static bool attr_set[64] = {false};
     cudaError_t e = set_smem_attr(kern, attr_set);
     if (e != cudaSuccess) return e;
-    kern<<<nblocks, pl->threads, pl->smem_fixup, st>>>(prm);
+    kern<<<nblocks, pl->team, pl->smem_fixup, st>>>(prm);
     return cudaGetLastError();
 }
 
@@ -374,7 +374,7 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
         }
     }
     p.smem_pass1 = team_layout_bytes(&p);
-    p.smem_fixup = msq::fix_layout(p.threads, p.wpt, p.tile_rows).total;
+    p.smem_fixup = msq::fix_layout(p.team, p.wpt, p.tile_rows).total;
     if (p.smem_pass1 > kSmemMax || p.smem_fixup > kSmemMax) return MSQ_EINVAL;
     p.ws_bytes = (int64_t)ws_layout(&p).total;
     *plan = p;
