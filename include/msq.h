@@ -81,6 +81,8 @@ typedef struct {
     int32_t tile_rows_l;  /* rows per tile once the threshold is >= tl      */
     int32_t tl;           /* threshold where the word-level filter takes over */
     int32_t grid;         /* pass-1 CTAs                                    */
+    int32_t fix_threads;  /* fix-up CTA size                                */
+    int32_t fix_wpt;      /* fix-up words per thread                        */
     int32_t reserved;
 } msq_plan;
 
@@ -154,6 +156,8 @@ int32_t msq_last_launch_count(void);
 void msq_debug_set_profile(void* d_counters);
 
 const char* msq_strerror(int code);
+/* Name and text of the last CUDA error seen by this thread ("" if none). */
+const char* msq_last_cuda_error(void);
 const char* msq_version(void);
 
 #ifdef __cplusplus

@@ -40,7 +40,8 @@ class MsqPlan(ctypes.Structure):
                 ("deterministic", ctypes.c_int32), ("row_base", ctypes.c_int64),
                 ("ws_bytes", ctypes.c_int64), ("team", ctypes.c_int32),
                 ("teams_per_cta", ctypes.c_int32), ("tile_rows_l", ctypes.c_int32),
-                ("tl", ctypes.c_int32), ("grid", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("tl", ctypes.c_int32), ("grid", ctypes.c_int32), ("fix_threads", ctypes.c_int32),
+                ("fix_wpt", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 _lib = None
@@ -84,6 +85,7 @@ def load():
         "msq_last_launch_count": ([], I32),
         "msq_debug_set_profile": ([P], None),
         "msq_strerror": ([ctypes.c_int], ctypes.c_char_p),
+        "msq_last_cuda_error": ([], ctypes.c_char_p),
         "msq_version": ([], ctypes.c_char_p),
     }
     for name, (args, res) in sig.items():
@@ -105,7 +107,8 @@ def check(rc: int) -> None:
     msg = load().msq_strerror(rc).decode()
     if rc in (MSQ_EVALUE, MSQ_EINVAL):
         raise ValueError(msg)
-    raise MsqError(f"libmsq: {msg} (code {rc})")
+    detail = load().msq_last_cuda_error().decode() if rc == MSQ_ECUDA else ""
+    raise MsqError(f"libmsq: {msg} (code {rc}) {detail}")
 
 
 def plan(fmt: int, batch: int, rows: int, cols: int, ld: int, nbands: int = 0,

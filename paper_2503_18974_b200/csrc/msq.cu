@@ -20,6 +20,7 @@ constexpr int kModeLThreshold = 96;  // >= 63 (see msq_engine.cuh)
 constexpr int kMaxWords = 2048;   // 65536 columns
 
 thread_local int32_t g_last_launches = 0;
+thread_local char g_last_err[256] = "";
 unsigned long long* g_prof = nullptr;  // debug: per-unit phase counters
 
 inline long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
@@ -94,7 +95,16 @@ cudaError_t launch_pass1_t(const msq_plan* pl, const msq::Pass1Params& prm, cuda
     cudaError_t e = set_smem_attr(kern, attr_set);
     if (e != cudaSuccess) return e;
     kern<<<pl->grid, pl->threads, pl->smem_pass1, st>>>(prm);
-    return cudaGetLastError();
+    cudaError_t e2 = cudaGetLastError();
+    if (e2 != cudaSuccess) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, kern);
+        snprintf(g_last_err, sizeof(g_last_err), "%s (pass1: regs %d, maxThreads %d, localBytes %zu, block %d, smem %d)",
+                 cudaGetErrorString(e2), fa.numRegs, fa.maxThreadsPerBlock, fa.localSizeBytes, pl->threads,
+                 pl->smem_pass1);
+        return e2;
+    }
+    return cudaSuccess;
 }
 
 template <int WPT>
@@ -103,7 +113,7 @@ cudaError_t launch_fixup_t(const msq_plan* pl, const msq::FixParams& prm, int nb
     static bool attr_set[64] = {false};
     cudaError_t e = set_smem_attr(kern, attr_set);
     if (e != cudaSuccess) return e;
-    kern<<<nblocks, pl->team, pl->smem_fixup, st>>>(prm);
+    kern<<<nblocks, pl->fix_threads, pl->smem_fixup, st>>>(prm);
     return cudaGetLastError();
 }
 
@@ -121,13 +131,15 @@ cudaError_t launch_pass1(const msq_plan* pl, const msq::Pass1Params& prm, cudaSt
     MSQ_P1(2, false, false, false)
     MSQ_P1(4, true, true, false) MSQ_P1(4, true, false, false) MSQ_P1(4, false, true, false)
     MSQ_P1(4, false, false, false)
+    MSQ_P1(8, true, true, false) MSQ_P1(8, true, false, false) MSQ_P1(8, false, true, false)
+    MSQ_P1(8, false, false, false)
 #undef MSQ_P1
     return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_fixup(const msq_plan* pl, const msq::FixParams& prm, int nblocks, cudaStream_t st) {
     if (nblocks <= 0) return cudaSuccess;
-    switch (pl->wpt) {
+    switch (pl->fix_wpt) {
         case 1: return launch_fixup_t<1>(pl, prm, nblocks, st);
         case 2: return launch_fixup_t<2>(pl, prm, nblocks, st);
         case 4: return launch_fixup_t<4>(pl, prm, nblocks, st);
@@ -199,7 +211,12 @@ msq::FixParams make_fix(const msq_plan* pl, void* ws, const uint32_t* base, msq_
     return f;
 }
 
-int cuda_status(cudaError_t e) { return e == cudaSuccess ? MSQ_OK : MSQ_ECUDA; }
+int cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return MSQ_OK;
+    if (g_last_err[0] && e == cudaErrorLaunchOutOfResources) return MSQ_ECUDA;
+    snprintf(g_last_err, sizeof(g_last_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+    return MSQ_ECUDA;
+}
 
 cudaError_t launch_carry(const msq_plan* pl, void* ws, const uint32_t* base, cudaStream_t st) {
     WsLayout L = ws_layout(pl);
@@ -317,7 +334,7 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
         long long tpc = std::max<long long>(1, ceil_div(batch, sms));
         const long long gran = std::max(1, 32 / ts);  // teams per warp
         tpc = round_up(tpc, gran);
-        tpc = std::min<long long>(tpc, 512 / ts);
+        tpc = std::min<long long>(tpc, 256 / ts);
         p.nstage = tma_ok ? 2 * msq::BMAX : 0;  // ring holds the previous and the current tile
         for (;;) {
             const long long per = msq::p1_layout(ts, 1, p.nstage, (int)row_bytes, p.tile_rows, zplanes_for(&p),
@@ -340,9 +357,11 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
         *plan = p;
         return MSQ_OK;
     }
-    // ---- CTA teams: one band of one matrix per CTA
-    p.wpt = words <= 512 ? 1 : (words <= 1024 ? 2 : 4);
+    // ---- CTA teams: one band of one matrix per CTA (256 consumer threads max)
+    p.wpt = words <= 256 ? 1 : (words <= 512 ? 2 : (words <= 1024 ? 4 : 8));
     p.threads = (int32_t)std::max<long long>(32, round_up(ceil_div(words, p.wpt), 32));
+    p.fix_wpt = words <= 512 ? 1 : (words <= 1024 ? 2 : 4);
+    p.fix_threads = (int32_t)std::max<long long>(32, round_up(ceil_div(words, p.fix_wpt), 32));
     p.team = p.threads;
     p.teams_per_cta = 1;
     int nb = nbands;
@@ -374,7 +393,7 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
         }
     }
     p.smem_pass1 = team_layout_bytes(&p);
-    p.smem_fixup = msq::fix_layout(p.team, p.wpt, p.tile_rows).total;
+    p.smem_fixup = msq::fix_layout(p.fix_threads, p.fix_wpt, p.tile_rows).total;
     if (p.smem_pass1 > kSmemMax || p.smem_fixup > kSmemMax) return MSQ_EINVAL;
     p.ws_bytes = (int64_t)ws_layout(&p).total;
     *plan = p;
@@ -395,14 +414,14 @@ int msq_launch(const msq_plan* pl, const void* d_src, void* d_ws, msq_devresult*
     const bool multi = pl->batch == 1 && pl->nbands > 1;
     msq::Pass1Params p1 = make_pass1(pl, d_src, d_ws, d_result, multi);
     cudaError_t e = launch_pass1(pl, p1, st);
-    if (e != cudaSuccess) return MSQ_ECUDA;
+    if (e != cudaSuccess) return cuda_status(e);
     g_last_launches = 1;
     if (multi) {
         e = launch_carry(pl, d_ws, nullptr, st);
-        if (e != cudaSuccess) return MSQ_ECUDA;
+        if (e != cudaSuccess) return cuda_status(e);
         msq::FixParams f = make_fix(pl, d_ws, nullptr, d_result);
         e = launch_fixup(pl, f, pl->nbands - 1, st);
-        if (e != cudaSuccess) return MSQ_ECUDA;
+        if (e != cudaSuccess) return cuda_status(e);
         g_last_launches = 3;
     }
     return MSQ_OK;
@@ -560,5 +579,7 @@ const char* msq_strerror(int code) {
 }
 
 const char* msq_version(void) { return "msq 0.1.0 sm_100a"; }
+
+const char* msq_last_cuda_error(void) { return g_last_err; }
 
 }  // extern "C"

@@ -569,7 +569,7 @@ __device__ int warp_first_window(const uint32_t* X, int W, int s0, int T, int la
 // CTA teams: warps 0..NT/32-1 consume; one extra warp streams rows with TMA
 // (full/empty mbarrier ring).  Sub-warp teams: lane 0 of the team streams.
 template <int WPT, bool U8, bool TMA, bool SUB>
-__global__ void __maxnreg__(120) pass1_kernel(const Pass1Params p) {
+__global__ void __launch_bounds__(288, 1) pass1_kernel(const Pass1Params p) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int NT = p.team;
     const int tid = threadIdx.x;
