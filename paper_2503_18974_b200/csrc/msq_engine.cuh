@@ -375,12 +375,15 @@ __device__ __forceinline__ void fetch_words(const uint8_t* stage_row, const uint
         if (TMA) {
             const uint32_t* rp = (const uint32_t*)stage_row + tau * WPT;
             if (tau * WPT < W) {
-                if (WPT == 4) {
-                    const uint4 v = *(const uint4*)rp;
-                    w[0] = v.x;
-                    w[1 % WPT] = v.y;
-                    w[2 % WPT] = v.z;
-                    w[3 % WPT] = v.w;
+                if (WPT >= 4) {
+#pragma unroll
+                    for (int q = 0; q < WPT / 4; ++q) {
+                        const uint4 v = ((const uint4*)rp)[q];
+                        w[(4 * q + 0) % WPT] = v.x;
+                        w[(4 * q + 1) % WPT] = v.y;
+                        w[(4 * q + 2) % WPT] = v.z;
+                        w[(4 * q + 3) % WPT] = v.w;
+                    }
                 } else if (WPT == 2) {
                     const uint2 v = *(const uint2*)rp;
                     w[0] = v.x;

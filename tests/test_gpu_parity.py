@@ -138,6 +138,19 @@ def test_random_banded_solves(torch):
             _same(Solver(N.FMT_BITS, rows, cols, nbands=nb).solve(w)[0], want)
 
 
+@pytest.mark.parametrize("cols", [65536, 40000, 33000])
+def test_wide_rows_every_word_width(torch, cols):
+    """Widths that select 8 (bits) / 4 (u8) words per thread, both formats."""
+    rng = np.random.default_rng(cols)
+    a = (rng.random((300, cols)) < 0.995).astype(np.uint8)
+    a[100:190, cols - 120:cols - 30] = 1  # planted 90x90 near the right edge
+    want = oracle.freq(a)
+    w = torch.from_numpy(grid.pack_bits(a).view(np.int32)).cuda()
+    for nb in (1, 7):
+        _same(Solver(N.FMT_BITS, 300, cols, nbands=nb).solve(w)[0], want)
+        _same(Solver(N.FMT_U8, 300, cols, nbands=nb).solve(torch.from_numpy(a).cuda())[0], want)
+
+
 def test_strided_and_odd_widths(torch):
     rng = np.random.default_rng(9)
     for cols in (1, 3, 17, 31, 33, 63, 65, 100, 130):
