@@ -73,7 +73,7 @@ int zplanes_for(const msq_plan* pl) {
     return P;
 }
 
-bool uses_producer_warp(const msq_plan* pl) { return pl->teams_per_cta == 1 && pl->team == pl->threads - 32; }
+bool uses_producer_warp(const msq_plan*) { return false; }
 
 
 template <class K>
@@ -131,8 +131,6 @@ cudaError_t launch_pass1(const msq_plan* pl, const msq::Pass1Params& prm, cudaSt
     MSQ_P1(2, false, false, false)
     MSQ_P1(4, true, true, false) MSQ_P1(4, true, false, false) MSQ_P1(4, false, true, false)
     MSQ_P1(4, false, false, false)
-    MSQ_P1(8, true, true, false) MSQ_P1(8, true, false, false) MSQ_P1(8, false, true, false)
-    MSQ_P1(8, false, false, false)
 #undef MSQ_P1
     return cudaErrorInvalidValue;
 }
@@ -334,7 +332,7 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
         long long tpc = std::max<long long>(1, ceil_div(batch, sms));
         const long long gran = std::max(1, 32 / ts);  // teams per warp
         tpc = round_up(tpc, gran);
-        tpc = std::min<long long>(tpc, 256 / ts);
+        tpc = std::min<long long>(tpc, 512 / ts);
         p.nstage = tma_ok ? 2 * msq::BMAX : 0;  // ring holds the previous and the current tile
         for (;;) {
             const long long per = msq::p1_layout(ts, 1, p.nstage, (int)row_bytes, p.tile_rows, zplanes_for(&p),
@@ -357,8 +355,8 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
         *plan = p;
         return MSQ_OK;
     }
-    // ---- CTA teams: one band of one matrix per CTA (256 consumer threads max)
-    p.wpt = words <= 256 ? 1 : (words <= 512 ? 2 : (words <= 1024 ? 4 : 8));
+    // ---- CTA teams: one band of one matrix per CTA (512 consumer threads max)
+    p.wpt = words <= 512 ? 1 : (words <= 1024 ? 2 : 4);
     p.threads = (int32_t)std::max<long long>(32, round_up(ceil_div(words, p.wpt), 32));
     p.fix_wpt = words <= 512 ? 1 : (words <= 1024 ? 2 : 4);
     p.fix_threads = (int32_t)std::max<long long>(32, round_up(ceil_div(words, p.fix_wpt), 32));
@@ -370,7 +368,7 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
     } else if (nb <= 0) {
         nb = (int)std::min<long long>(sms, std::max<long long>(1, rows / 64));
     }
-    nb = (int)std::max<long long>(nb, ceil_div(rows, 65535));
+    nb = (int)std::max<long long>(nb, ceil_div(rows, 4095));  // band heights fit MAXP=12 planes
     if (nb > rows) nb = (int)rows;
     if (nb > 2048) return MSQ_EINVAL;
     if (batch > 1 && nb != 1) return MSQ_EINVAL;
@@ -381,16 +379,13 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
     p.nstage = 0;
     const int P = zplanes_for(&p);
     if (tma_ok) {
-        // a producer warp streams rows; a stage is refilled as soon as its row
-        // is released, so the ring only has to hold one tile (more = deeper prefetch)
-        const int base = msq::p1_layout(p.threads, p.wpt, 0, (int)row_bytes, p.tile_rows, P, true, true).total;
+        // refills happen after the next tile's first barrier, so the ring must
+        // hold the previous tile plus the current one (more = deeper prefetch)
+        const int base = msq::p1_layout(p.threads, p.wpt, 0, (int)row_bytes, p.tile_rows, P, true, false).total;
         long long ns = (kSmemMax - base - 512) / row_bytes;
         ns = std::min<long long>(ns, 32);
         if (ns < 2 * p.tile_rows_l) p.tile_rows_l = p.tile_rows;
-        if (ns >= 2 * p.tile_rows_l) {
-            p.nstage = (int32_t)ns;
-            p.threads += 32;  // + producer warp (team stays the consumer count)
-        }
+        if (ns >= 2 * p.tile_rows_l) p.nstage = (int32_t)ns;
     }
     p.smem_pass1 = team_layout_bytes(&p);
     p.smem_fixup = msq::fix_layout(p.fix_threads, p.fix_wpt, p.tile_rows).total;

@@ -42,6 +42,7 @@ constexpr int NPLANES = 7;   // mode S counters saturate at 127
 constexpr int BMAX = 4;      // max rows per tile
 constexpr int FIX_XPL = 6;   // fix-up mode X planes (c, e clamped at 63)
 constexpr int FIX_TL = 63;   // fix-up mode L threshold (runs then contain a full word)
+constexpr int MAXP = 12;     // last-zero bit planes: bands are <= 4095 rows
 
 __host__ __device__ __forceinline__ unsigned long long pack_key(long long side, long long bottom,
                                                                 long long right) {
@@ -480,16 +481,33 @@ __device__ __forceinline__ int zp_index(int a, int p, int WPT, int NT, int Wpad)
     return p * Wpad + k * NT + tau;
 }
 
+// z_j = rho for the columns in `cols` (bit-sliced, P planes); loads first for ILP
+__device__ __forceinline__ void zplanes_set(uint32_t* zp, int base, int stride, int P, uint32_t cols, int rho) {
+    uint32_t v[MAXP];
+#pragma unroll
+    for (int q = 0; q < MAXP; ++q)
+        if (q < P) v[q] = zp[base + q * stride];
+#pragma unroll
+    for (int q = 0; q < MAXP; ++q)
+        if (q < P) zp[base + q * stride] = (v[q] & ~cols) | (((rho >> q) & 1) ? cols : 0u);
+}
+
 // bit-sliced "Z <= c" over P planes (c < 2^P)
 __device__ __forceinline__ uint32_t planes_le(const uint32_t* zp, int base, int stride, int P, int c) {
+    uint32_t v[MAXP];
+#pragma unroll
+    for (int q = 0; q < MAXP; ++q)
+        if (q < P) v[q] = zp[base + q * stride];
     uint32_t lt = 0, eq = 0xFFFFFFFFu;
-    for (int p = P - 1; p >= 0; --p) {
-        const uint32_t zb = zp[base + p * stride];
-        if ((c >> p) & 1) {
-            lt |= eq & ~zb;
-            eq &= zb;
-        } else {
-            eq &= ~zb;
+#pragma unroll
+    for (int q = MAXP - 1; q >= 0; --q) {
+        if (q < P) {
+            if ((c >> q) & 1) {
+                lt |= eq & ~v[q];
+                eq &= v[q];
+            } else {
+                eq &= ~v[q];
+            }
         }
     }
     return lt | eq;
@@ -569,10 +587,11 @@ __device__ int warp_first_window(const uint32_t* X, int W, int s0, int T, int la
 // Tile kinds: CLIMB (t >= rho: heights <= rho, so E = prefix-AND of the band
 // top when t == rho; 1 row per tile, one warp finds the leftmost window),
 // S (t < tl: bit-sliced counters), L (t >= tl: word-level F filter).
-// CTA teams: warps 0..NT/32-1 consume; one extra warp streams rows with TMA
-// (full/empty mbarrier ring).  Sub-warp teams: lane 0 of the team streams.
+// Rows stream through the TMA ring; refills are issued by lane 0 of the last
+// warp of the team right after the tile's first barrier (that warp is idle
+// during most of phase B).
 template <int WPT, bool U8, bool TMA, bool SUB>
-__global__ void __launch_bounds__(288, 1) pass1_kernel(const Pass1Params p) {
+__global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int NT = p.team;
     const int tid = threadIdx.x;
@@ -595,11 +614,10 @@ __global__ void __launch_bounds__(288, 1) pass1_kernel(const Pass1Params p) {
     const int P = p.zplanes;
     unsigned char* result = p.results + (size_t)mat * 32;
 
-    const P1Layout Lo = p1_layout(NT, WPT, p.nstage, p.rs, p.bs, P, TMA, !SUB && TMA);
+    const P1Layout Lo = p1_layout(NT, WPT, p.nstage, p.rs, p.bs, P, TMA, false);
     uint8_t* tsm = smem + (size_t)team_idx * p.layout_bytes;
     uint8_t* ring = tsm + Lo.ring;
     uint64_t* bars = (uint64_t*)(tsm + Lo.bars);
-    uint64_t* ebars = (uint64_t*)(tsm + Lo.ebars);
     uint32_t* zp = (uint32_t*)(tsm + Lo.zp);  // bit-sliced last-zero rows
     uint32_t* hist = (uint32_t*)(tsm + Lo.hist);
     uint32_t* fmap = (uint32_t*)(tsm + Lo.fmap);
@@ -607,55 +625,25 @@ __global__ void __launch_bounds__(288, 1) pass1_kernel(const Pass1Params p) {
     const uint8_t* mbase = p.src + (size_t)mat * p.batch_stride;
     const size_t sum_base = (size_t)band * p.cols_pad;
     const uint64_t pol = TMA ? l2_evict_first_policy() : 0ull;
-    const bool producer_warp = !SUB && TMA && tid >= NT;  // CTA teams only
-    const int nconsumer_warps = NT / 32;
+    // TMA issuer: lane 0 of the last warp of the team (idle during most of phase B)
+    const int issuer = SUB ? 0 : NT - 32;
 
-    // ---- setup (all threads, including the producer warp)
-    for (int i = tid; i < P * Wpad; i += blockDim.x) {
-        if (!SUB) zp[i] = 0u;
-    }
-    if (SUB)
-        for (int i = tau; i < P * Wpad; i += NT) zp[i] = 0u;
-    for (int i = (SUB ? tau : tid); i < 2 * BMAX * fstride; i += (SUB ? NT : (int)blockDim.x)) fmap[i] = 0u;
+    // ---- setup
+    for (int i = tau; i < P * Wpad; i += NT) zp[i] = 0u;
+    for (int i = tau; i < 2 * BMAX * fstride; i += NT) fmap[i] = 0u;
     if (tau == 0) {
         misc->res[0] = misc->res[1] = misc->res[2] = RES_INF;
         misc->g = p.share ? ld_volatile(res_best(result)) : 0;
         if (TMA) {
-            for (int s = 0; s < p.nstage; ++s) {
-                mbar_init(&bars[s], 1);
-                if (!SUB) mbar_init(&ebars[s], nconsumer_warps);
-            }
+            for (int s = 0; s < p.nstage; ++s) mbar_init(&bars[s], 1);
             fence_mbar_init();
         }
     }
-    if (SUB)
-        tsync<true>(tmask);
-    else
-        __syncthreads();
+    auto csync = [&]() { tsync<SUB>(tmask); };
+    csync();
 
-    if (producer_warp) {  // ------------------------------ TMA producer warp
-        if (lane == 0) {
-            for (int r = 0; r < H; ++r) {
-                const int s = r % p.nstage;
-                if (r >= p.nstage) mbar_wait(&ebars[s], (uint32_t)(((r / p.nstage) - 1) & 1));
-                mbar_expect_tx(&bars[s], (uint32_t)p.row_bytes);
-                tma_row(ring + (size_t)s * p.rs, mbase + (size_t)(r0 + r) * p.ld_bytes, (uint32_t)p.row_bytes,
-                        &bars[s], pol);
-            }
-        }
-        return;
-    }
-    auto csync = [&]() {  // consumer-only barrier
-        if (SUB)
-            __syncwarp(tmask);
-        else if (TMA)
-            asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");
-        else
-            __syncthreads();
-    };
-
-    int issued = 0;  // sub-warp teams: lane 0 streams rows itself
-    if (SUB && TMA && tau == 0) {
+    int issued = 0;  // rows staged so far (issuer thread)
+    if (TMA && tau == issuer) {
         for (; issued < min(p.nstage, H); ++issued) {
             const int s = issued % p.nstage;
             mbar_expect_tx(&bars[s], (uint32_t)p.row_bytes);
@@ -665,7 +653,6 @@ __global__ void __launch_bounds__(288, 1) pass1_kernel(const Pass1Params p) {
     }
 
     uint32_t VAL[WPT], NZ[WPT], EPREV[WPT], AL[WPT];
-    uint32_t HC[WPT][NPLANES];
     int ZW[WPT];
 #pragma unroll
     for (int k = 0; k < WPT; ++k) {
@@ -674,13 +661,10 @@ __global__ void __launch_bounds__(288, 1) pass1_kernel(const Pass1Params p) {
         AL[k] = VAL[k];
         EPREV[k] = 0;
         ZW[k] = 0;
-#pragma unroll
-        for (int q = 0; q < NPLANES; ++q) HC[k][q] = 0;
     }
 
     int t = max(1, misc->g);
     bool full_next = false;
-    bool counters_ok = true;
     int climb_s = 0;
     unsigned long long bandkey = 0ull;
     int round_ctr = 0;
@@ -705,28 +689,6 @@ __global__ void __launch_bounds__(288, 1) pass1_kernel(const Pass1Params p) {
         const bool modeS = !climb && !modeL;
         const int nrows = climb ? 1 : min(modeL ? p.bl : p.bs, H - row0);
         uint32_t* fm = fmap + (tile & 1) * BMAX * fstride;
-        if (modeS && !counters_ok) {  // counters from the bit-sliced last-zero rows
-#pragma unroll
-            for (int k = 0; k < WPT; ++k) {
-                uint32_t zb[16];
-#pragma unroll
-                for (int q = 0; q < 16; ++q) zb[q] = q < P ? zp[q * Wpad + k * NT + tau] : 0u;
-#pragma unroll
-                for (int q = 0; q < NPLANES; ++q) HC[k][q] = 0;
-                for (int j = 0; j < 32; ++j) {
-                    int z = 0;
-#pragma unroll
-                    for (int q = 0; q < 16; ++q) z |= (int)((zb[q] >> j) & 1u) << q;
-                    const int h = min(rho0 - 1 - z, 127);
-#pragma unroll
-                    for (int q = 0; q < NPLANES; ++q) HC[k][q] |= (uint32_t)((h >> q) & 1) << j;
-                }
-#pragma unroll
-                for (int q = 0; q < NPLANES; ++q) HC[k][q] &= VAL[k];
-            }
-            counters_ok = true;
-            full_next = true;
-        }
         int polled = 0;
         if (p.share && tau == 0 && (tile & 7) == 7) polled = ld_volatile(res_best(result));
 
@@ -756,9 +718,11 @@ __global__ void __launch_bounds__(288, 1) pass1_kernel(const Pass1Params p) {
                         hist[b * Wpad + tau * WPT + k] = AL[k];
                     } else if (modeL) {
                         fnib |= ((VAL[k] == 0xFFFFFFFFu && ZW[k] <= rho - t) ? 1u : 0u) << k;
-                    } else {
-                        planes_step<NPLANES>(HC[k], w[k]);
-                        const uint32_t e = planes_ge<NPLANES>(HC[k], t) & VAL[k];
+                    } else {  // mode S: last-zero planes updated now; E = {z <= rho - t}
+                        const int zi = k * NT + tau;
+                        if (z) zplanes_set(zp, zi, Wpad, P, VAL[k] & ~w[k], rho);
+                        const int lim = rho - t;
+                        const uint32_t e = (lim >= (1 << P) ? 0xFFFFFFFFu : planes_le(zp, zi, Wpad, P, lim)) & VAL[k];
                         if (e & ~EPREV[k]) dirty |= 1u << (b * WPT + k);
                         EPREV[k] = e;
                         hist[b * Wpad + tau * WPT + k] = e;
@@ -774,7 +738,7 @@ __global__ void __launch_bounds__(288, 1) pass1_kernel(const Pass1Params p) {
         MSQ_CK(0)
         csync();  // (A)
         MSQ_CK(1)
-        if (SUB && TMA && tau == 0) {  // stages of the previous tile are free now
+        if (TMA && tau == issuer) {  // stages of the previous tile are free now
             const int upto = min(row0 + p.nstage, H);
             for (; issued < upto; ++issued) {
                 const int s = issued % p.nstage;
@@ -887,7 +851,6 @@ __global__ void __launch_bounds__(288, 1) pass1_kernel(const Pass1Params p) {
             }
         }
         full_next = raised || jumped;
-        if (!modeS) counters_ok = false;
         if (!climb || !raised) climb_s = 0;
 
         // ---------------------------------------------------- phase C
@@ -903,10 +866,7 @@ __global__ void __launch_bounds__(288, 1) pass1_kernel(const Pass1Params p) {
             const uint32_t wv =
                 word_of_row<U8, TMA>(srow, mbase + (size_t)(r0 + r) * p.ld_bytes, a, p.cols, p.rs);
             const uint32_t zeros = VAL[k] & ~wv;
-            for (int q = 0; q < P; ++q) {
-                uint32_t* zq = zp + q * Wpad + k * NT + tau;
-                *zq = (*zq & ~zeros) | (((rho >> q) & 1) ? zeros : 0u);
-            }
+            if (!modeS) zplanes_set(zp, k * NT + tau, Wpad, P, zeros, rho);
             uint32_t newly = NZ[k] & zeros;
             if (newly) {
                 if (p.write_summaries) {
@@ -922,14 +882,6 @@ __global__ void __launch_bounds__(288, 1) pass1_kernel(const Pass1Params p) {
         }
         if (modeL)
             for (int i = tau; i < BMAX * fstride; i += NT) fm[i] = 0u;
-        if (!SUB && TMA) {  // release this tile's rows to the producer
-            __syncwarp();
-            if (lane == 0)
-                for (int b = 0; b < nrows; ++b) {
-                    uint64_t* eb = &ebars[(row0 + b) % p.nstage];
-                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(eb)) : "memory");
-                }
-        }
         MSQ_CK(6)
         row0 += nrows;
     }
@@ -953,25 +905,16 @@ __global__ void __launch_bounds__(288, 1) pass1_kernel(const Pass1Params p) {
                     nz &= nz - 1;
                     p.e_out[cb + j] = (uint16_t)H;
                 }
-                uint32_t zb[16];
+                uint32_t zb[MAXP];
 #pragma unroll
-                for (int q = 0; q < 16; ++q) zb[q] = q < P ? zp[q * Wpad + k * NT + tau] : 0u;
-                uint4* bo = (uint4*)(p.zb + (size_t)unit * p.cols_pad + (size_t)a * 32);
+                for (int q = 0; q < MAXP; ++q) zb[q] = q < P ? zp[q * Wpad + k * NT + tau] : 0u;
+                uint16_t* bo = p.zb + (size_t)unit * p.cols_pad + (size_t)a * 32;
+#pragma unroll 1
+                for (int j = 0; j < 32; ++j) {
+                    int z = 0;
 #pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) {
-                    uint32_t v[4];
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        const int j0 = 8 * q4 + 2 * h;
-                        int z0 = 0, z1 = 0;
-#pragma unroll
-                        for (int q = 0; q < 16; ++q) {
-                            z0 |= (int)((zb[q] >> j0) & 1u) << q;
-                            z1 |= (int)((zb[q] >> (j0 + 1)) & 1u) << q;
-                        }
-                        v[h] = (uint32_t)(H - z0) | ((uint32_t)(H - z1) << 16);
-                    }
-                    bo[q4] = make_uint4(v[0], v[1], v[2], v[3]);
+                    for (int q = 0; q < MAXP; ++q) z |= (int)((zb[q] >> j) & 1u) << q;
+                    bo[j] = (uint16_t)(H - z);
                 }
                 p.ao_out[(size_t)band * W + a] = NZ[k];
             }

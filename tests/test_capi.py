@@ -28,13 +28,13 @@ def test_strerror_and_version(lib):
 
 def test_plan_shapes(lib):
     p = N.plan(N.FMT_BITS, 1, 65536, 65536, 2048)
-    assert (p.words, p.wpt, p.team) == (2048, 8, 256)
-    assert p.threads == 288  # + one TMA producer warp
+    assert (p.words, p.wpt, p.team) == (2048, 4, 512)
+    assert p.threads == 512
     assert (p.fix_wpt, p.fix_threads) == (4, 512)
     assert p.nstage >= 8 and p.smem_pass1 <= 232448 and p.smem_fixup <= 232448
     assert 1 <= p.nbands <= 148
     p = N.plan(N.FMT_U8, 1, 32768, 32768, 32768)
-    assert (p.words, p.wpt, p.team) == (1024, 4, 256)
+    assert (p.words, p.wpt, p.team) == (1024, 2, 512)
     assert p.nstage >= 2
     p = N.plan(N.FMT_U8, 4096, 256, 256, 256)
     assert (p.nbands, p.team, p.batch) == (1, 8, 4096)  # sub-warp teams of 8 lanes
