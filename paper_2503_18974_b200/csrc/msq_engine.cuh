@@ -482,35 +482,52 @@ __device__ __forceinline__ int zp_index(int a, int p, int WPT, int NT, int Wpad)
 }
 
 // z_j = rho for the columns in `cols` (bit-sliced, P planes); loads first for ILP
+template <int P>
+__device__ __forceinline__ void zplanes_set_t(uint32_t* zp, int base, int stride, uint32_t cols, int rho) {
+    uint32_t v[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) v[q] = zp[base + q * stride];
+#pragma unroll
+    for (int q = 0; q < P; ++q) zp[base + q * stride] = (v[q] & ~cols) | (((rho >> q) & 1) ? cols : 0u);
+}
 __device__ __forceinline__ void zplanes_set(uint32_t* zp, int base, int stride, int P, uint32_t cols, int rho) {
-    uint32_t v[MAXP];
-#pragma unroll
-    for (int q = 0; q < MAXP; ++q)
-        if (q < P) v[q] = zp[base + q * stride];
-#pragma unroll
-    for (int q = 0; q < MAXP; ++q)
-        if (q < P) zp[base + q * stride] = (v[q] & ~cols) | (((rho >> q) & 1) ? cols : 0u);
+    switch (P) {
+#define MSQ_ZS(n) \
+    case n: zplanes_set_t<n>(zp, base, stride, cols, rho); break;
+        MSQ_ZS(1) MSQ_ZS(2) MSQ_ZS(3) MSQ_ZS(4) MSQ_ZS(5) MSQ_ZS(6)
+        MSQ_ZS(7) MSQ_ZS(8) MSQ_ZS(9) MSQ_ZS(10) MSQ_ZS(11) MSQ_ZS(12)
+#undef MSQ_ZS
+        default: break;
+    }
 }
 
-// bit-sliced "Z <= c" over P planes (c < 2^P)
-__device__ __forceinline__ uint32_t planes_le(const uint32_t* zp, int base, int stride, int P, int c) {
-    uint32_t v[MAXP];
+// bit-sliced "Z <= c" over P planes (0 <= c < 2^P)
+template <int P>
+__device__ __forceinline__ uint32_t planes_le_t(const uint32_t* zp, int base, int stride, int c) {
+    uint32_t v[P];
 #pragma unroll
-    for (int q = 0; q < MAXP; ++q)
-        if (q < P) v[q] = zp[base + q * stride];
+    for (int q = 0; q < P; ++q) v[q] = zp[base + q * stride];
     uint32_t lt = 0, eq = 0xFFFFFFFFu;
 #pragma unroll
-    for (int q = MAXP - 1; q >= 0; --q) {
-        if (q < P) {
-            if ((c >> q) & 1) {
-                lt |= eq & ~v[q];
-                eq &= v[q];
-            } else {
-                eq &= ~v[q];
-            }
+    for (int q = P - 1; q >= 0; --q) {
+        if ((c >> q) & 1) {
+            lt |= eq & ~v[q];
+            eq &= v[q];
+        } else {
+            eq &= ~v[q];
         }
     }
     return lt | eq;
+}
+__device__ __forceinline__ uint32_t planes_le(const uint32_t* zp, int base, int stride, int P, int c) {
+    switch (P) {
+#define MSQ_LE(n) \
+    case n: return planes_le_t<n>(zp, base, stride, c);
+        MSQ_LE(1) MSQ_LE(2) MSQ_LE(3) MSQ_LE(4) MSQ_LE(5) MSQ_LE(6)
+        MSQ_LE(7) MSQ_LE(8) MSQ_LE(9) MSQ_LE(10) MSQ_LE(11) MSQ_LE(12)
+#undef MSQ_LE
+        default: return 0u;
+    }
 }
 
 template <bool U8, bool TMA>
@@ -528,7 +545,7 @@ struct Pass1Exact {
     __device__ __forceinline__ const uint8_t* grow(int b) const {
         return mbase + (size_t)(r0 + tile_row0 + b) * ld_bytes;
     }
-    __device__ uint32_t mask(int a, int b, int T) const {
+    __device__ __noinline__ uint32_t mask(int a, int b, int T) const {
         const uint32_t val = valid_mask(a, W, cols);
         const int lim = tile_row0 + b + 1 - T;
         if (lim < 0) return 0u;
@@ -542,7 +559,7 @@ struct Pass1Exact {
 // leftmost window of T consecutive ones in row X (smem, W words) starting at
 // column >= s0; one full warp; returns the start column or -1.  Segmented
 // warp scan of run lengths (R = full ? R_prev + 32 : suffix), chunk by chunk.
-__device__ int warp_first_window(const uint32_t* X, int W, int s0, int T, int lane) {
+__device__ __noinline__ int warp_first_window(const uint32_t* X, int W, int s0, int T, int lane) {
     int carry = 0;
     const int w0 = s0 >> 5;
     const uint32_t first_mask = ~((1u << (s0 & 31)) - 1u);
@@ -581,6 +598,40 @@ __device__ int warp_first_window(const uint32_t* X, int W, int s0, int T, int la
         carry = __shfl_sync(0xFFFFFFFFu, R, 31);
     }
     return -1;
+}
+
+// mode-S row tests of one thread's words (outlined: keeps the hot loop's
+// register pressure down)
+__device__ __noinline__ uint32_t test_rows_s(const uint32_t* hist, int Wpad, int W, int WPT, int tau, int start_b,
+                                             int lastb, int full_from, uint32_t dirty, int m, int T) {
+    uint32_t best = RES_INF;
+    for (int b = start_b; b <= lastb; ++b) {
+        const bool full = b >= full_from;
+        for (int k = 0; k < WPT; ++k) {
+            const int a = tau * WPT + k;
+            if (a < W) {
+                if (full)
+                    test_word_full(hist, Wpad, W, b, m, a, T, best);
+                else if ((dirty >> (b * WPT + k)) & 1u)
+                    test_word_incr(hist, Wpad, W, b, m, a, T, best);
+            }
+        }
+    }
+    return best;
+}
+
+// band outputs: bottom run b_j = H - z_j from the last-zero planes
+__device__ __noinline__ void band_bottom_runs(const uint32_t* zp, int zbase, int Wpad, int P, int H, uint16_t* bo) {
+    uint32_t zb[MAXP];
+#pragma unroll
+    for (int q = 0; q < MAXP; ++q) zb[q] = q < P ? zp[zbase + q * Wpad] : 0u;
+#pragma unroll 1
+    for (int j = 0; j < 32; ++j) {
+        int z = 0;
+#pragma unroll
+        for (int q = 0; q < MAXP; ++q) z |= (int)((zb[q] >> j) & 1u) << q;
+        bo[j] = (uint16_t)(H - z);
+    }
 }
 
 // ============================================================= pass 1 kernel
@@ -694,6 +745,8 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 
         // ---------------------------------------------------- phase A
         uint32_t dirty = 0, zflag = 0;
+        const int st0 = TMA ? row0 % p.nstage : 0;
+        const uint32_t par0 = TMA ? (uint32_t)((row0 / p.nstage) & 1) : 0u;
 #pragma unroll
         for (int b = 0; b < BMAX; ++b) {
             if (b < nrows) {
@@ -701,8 +754,9 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 const int rho = r + 1;
                 const uint8_t* srow = nullptr;
                 if (TMA) {
-                    mbar_wait(&bars[r % p.nstage], (uint32_t)((r / p.nstage) & 1));
-                    srow = ring + (size_t)(r % p.nstage) * p.rs;
+                    const int sb = st0 + b >= p.nstage ? st0 + b - p.nstage : st0 + b;
+                    mbar_wait(&bars[sb], st0 + b >= p.nstage ? par0 ^ 1u : par0);
+                    srow = ring + (size_t)sb * p.rs;
                 }
                 uint32_t w[WPT];
                 fetch_words<WPT, U8, TMA>(srow, mbase + (size_t)(r0 + r) * p.ld_bytes, tau, W, p.cols, p.rs,
@@ -800,19 +854,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                         });
                     }
                 } else {
-                    for (int b = start_b; b <= lastb; ++b) {
-                        const bool full = b >= full_from;
-#pragma unroll
-                        for (int k = 0; k < WPT; ++k) {
-                            const int a = tau * WPT + k;
-                            if (a < W) {
-                                if (full)
-                                    test_word_full(hist, Wpad, W, b, m, a, cur_t, best);
-                                else if ((dirty >> (b * WPT + k)) & 1u)
-                                    test_word_incr(hist, Wpad, W, b, m, a, cur_t, best);
-                            }
-                        }
-                    }
+                    best = test_rows_s(hist, Wpad, W, WPT, tau, start_b, lastb, full_from, dirty, m, cur_t);
                 }
                 const int slot = round_ctr % 3;
                 if (best != RES_INF) atomicMin(&misc->res[slot], best);
@@ -862,7 +904,8 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
             const int b = bit / WPT, k = bit - b * WPT;
             const int r = row0 + b, rho = r + 1;
             const int a = tau * WPT + k;
-            const uint8_t* srow = TMA ? ring + (size_t)(r % p.nstage) * p.rs : nullptr;
+            const uint8_t* srow =
+                TMA ? ring + (size_t)(st0 + b >= p.nstage ? st0 + b - p.nstage : st0 + b) * p.rs : nullptr;
             const uint32_t wv =
                 word_of_row<U8, TMA>(srow, mbase + (size_t)(r0 + r) * p.ld_bytes, a, p.cols, p.rs);
             const uint32_t zeros = VAL[k] & ~wv;
@@ -905,17 +948,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     nz &= nz - 1;
                     p.e_out[cb + j] = (uint16_t)H;
                 }
-                uint32_t zb[MAXP];
-#pragma unroll
-                for (int q = 0; q < MAXP; ++q) zb[q] = q < P ? zp[q * Wpad + k * NT + tau] : 0u;
-                uint16_t* bo = p.zb + (size_t)unit * p.cols_pad + (size_t)a * 32;
-#pragma unroll 1
-                for (int j = 0; j < 32; ++j) {
-                    int z = 0;
-#pragma unroll
-                    for (int q = 0; q < MAXP; ++q) z |= (int)((zb[q] >> j) & 1u) << q;
-                    bo[j] = (uint16_t)(H - z);
-                }
+                band_bottom_runs(zp, k * NT + tau, Wpad, P, H, p.zb + (size_t)unit * p.cols_pad + (size_t)a * 32);
                 p.ao_out[(size_t)band * W + a] = NZ[k];
             }
         }
