@@ -327,13 +327,13 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
         while (ts < words) ts *= 2;
         p.team = ts;
         p.nbands = 1;
-        p.tile_rows = msq::BMAX;
-        p.tile_rows_l = msq::BMAX;
+        p.tile_rows = 4;
+        p.tile_rows_l = 4;
         long long tpc = std::max<long long>(1, ceil_div(batch, sms));
         const long long gran = std::max(1, 32 / ts);  // teams per warp
         tpc = round_up(tpc, gran);
         tpc = std::min<long long>(tpc, 512 / ts);
-        p.nstage = tma_ok ? 2 * msq::BMAX : 0;  // ring holds the previous and the current tile
+        p.nstage = tma_ok ? 2 * 4 : 0;  // ring holds the previous and the current tile
         for (;;) {
             const long long per = msq::p1_layout(ts, 1, p.nstage, (int)row_bytes, p.tile_rows, zplanes_for(&p),
                                                  p.nstage > 0, false)
@@ -384,7 +384,7 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
         const int base = msq::p1_layout(p.threads, p.wpt, 0, (int)row_bytes, p.tile_rows, P, true, false).total;
         long long ns = (kSmemMax - base - 512) / row_bytes;
         ns = std::min<long long>(ns, 32);
-        if (ns < 2 * p.tile_rows_l) p.tile_rows_l = p.tile_rows;
+        while (p.tile_rows_l > p.tile_rows && ns < 2 * p.tile_rows_l) p.tile_rows_l /= 2;
         if (ns >= 2 * p.tile_rows_l) p.nstage = (int32_t)ns;
     }
     p.smem_pass1 = team_layout_bytes(&p);

@@ -39,7 +39,7 @@ constexpr int KEY_DIM_BITS = 21;
 constexpr unsigned long long KEY_DIM_MASK = (1ull << KEY_DIM_BITS) - 1ull;
 constexpr uint32_t RES_INF = 0xFFFFFFFFu;
 constexpr int NPLANES = 7;   // mode S counters saturate at 127
-constexpr int BMAX = 4;      // max rows per tile
+constexpr int BMAX = 8;      // max rows per tile
 constexpr int FIX_XPL = 6;   // fix-up mode X planes (c, e clamped at 63)
 constexpr int FIX_TL = 63;   // fix-up mode L threshold (runs then contain a full word)
 constexpr int MAXP = 12;     // last-zero bit planes: bands are <= 4095 rows
@@ -61,7 +61,7 @@ __host__ __device__ __forceinline__ int r16(int x) { return (x + 15) & ~15; }
 
 // ------------------------------------------------------------ smem layouts
 struct P1Layout {
-    int ring, bars, ebars, zp, hist, fmap, misc, total;
+    int ring, bars, ebars, zp, ab, hist, fmap, misc, total;
 };
 // per team; zp holds P bit-planes of the last-zero rows, hist bs rows of E
 // words, fmap 2 x BMAX rows of F bits; ebars = empty barriers of the
@@ -79,6 +79,8 @@ __host__ __device__ inline P1Layout p1_layout(int NT, int WPT, int nstage, int r
     if (ebar) off += r16(nstage * 8);
     L.zp = off;
     off += P * wpad * 4;
+    L.ab = off;  // prefix-AND of the band top at the row above the tile (climb tiles)
+    off += wpad * 4;
     L.hist = off;
     off += bs * wpad * 4;
     L.fmap = off;
@@ -305,7 +307,8 @@ __device__ __forceinline__ int* res_best(unsigned char* r) { return (int*)(r + 2
 struct Misc {
     uint32_t res[3];
     int g;
-    int pad[12];
+    int cres[BMAX];  // climb: leftmost window start per tile row (-1 = none)
+    int pad[4];
 };
 
 // bit-sliced saturating increment (reset on zero): planes h[0..P-1]
@@ -559,13 +562,14 @@ struct Pass1Exact {
 // leftmost window of T consecutive ones in row X (smem, W words) starting at
 // column >= s0; one full warp; returns the start column or -1.  Segmented
 // warp scan of run lengths (R = full ? R_prev + 32 : suffix), chunk by chunk.
-__device__ __noinline__ int warp_first_window(const uint32_t* X, int W, int s0, int T, int lane) {
+template <class Fetch>
+__device__ __forceinline__ int warp_first_window(const Fetch& X, int W, int s0, int T, int lane) {
     int carry = 0;
     const int w0 = s0 >> 5;
     const uint32_t first_mask = ~((1u << (s0 & 31)) - 1u);
     for (int base = w0; base < W; base += 32) {
         const int w = base + lane;
-        uint32_t x = (w < W) ? X[w] : 0u;
+        uint32_t x = (w < W) ? X(w) : 0u;
         if (w == w0) x &= first_mask;
         const bool full = x == 0xFFFFFFFFu;
         const int pre = prefix_ones(x);
@@ -598,6 +602,44 @@ __device__ __noinline__ int warp_first_window(const uint32_t* X, int W, int s0, 
         carry = __shfl_sync(0xFFFFFFFFu, R, 31);
     }
     return -1;
+}
+
+// climb tile row b: prefix-AND of the band top = ab & tile rows 0..b
+template <bool U8, bool TMA>
+struct ClimbRow {
+    const uint32_t* ab;
+    const Pass1Exact<U8, TMA>* ex;
+    int b;
+    __device__ __forceinline__ uint32_t operator()(int w) const {
+        uint32_t x = ab[w];
+        for (int q = 0; q <= b; ++q) x &= word_of_row<U8, TMA>(ex->srow(q), ex->grow(q), w, ex->cols, ex->rs);
+        return x;
+    }
+};
+
+template <bool U8, bool TMA>
+__device__ __noinline__ int climb_scan(const uint32_t* ab, const Pass1Exact<U8, TMA>* ex, int b, int W, int s0, int T,
+                                       int lane) {
+    const ClimbRow<U8, TMA> f{ab, ex, b};
+    return warp_first_window(f, W, s0, T, lane);
+}
+
+// exact eligibility of word a at tile row b for any threshold T (rows after a
+// climb failure): last zero <= rho_b - T, from the planes (row above the tile)
+// and the zeros of tile rows 0..b that are later than rho_b - T
+template <bool U8, bool TMA>
+__device__ __noinline__ uint32_t exact_row_mask(const Pass1Exact<U8, TMA>* ex, int a, int b, int T) {
+    const uint32_t val = valid_mask(a, ex->W, ex->cols);
+    const int rho_b = ex->tile_row0 + b + 1;
+    const int lim = rho_b - T;
+    if (lim < 0) return 0u;
+    uint32_t late = 0;
+    for (int q = 0; q <= b; ++q)
+        if (ex->tile_row0 + q + 1 > lim) late |= ~word_of_row<U8, TMA>(ex->srow(q), ex->grow(q), a, ex->cols, ex->rs);
+    const uint32_t le = (lim >= (1 << ex->P)) ? 0xFFFFFFFFu
+                                              : planes_le(ex->zp, zp_index(a, 0, ex->WPT, ex->NT, ex->Wpad), ex->Wpad,
+                                                          ex->P, lim);
+    return le & ~late & val;
 }
 
 // mode-S row tests of one thread's words (outlined: keeps the hot loop's
@@ -670,6 +712,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     uint8_t* ring = tsm + Lo.ring;
     uint64_t* bars = (uint64_t*)(tsm + Lo.bars);
     uint32_t* zp = (uint32_t*)(tsm + Lo.zp);  // bit-sliced last-zero rows
+    uint32_t* ab = (uint32_t*)(tsm + Lo.ab);  // prefix-AND of the band top, row above the tile
     uint32_t* hist = (uint32_t*)(tsm + Lo.hist);
     uint32_t* fmap = (uint32_t*)(tsm + Lo.fmap);
     Misc* misc = (Misc*)(tsm + Lo.misc);
@@ -681,6 +724,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 
     // ---- setup
     for (int i = tau; i < P * Wpad; i += NT) zp[i] = 0u;
+    for (int i = tau; i < Wpad; i += NT) ab[i] = valid_mask(i, W, p.cols);
     for (int i = tau; i < 2 * BMAX * fstride; i += NT) fmap[i] = 0u;
     if (tau == 0) {
         misc->res[0] = misc->res[1] = misc->res[2] = RES_INF;
@@ -738,7 +782,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         const bool climb = t >= rho0;
         const bool modeL = !climb && t >= p.tl;
         const bool modeS = !climb && !modeL;
-        const int nrows = climb ? 1 : min(modeL ? p.bl : p.bs, H - row0);
+        const int nrows = min(climb ? (SUB ? 1 : p.bl) : (modeL ? p.bl : p.bs), H - row0);
         uint32_t* fm = fmap + (tile & 1) * BMAX * fstride;
         int polled = 0;
         if (p.share && tau == 0 && (tile & 7) == 7) polled = ld_volatile(res_best(result));
@@ -769,7 +813,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     zflag |= (z ? 1u : 0u) << (b * WPT + k);
                     AL[k] &= w[k];
                     if (climb) {
-                        hist[b * Wpad + tau * WPT + k] = AL[k];
+                        if (SUB) hist[b * Wpad + tau * WPT + k] = AL[k];
                     } else if (modeL) {
                         fnib |= ((VAL[k] == 0xFFFFFFFFu && ZW[k] <= rho - t) ? 1u : 0u) << k;
                     } else {  // mode S: last-zero planes updated now; E = {z <= rho - t}
@@ -808,34 +852,87 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         int cur_t = t;
         const Pass1Exact<U8, TMA> ex{zp, ring, mbase, p.ld_bytes, W, p.cols, p.rs, p.nstage, P, WPT, NT, Wpad,
                                      row0, r0};
-        if (climb) {
+        if (climb && SUB) {
             if (t == rho0) {  // E = prefix-AND of the band top; leftmost t-window
-                if (!SUB) {
-                    if (tid < 32) {
-                        const int start = warp_first_window(hist, W, climb_s, t, lane);
-                        if (lane == 0) misc->res[0] = (uint32_t)start;
-                    }
-                } else {
-                    uint32_t best = RES_INF;
+                uint32_t best = RES_INF;
 #pragma unroll
-                    for (int k = 0; k < WPT; ++k) {
-                        const int a = tau * WPT + k;
-                        if (a < W) test_word_full(hist, Wpad, W, 0, 0, a, t, best);
-                    }
-                    if (best != RES_INF) atomicMin(&misc->res[0], best);
+                for (int k = 0; k < WPT; ++k) {
+                    const int a = tau * WPT + k;
+                    if (a < W) test_word_full(hist, Wpad, W, 0, 0, a, t, best);
                 }
+                const int slot = round_ctr % 3;
+                if (best != RES_INF) atomicMin(&misc->res[slot], best);
+                if (tau == 0) misc->res[(round_ctr + 1) % 3] = RES_INF;
                 csync();  // (B)
-                const uint32_t rr = misc->res[0];
-                csync();
-                if (tau == 0) misc->res[0] = RES_INF;
-                const int start = (rr == RES_INF) ? -1 : (int)(rr & 0xFFFFFu);
-                if (start >= 0) {
+                const uint32_t rr = misc->res[slot];
+                ++round_ctr;
+                if (rr != RES_INF) {
+                    const int start = (int)(rr & 0xFFFFFu);
                     if (tau == 0) {
                         bandkey = pack_key(t, p.row_base + r0 + row0, start + t - 1);
                         if (p.share) atomicMax(res_best(result), t);
                     }
-                    climb_s = start;
                     cur_t = t + 1;
+                }
+            }
+        } else if (climb) {
+            // heights are <= rho, so the only rows with a test are rho >= t; a
+            // test at rho == t asks for a t-window in the prefix-AND A(rho), and
+            // success is monotone in rho: test every row of the tile in parallel
+            // (warp w takes row bfirst + w) and keep the last success.
+            const int bfirst = t - rho0;
+            if (bfirst <= lastb) {
+                const int wid = tid >> 5;
+                const int b = bfirst + wid;
+                if (b <= lastb) {
+                    const int st = climb_scan<U8, TMA>(ab, &ex, b, W, climb_s, rho0 + b, lane);
+                    if (lane == 0) misc->cres[wid] = st;
+                }
+                csync();  // (B)
+                int nsucc = 0, last_start = -1;
+                for (int w2 = 0; w2 <= lastb - bfirst; ++w2) {
+                    const int st = misc->cres[w2];
+                    if (st < 0) break;
+                    ++nsucc;
+                    last_start = st;
+                }
+                if (nsucc > 0) {
+                    cur_t = t + nsucc;  // rows rho0+bfirst .. +nsucc-1 raised once each
+                    if (tau == 0) {
+                        bandkey = pack_key(cur_t - 1, p.row_base + r0 + row0 + bfirst + nsucc - 1,
+                                           last_start + cur_t - 2);
+                        if (p.share) atomicMax(res_best(result), cur_t - 1);
+                    }
+                    climb_s = last_start;
+                }
+                // rows after the failing row are general rows: exact E at cur_t
+                for (int bg = bfirst + nsucc + 1; bg <= lastb; ++bg) {
+#pragma unroll
+                    for (int k = 0; k < WPT; ++k) {
+                        const int a = tau * WPT + k;
+                        hist[a] = a < W ? exact_row_mask<U8, TMA>(&ex, a, bg, cur_t) : 0u;
+                    }
+                    csync();
+                    uint32_t best = RES_INF;
+#pragma unroll
+                    for (int k = 0; k < WPT; ++k) {
+                        const int a = tau * WPT + k;
+                        if (a < W) test_word_full(hist, Wpad, W, 0, 0, a, cur_t, best);
+                    }
+                    const int slot = round_ctr % 3;
+                    if (best != RES_INF) atomicMin(&misc->res[slot], best);
+                    if (tau == 0) misc->res[(round_ctr + 1) % 3] = RES_INF;
+                    csync();
+                    const uint32_t rr = misc->res[slot];
+                    ++round_ctr;
+                    if (rr != RES_INF) {
+                        const int col = (int)(rr & 0xFFFFFu);
+                        if (tau == 0) {
+                            bandkey = pack_key(cur_t, p.row_base + r0 + row0 + bg, col + cur_t - 1);
+                            if (p.share) atomicMax(res_best(result), cur_t);
+                        }
+                        ++cur_t;
+                    }
                 }
             }
         } else {
@@ -892,8 +989,10 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 jumped = true;
             }
         }
-        full_next = raised || jumped;
+        full_next = raised || jumped || climb;
         if (!climb || !raised) climb_s = 0;
+#pragma unroll
+        for (int k = 0; k < WPT; ++k) ab[tau * WPT + k] = AL[k];
 
         // ---------------------------------------------------- phase C
         // last-zero rows (bit-sliced) and first zeros, in row order per word
