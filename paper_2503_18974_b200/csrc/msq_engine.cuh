@@ -882,11 +882,10 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
             // (warp w takes row bfirst + w) and keep the last success.
             const int bfirst = t - rho0;
             if (bfirst <= lastb) {
-                const int wid = tid >> 5;
-                const int b = bfirst + wid;
-                if (b <= lastb) {
+                const int wid = tid >> 5, nwarps = NT >> 5;
+                for (int b = bfirst + wid; b <= lastb; b += nwarps) {
                     const int st = climb_scan<U8, TMA>(ab, &ex, b, W, climb_s, rho0 + b, lane);
-                    if (lane == 0) misc->cres[wid] = st;
+                    if (lane == 0) misc->cres[b - bfirst] = st;
                 }
                 csync();  // (B)
                 int nsucc = 0, last_start = -1;
