@@ -67,6 +67,7 @@ WsLayout ws_layout(const msq_plan* p) {
 
 // ------------------------------------------------------------- dispatch
 int zplanes_for(const msq_plan* pl) {
+    if (pl->fmt != MSQ_FMT_U8) return 0;  // bits inputs keep last-zero rows in global scratch
     const long long hmax = ceil_div(pl->rows, pl->nbands);
     int P = 1;
     while ((1ll << P) <= hmax) ++P;

@@ -61,7 +61,7 @@ __host__ __device__ __forceinline__ int r16(int x) { return (x + 15) & ~15; }
 
 // ------------------------------------------------------------ smem layouts
 struct P1Layout {
-    int ring, bars, ebars, zp, ab, hist, fmap, misc, total;
+    int ring, bars, ebars, zp, za, nzm, ab, hist, fmap, misc, total;
 };
 // per team; zp holds P bit-planes of the last-zero rows, hist bs rows of E
 // words, fmap 2 x BMAX rows of F bits; ebars = empty barriers of the
@@ -79,6 +79,10 @@ __host__ __device__ inline P1Layout p1_layout(int NT, int WPT, int nstage, int r
     if (ebar) off += r16(nstage * 8);
     L.zp = off;
     off += P * wpad * 4;
+    L.za = off;  // global-z mode: last all-zero row per word
+    off += r16(wpad * 2);
+    L.nzm = off;  // global-z mode: never-zeroed column masks
+    off += wpad * 4;
     L.ab = off;  // prefix-AND of the band top at the row above the tile (climb tiles)
     off += wpad * 4;
     L.hist = off;
@@ -533,9 +537,17 @@ __device__ __forceinline__ uint32_t planes_le(const uint32_t* zp, int base, int 
     }
 }
 
+// Per-column last-zero rows z_j (0 = no zero in the band yet) live either in
+// smem bit planes (u8 inputs: dense zero events, updated with P-plane
+// read-modify-writes) or, for bit-packed inputs (sparse zero events), as
+// uint16 in L2-resident global scratch with one store per zero bit, a lazy
+// all-zero row per word (za) and the never-zeroed masks (nzm) in smem.
 template <bool U8, bool TMA>
 struct Pass1Exact {
     const uint32_t* zp;
+    const uint16_t* zg;   // global z (bits inputs)
+    const uint16_t* za;
+    const uint32_t* nzm;
     const uint8_t* ring;
     const uint8_t* mbase;
     long long ld_bytes;
@@ -548,14 +560,31 @@ struct Pass1Exact {
     __device__ __forceinline__ const uint8_t* grow(int b) const {
         return mbase + (size_t)(r0 + tile_row0 + b) * ld_bytes;
     }
+    // columns of word a whose last zero (before the current tile) is <= lim (lim >= 0)
+    __device__ __forceinline__ uint32_t z_le(int a, int lim) const {
+        if (U8) return (lim >= (1 << P)) ? 0xFFFFFFFFu : planes_le(zp, zp_index(a, 0, WPT, NT, Wpad), Wpad, P, lim);
+        if ((int)za[a] > lim) return 0u;
+        uint32_t m = nzm[a];
+        const uint4* zq = (const uint4*)(zg + (size_t)a * 32);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint4 v = zq[q];
+            const uint32_t pr[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                m |= ((int)(pr[h] & 0xFFFFu) <= lim ? 1u : 0u) << (8 * q + 2 * h);
+                m |= ((int)(pr[h] >> 16) <= lim ? 1u : 0u) << (8 * q + 2 * h + 1);
+            }
+        }
+        return m;
+    }
     __device__ __noinline__ uint32_t mask(int a, int b, int T) const {
         const uint32_t val = valid_mask(a, W, cols);
         const int lim = tile_row0 + b + 1 - T;
         if (lim < 0) return 0u;
         uint32_t zin = 0;
         for (int q = 0; q <= b; ++q) zin |= ~word_of_row<U8, TMA>(srow(q), grow(q), a, cols, rs);
-        const uint32_t le = (lim >= (1 << P)) ? 0xFFFFFFFFu : planes_le(zp, zp_index(a, 0, WPT, NT, Wpad), Wpad, P, lim);
-        return le & val & ~zin;
+        return z_le(a, lim) & val & ~zin;
     }
 };
 
@@ -636,10 +665,7 @@ __device__ __noinline__ uint32_t exact_row_mask(const Pass1Exact<U8, TMA>* ex, i
     uint32_t late = 0;
     for (int q = 0; q <= b; ++q)
         if (ex->tile_row0 + q + 1 > lim) late |= ~word_of_row<U8, TMA>(ex->srow(q), ex->grow(q), a, ex->cols, ex->rs);
-    const uint32_t le = (lim >= (1 << ex->P)) ? 0xFFFFFFFFu
-                                              : planes_le(ex->zp, zp_index(a, 0, ex->WPT, ex->NT, ex->Wpad), ex->Wpad,
-                                                          ex->P, lim);
-    return le & ~late & val;
+    return ex->z_le(a, lim) & ~late & val;
 }
 
 // mode-S row tests of one thread's words (outlined: keeps the hot loop's
@@ -704,7 +730,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     const int fstride = r16(nfw * 4) / 4;
     const int r0 = band_row0(p.rows, p.nbands, band);
     const int H = band_row0(p.rows, p.nbands, band + 1) - r0;
-    const int P = p.zplanes;
+    const int P = U8 ? p.zplanes : 0;  // bit planes only for u8 inputs
     unsigned char* result = p.results + (size_t)mat * 32;
 
     const P1Layout Lo = p1_layout(NT, WPT, p.nstage, p.rs, p.bs, P, TMA, false);
@@ -713,6 +739,9 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     uint64_t* bars = (uint64_t*)(tsm + Lo.bars);
     uint32_t* zp = (uint32_t*)(tsm + Lo.zp);  // bit-sliced last-zero rows
     uint32_t* ab = (uint32_t*)(tsm + Lo.ab);  // prefix-AND of the band top, row above the tile
+    uint16_t* za = (uint16_t*)(tsm + Lo.za);
+    uint32_t* nzm = (uint32_t*)(tsm + Lo.nzm);
+    uint16_t* zg = p.zb + (size_t)unit * p.cols_pad;  // bits inputs: global last-zero rows
     uint32_t* hist = (uint32_t*)(tsm + Lo.hist);
     uint32_t* fmap = (uint32_t*)(tsm + Lo.fmap);
     Misc* misc = (Misc*)(tsm + Lo.misc);
@@ -724,7 +753,11 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 
     // ---- setup
     for (int i = tau; i < P * Wpad; i += NT) zp[i] = 0u;
-    for (int i = tau; i < Wpad; i += NT) ab[i] = valid_mask(i, W, p.cols);
+    for (int i = tau; i < Wpad; i += NT) {
+        ab[i] = valid_mask(i, W, p.cols);
+        nzm[i] = valid_mask(i, W, p.cols);
+        za[i] = 0;
+    }
     for (int i = tau; i < 2 * BMAX * fstride; i += NT) fmap[i] = 0u;
     if (tau == 0) {
         misc->res[0] = misc->res[1] = misc->res[2] = RES_INF;
@@ -757,6 +790,44 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         EPREV[k] = 0;
         ZW[k] = 0;
     }
+
+    // side effects of the zeros of own word k at row rho: last-zero rows
+    // (optional), first zeros (e_out) and the never-zeroed masks
+    auto apply_event = [&](int k, int a, int rho, uint32_t zeros, bool do_z) {
+        uint32_t newly = NZ[k] & zeros;
+        if (do_z) {
+            if (U8) {
+                zplanes_set(zp, k * NT + tau, Wpad, P, zeros, rho);
+            } else if (zeros == VAL[k]) {
+                za[a] = (uint16_t)rho;  // whole word zero: lazy row; first zeros read as <= za
+                uint32_t nn = newly;
+                while (nn) {
+                    const int j = __ffs(nn) - 1;
+                    nn &= nn - 1;
+                    zg[(size_t)a * 32 + j] = 0;
+                }
+            } else {
+                uint32_t zz = zeros;
+                while (zz) {
+                    const int j = __ffs(zz) - 1;
+                    zz &= zz - 1;
+                    zg[(size_t)a * 32 + j] = (uint16_t)rho;
+                }
+            }
+        }
+        if (newly) {
+            if (p.write_summaries) {
+                const size_t cb = sum_base + (size_t)a * 32;
+                while (newly) {
+                    const int j = __ffs(newly) - 1;
+                    newly &= newly - 1;
+                    p.e_out[cb + j] = (uint16_t)(rho - 1);
+                }
+            }
+            NZ[k] &= ~zeros;
+            if (!U8) nzm[a] = NZ[k];
+        }
+    };
 
     int t = max(1, misc->g);
     bool full_next = false;
@@ -816,11 +887,26 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                         if (SUB) hist[b * Wpad + tau * WPT + k] = AL[k];
                     } else if (modeL) {
                         fnib |= ((VAL[k] == 0xFFFFFFFFu && ZW[k] <= rho - t) ? 1u : 0u) << k;
-                    } else {  // mode S: last-zero planes updated now; E = {z <= rho - t}
+                    } else {  // mode S: last-zero rows updated now; E = {z <= rho - t}
                         const int zi = k * NT + tau;
-                        if (z) zplanes_set(zp, zi, Wpad, P, VAL[k] & ~w[k], rho);
                         const int lim = rho - t;
-                        const uint32_t e = (lim >= (1 << P) ? 0xFFFFFFFFu : planes_le(zp, zi, Wpad, P, lim)) & VAL[k];
+                        uint32_t e;
+                        if (U8) {
+                            if (z) zplanes_set(zp, zi, Wpad, P, VAL[k] & ~w[k], rho);
+                            e = (lim >= (1 << P) ? 0xFFFFFFFFu : planes_le(zp, zi, Wpad, P, lim)) & VAL[k];
+                        } else {  // bits inputs, small threshold: slow path through global z
+                            const int a = tau * WPT + k;
+                            if (z) apply_event(k, a, rho, VAL[k] & ~w[k], true);
+                            e = 0;
+                            if (VAL[k] && lim >= 0) {
+                                if ((int)za[a] <= lim) {
+                                    e = NZ[k];
+                                    for (int j = 0; j < 32; ++j)
+                                        if (!((NZ[k] >> j) & 1u) && (int)zg[(size_t)a * 32 + j] <= lim) e |= 1u << j;
+                                }
+                                e &= VAL[k];
+                            }
+                        }
                         if (e & ~EPREV[k]) dirty |= 1u << (b * WPT + k);
                         EPREV[k] = e;
                         hist[b * Wpad + tau * WPT + k] = e;
@@ -850,7 +936,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         // ---------------------------------------------------- phase B
         const int lastb = nrows - 1;
         int cur_t = t;
-        const Pass1Exact<U8, TMA> ex{zp, ring, mbase, p.ld_bytes, W, p.cols, p.rs, p.nstage, P, WPT, NT, Wpad,
+        const Pass1Exact<U8, TMA> ex{zp, zg, za, nzm, ring, mbase, p.ld_bytes, W, p.cols, p.rs, p.nstage, P, WPT, NT, Wpad,
                                      row0, r0};
         if (climb && SUB) {
             if (t == rho0) {  // E = prefix-AND of the band top; leftmost t-window
@@ -1007,19 +1093,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
             const uint32_t wv =
                 word_of_row<U8, TMA>(srow, mbase + (size_t)(r0 + r) * p.ld_bytes, a, p.cols, p.rs);
             const uint32_t zeros = VAL[k] & ~wv;
-            if (!modeS) zplanes_set(zp, k * NT + tau, Wpad, P, zeros, rho);
-            uint32_t newly = NZ[k] & zeros;
-            if (newly) {
-                if (p.write_summaries) {
-                    const size_t cb = sum_base + (size_t)a * 32;
-                    while (newly) {
-                        const int j = __ffs(newly) - 1;
-                        newly &= newly - 1;
-                        p.e_out[cb + j] = (uint16_t)(rho - 1);
-                    }
-                }
-                NZ[k] &= ~zeros;
-            }
+            if (!modeS || U8) apply_event(k, a, rho, zeros, !modeS);
         }
         if (modeL)
             for (int i = tau; i < BMAX * fstride; i += NT) fm[i] = 0u;
@@ -1046,7 +1120,26 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     nz &= nz - 1;
                     p.e_out[cb + j] = (uint16_t)H;
                 }
-                band_bottom_runs(zp, k * NT + tau, Wpad, P, H, p.zb + (size_t)unit * p.cols_pad + (size_t)a * 32);
+                if (U8) {
+                    band_bottom_runs(zp, k * NT + tau, Wpad, P, H, p.zb + (size_t)unit * p.cols_pad + (size_t)a * 32);
+                } else {  // bottom runs overwrite the global last-zero rows in place
+                    const int zaa = za[a];
+                    uint4* zq = (uint4*)(zg + (size_t)a * 32);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint4 zv = zq[q];
+                        const uint32_t pr[4] = {zv.x, zv.y, zv.z, zv.w};
+                        uint32_t v[4];
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            const int j0 = 8 * q + 2 * h;
+                            const int u0 = ((NZ[k] >> j0) & 1u) ? 0 : max((int)(pr[h] & 0xFFFFu), zaa);
+                            const int u1 = ((NZ[k] >> (j0 + 1)) & 1u) ? 0 : max((int)(pr[h] >> 16), zaa);
+                            v[h] = (uint32_t)(H - u0) | ((uint32_t)(H - u1) << 16);
+                        }
+                        zq[q] = make_uint4(v[0], v[1], v[2], v[3]);
+                    }
+                }
                 p.ao_out[(size_t)band * W + a] = NZ[k];
             }
         }
