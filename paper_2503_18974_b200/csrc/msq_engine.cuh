@@ -554,8 +554,9 @@ struct Pass1Exact {
     int W, cols, rs, nstage, P, WPT, NT, Wpad;
     int tile_row0;  // band-relative 0-based row of tile row 0
     int r0;         // band top row (matrix)
+    int st0;        // ring stage of tile row 0
     __device__ __forceinline__ const uint8_t* srow(int b) const {
-        return TMA ? ring + (size_t)((tile_row0 + b) % nstage) * rs : nullptr;
+        return TMA ? ring + (size_t)(st0 + b >= nstage ? st0 + b - nstage : st0 + b) * rs : nullptr;
     }
     __device__ __forceinline__ const uint8_t* grow(int b) const {
         return mbase + (size_t)(r0 + tile_row0 + b) * ld_bytes;
@@ -773,10 +774,9 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     int issued = 0;  // rows staged so far (issuer thread)
     if (TMA && tau == issuer) {
         for (; issued < min(p.nstage, H); ++issued) {
-            const int s = issued % p.nstage;
-            mbar_expect_tx(&bars[s], (uint32_t)p.row_bytes);
-            tma_row(ring + (size_t)s * p.rs, mbase + (size_t)(r0 + issued) * p.ld_bytes, (uint32_t)p.row_bytes,
-                    &bars[s], pol);
+            mbar_expect_tx(&bars[issued], (uint32_t)p.row_bytes);
+            tma_row(ring + (size_t)issued * p.rs, mbase + (size_t)(r0 + issued) * p.ld_bytes, (uint32_t)p.row_bytes,
+                    &bars[issued], pol);
         }
     }
 
@@ -829,6 +829,13 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         }
     };
 
+    uint32_t fullk = 0;  // words whose 32 columns are all valid (only those can be F)
+#pragma unroll
+    for (int k = 0; k < WPT; ++k) fullk |= (VAL[k] == 0xFFFFFFFFu ? 1u : 0u) << k;
+    int st_base = 0;          // ring stage of the tile's first row
+    uint32_t par_base = 0u;   // its mbarrier phase parity
+    int iss_s = 0;            // issuer: stage of the next row to stage
+
     int t = max(1, misc->g);
     bool full_next = false;
     int climb_s = 0;
@@ -860,34 +867,29 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 
         // ---------------------------------------------------- phase A
         uint32_t dirty = 0, zflag = 0;
-        const int st0 = TMA ? row0 % p.nstage : 0;
-        const uint32_t par0 = TMA ? (uint32_t)((row0 / p.nstage) & 1) : 0u;
+        const int st0 = st_base;
+        const uint32_t par0 = par_base;
+        if (!climb && !modeL) {  // ---- mode S (small threshold): E rows for the tests
 #pragma unroll
-        for (int b = 0; b < BMAX; ++b) {
-            if (b < nrows) {
-                const int r = row0 + b;
-                const int rho = r + 1;
-                const uint8_t* srow = nullptr;
-                if (TMA) {
-                    const int sb = st0 + b >= p.nstage ? st0 + b - p.nstage : st0 + b;
-                    mbar_wait(&bars[sb], st0 + b >= p.nstage ? par0 ^ 1u : par0);
-                    srow = ring + (size_t)sb * p.rs;
-                }
-                uint32_t w[WPT];
-                fetch_words<WPT, U8, TMA>(srow, mbase + (size_t)(r0 + r) * p.ld_bytes, tau, W, p.cols, p.rs,
-                                          VAL, w, bad_or);
-                uint32_t fnib = 0;
+            for (int b = 0; b < BMAX; ++b) {
+                if (b < nrows) {
+                    const int r = row0 + b;
+                    const int rho = r + 1;
+                    const uint8_t* srow = nullptr;
+                    if (TMA) {
+                        const int sb = st0 + b >= p.nstage ? st0 + b - p.nstage : st0 + b;
+                        mbar_wait(&bars[sb], st0 + b >= p.nstage ? par0 ^ 1u : par0);
+                        srow = ring + (size_t)sb * p.rs;
+                    }
+                    uint32_t w[WPT];
+                    fetch_words<WPT, U8, TMA>(srow, mbase + (size_t)(r0 + r) * p.ld_bytes, tau, W, p.cols, p.rs,
+                                              VAL, w, bad_or);
 #pragma unroll
-                for (int k = 0; k < WPT; ++k) {
-                    const bool z = w[k] != VAL[k];
-                    ZW[k] = z ? rho : ZW[k];
-                    zflag |= (z ? 1u : 0u) << (b * WPT + k);
-                    AL[k] &= w[k];
-                    if (climb) {
-                        if (SUB) hist[b * Wpad + tau * WPT + k] = AL[k];
-                    } else if (modeL) {
-                        fnib |= ((VAL[k] == 0xFFFFFFFFu && ZW[k] <= rho - t) ? 1u : 0u) << k;
-                    } else {  // mode S: last-zero rows updated now; E = {z <= rho - t}
+                    for (int k = 0; k < WPT; ++k) {
+                        const bool z = w[k] != VAL[k];
+                        ZW[k] = z ? rho : ZW[k];
+                        zflag |= (z ? 1u : 0u) << (b * WPT + k);
+                        AL[k] &= w[k];
                         const int zi = k * NT + tau;
                         const int lim = rho - t;
                         uint32_t e;
@@ -912,9 +914,40 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                         hist[b * Wpad + tau * WPT + k] = e;
                     }
                 }
-                if (modeL && fnib) {
-                    const int a0 = tau * WPT;
-                    atomicOr(&fm[b * fstride + (a0 >> 5)], fnib << (a0 & 31));
+            }
+        } else {  // ---- climb / mode L: per word one zero test, the last-zero row, F
+            const uint32_t tmode = modeL ? 1u : 0u;
+#pragma unroll
+            for (int b = 0; b < BMAX; ++b) {
+                if (b < nrows) {
+                    const int rho = row0 + b + 1;
+                    const uint8_t* srow = nullptr;
+                    if (TMA) {
+                        const bool wrap = st0 + b >= p.nstage;
+                        const int sb = wrap ? st0 + b - p.nstage : st0 + b;
+                        mbar_wait(&bars[sb], wrap ? par0 ^ 1u : par0);
+                        srow = ring + (size_t)sb * p.rs;
+                    }
+                    uint32_t w[WPT];
+                    fetch_words<WPT, U8, TMA>(srow, mbase + (size_t)(r0 + row0 + b) * p.ld_bytes, tau, W, p.cols,
+                                              p.rs, VAL, w, bad_or);
+                    const int lim = rho - t;
+                    uint32_t zn = 0, fn = 0;
+#pragma unroll
+                    for (int k = 0; k < WPT; ++k) {
+                        const bool z = w[k] != VAL[k];
+                        ZW[k] = z ? rho : ZW[k];
+                        zn |= z ? (1u << k) : 0u;
+                        fn |= ZW[k] <= lim ? (1u << k) : 0u;
+                        AL[k] &= w[k];
+                        if (SUB && !modeL) hist[b * Wpad + tau * WPT + k] = AL[k];
+                    }
+                    zflag |= zn << (b * WPT);
+                    fn &= fullk & (0u - tmode);
+                    if (fn) {
+                        const int a0 = tau * WPT;
+                        atomicOr(&fm[b * fstride + (a0 >> 5)], fn << (a0 & 31));
+                    }
                 }
             }
         }
@@ -925,10 +958,10 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         if (TMA && tau == issuer) {  // stages of the previous tile are free now
             const int upto = min(row0 + p.nstage, H);
             for (; issued < upto; ++issued) {
-                const int s = issued % p.nstage;
-                mbar_expect_tx(&bars[s], (uint32_t)p.row_bytes);
-                tma_row(ring + (size_t)s * p.rs, mbase + (size_t)(r0 + issued) * p.ld_bytes,
-                        (uint32_t)p.row_bytes, &bars[s], pol);
+                mbar_expect_tx(&bars[iss_s], (uint32_t)p.row_bytes);
+                tma_row(ring + (size_t)iss_s * p.rs, mbase + (size_t)(r0 + issued) * p.ld_bytes,
+                        (uint32_t)p.row_bytes, &bars[iss_s], pol);
+                if (++iss_s == p.nstage) iss_s = 0;
             }
         }
         MSQ_CK(2)
@@ -937,7 +970,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         const int lastb = nrows - 1;
         int cur_t = t;
         const Pass1Exact<U8, TMA> ex{zp, zg, za, nzm, ring, mbase, p.ld_bytes, W, p.cols, p.rs, p.nstage, P, WPT, NT, Wpad,
-                                     row0, r0};
+                                     row0, r0, st0};
         if (climb && SUB) {
             if (t == rho0) {  // E = prefix-AND of the band top; leftmost t-window
                 uint32_t best = RES_INF;
@@ -1099,6 +1132,11 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
             for (int i = tau; i < BMAX * fstride; i += NT) fm[i] = 0u;
         MSQ_CK(6)
         row0 += nrows;
+        st_base += nrows;
+        if (st_base >= p.nstage) {
+            st_base -= p.nstage;
+            par_base ^= 1u;
+        }
     }
 #undef MSQ_CK
     if (prof) {

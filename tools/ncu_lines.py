@@ -59,3 +59,25 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def by_instr(page, sass, kernel, top=30):
+    rows = list(csv.reader(open(page)))
+    h = rows[1]
+    data = [r for r in rows[2:] if r and r[0].startswith("0x")]
+    seen, uniq = set(), []
+    for r in data:
+        a = int(r[0], 16)
+        if a in seen:
+            break
+        seen.add(a)
+        uniq.append(r)
+    base = int(uniq[0][0], 16)
+    ie = h.index("Instructions Executed")
+    f = lambda x: float(x) if x not in ("", "-") else 0.0
+    lm = line_map(sass, kernel)
+    ins = collections.Counter()
+    for r in uniq:
+        ins[lm.get(int(r[0], 16) - base)] += f(r[ie])
+    tot = sum(ins.values())
+    return tot, ins.most_common(top)
