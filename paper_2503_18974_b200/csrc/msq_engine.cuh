@@ -587,6 +587,19 @@ struct Pass1Exact {
         for (int q = 0; q <= b; ++q) zin |= ~word_of_row<U8, TMA>(srow(q), grow(q), a, cols, rs);
         return z_le(a, lim) & val & ~zin;
     }
+    // suffix of word a (a >= 0) and prefix of word c (c < W) at row b, threshold T
+    __device__ __noinline__ int boundary_len(int a, int c, int b, int T) const {
+        const int lim = tile_row0 + b + 1 - T;
+        if (lim < 0) return 0;
+        uint32_t zina = 0, zinc = 0;
+        for (int q = 0; q <= b; ++q) {
+            if (a >= 0) zina |= ~word_of_row<U8, TMA>(srow(q), grow(q), a, cols, rs);
+            if (c < W) zinc |= ~word_of_row<U8, TMA>(srow(q), grow(q), c, cols, rs);
+        }
+        const uint32_t ma = a >= 0 ? z_le(a, lim) & ~zina : 0u;
+        const uint32_t mc = c < W ? z_le(c, lim) & valid_mask(c, W, cols) & ~zinc : 0u;
+        return (a >= 0 ? suffix_ones(ma) : 0) + (c < W ? prefix_ones(mc) : 0);
+    }
 };
 
 // leftmost window of T consecutive ones in row X (smem, W words) starting at
@@ -863,7 +876,8 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         const int nrows = min(climb ? (SUB ? 1 : p.bl) : (modeL ? p.bl : p.bs), H - row0);
         uint32_t* fm = fmap + (tile & 1) * BMAX * fstride;
         int polled = 0;
-        if (p.share && tau == 0 && (tile & 7) == 7) polled = ld_volatile(res_best(result));
+        const bool poll = p.share && ((tile & 7) == 7 || (!climb && !modeL));
+        if (poll && tau == 0) polled = ld_volatile(res_best(result));
 
         // ---------------------------------------------------- phase A
         uint32_t dirty = 0, zflag = 0;
@@ -951,7 +965,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 }
             }
         }
-        if (tau == 0 && (tile & 7) == 7) misc->g = polled;
+        if (tau == 0 && poll) misc->g = polled;
         MSQ_CK(0)
         csync();  // (A)
         MSQ_CK(1)
@@ -1063,9 +1077,11 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     for (int idx = tau; idx < n; idx += NT) {
                         const int b = start_b + idx / nfw, fw = idx % nfw;
                         scan_fword(fm, fstride, W, b, m, fw, cur_t, [&](int cb, int a0, int len) {
-                            const int suf = a0 > 0 ? suffix_ones(ex.mask(a0 - 1, cb, cur_t)) : 0;
-                            const int pre = a0 + len < W ? prefix_ones(ex.mask(a0 + len, cb, cur_t)) : 0;
-                            if (suf + 32 * len + pre >= cur_t) best = min(best, enc_res(cb, 32 * a0 - suf));
+                            const int bl2 = ex.boundary_len(a0 - 1, a0 + len, cb, cur_t);
+                            if (bl2 + 32 * len >= cur_t) {
+                                const int suf = a0 > 0 ? suffix_ones(ex.mask(a0 - 1, cb, cur_t)) : 0;
+                                best = min(best, enc_res(cb, 32 * a0 - suf));
+                            }
                         });
                     }
                 } else {
