@@ -108,6 +108,17 @@ class GpuBackend:
         return self.torch.cat([key, status])
 
 
+def _all_gather(out, t, group=None):
+    """all-gather of one tensor per rank into out[world, ...] (NCCL fast path;
+    list form for backends without the base collective)."""
+    import torch.distributed as dist
+    try:
+        dist.all_gather_into_tensor(out, t, group=group)
+    except (RuntimeError, NotImplementedError):
+        parts = list(out.unbind(0))
+        dist.all_gather(parts, t, group=group)
+
+
 class RowBandSolver:
     """Solve one (rows x cols) matrix sharded by rows over a process group."""
 
@@ -127,7 +138,7 @@ class RowBandSolver:
         base = None
         if self.world > 1:
             summary = be.rank_summary()
-            dist.all_gather_into_tensor(self.gathered, summary, group=self.group)
+            _all_gather(self.gathered, summary, self.group)
             if self.rank > 0:
                 base = be.compose(self.gathered, self.rank_rows, self.rank)
         be.fixup(base)

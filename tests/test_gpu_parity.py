@@ -222,3 +222,38 @@ def test_cfg5_full_size(torch):
     m = configs.cfg5_device()
     got = freq_square(m)
     _same(got, oracle.freq(m.cpu().numpy()))
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_row_band_ranks_on_one_gpu(torch, world):
+    """The rank API (msq_rank_pass1/summary/compose_carry/rank_fixup) with
+    `world` virtual ranks run one after another on one GPU (no kernel waits on
+    another), gathered on the device: same answer as the whole matrix."""
+    from paper_2503_18974_b200.distributed import GpuBackend, decode_key, slice_rows
+    rng = np.random.default_rng(world)
+    for it in range(6):
+        rows = int(rng.integers(world * 8, 900))
+        cols = int(rng.choice([64, 300, 1024, 4096]))
+        a = (rng.random((rows, cols)) < [0.99, 0.999, 1.0][it % 3]).astype(np.uint8)
+        k = min(rows, cols) // 2
+        a[rows // 2 - k // 2:rows // 2 - k // 2 + k, 3:3 + k] = 1  # crosses rank boundaries
+        for fmt in (N.FMT_U8, N.FMT_BITS):
+            full = a if fmt == N.FMT_U8 else grid.pack_bits(a).view(np.int32)
+            bes, srcs = [], []
+            rank_rows = [slice_rows(rows, world, q)[1] for q in range(world)]
+            for q in range(world):
+                r0, n = slice_rows(rows, world, q)
+                src = torch.from_numpy(np.ascontiguousarray(full[r0:r0 + n])).cuda()
+                be = GpuBackend(fmt, n, cols, r0, nbands=int(rng.integers(1, 6)))
+                be.pass1(src)
+                bes.append(be)
+                srcs.append(src)
+            gathered = torch.stack([be.rank_summary().clone() for be in bes])
+            keys = []
+            for q, be in enumerate(bes):
+                base = be.compose(gathered, rank_rows, q) if q > 0 else None
+                be.fixup(base)
+                keys.append(be.key_status())
+            ks = torch.stack(keys).max(dim=0).values.cpu().numpy()
+            got = decode_key(int(ks[0]), int(ks[1]), rows, cols)
+            _same(got, oracle.freq(a))
