@@ -334,10 +334,12 @@ def main():
                 if rank > 0:
                     base = be_.compose(band_solver.gathered, band_solver.rank_rows, rank)
             be_.fixup(base)
-            ks = be_.key_status()
             if world > 1:
+                ks = be_.key_status()
                 dist.all_reduce(ks, op=dist.ReduceOp.MAX)
-            band_solver._ks = ks
+                band_solver._ks = ks
+            else:
+                band_solver._ks = None
             return 0
         band_solver.launch(src)
         return 0

@@ -98,7 +98,7 @@ class GpuBackend:
         N.check(self.lib.msq_rank_fixup(ctypes.byref(self.plan), ctypes.c_void_p(self.ws.data_ptr()),
                                         ptr, ctypes.c_void_p(self.res.data_ptr()), self._stream()))
         nb = int(self.plan.nbands) - (0 if base is not None else 1)
-        self.launches += 1 if nb > 0 else 0
+        self.launches += 2 if nb > 0 else 0  # carry scan + fix-up
 
     def key_status(self):
         """int64 tensor [key, status] for the all-reduce (keys < 2^63)."""
@@ -142,13 +142,15 @@ class RowBandSolver:
             if self.rank > 0:
                 base = be.compose(self.gathered, self.rank_rows, self.rank)
         be.fixup(base)
-        ks = be.key_status()
         if self.world > 1:
+            ks = be.key_status()
             dist.all_reduce(ks, op=dist.ReduceOp.MAX, group=self.group)
-        self._ks = ks
+            self._ks = ks
+        else:
+            self._ks = None  # one rank: decode the device result block directly
 
     def result(self) -> SquareResult:
-        ks = self._ks.cpu().numpy().astype(np.int64)
+        ks = (self._ks if self._ks is not None else self.backend.key_status()).cpu().numpy().astype(np.int64)
         return decode_key(int(ks[0]), int(ks[1]), self.rows, self.cols)
 
     def solve(self, src) -> SquareResult:
