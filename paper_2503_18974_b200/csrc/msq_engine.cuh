@@ -682,6 +682,16 @@ __device__ __noinline__ uint32_t exact_row_mask(const Pass1Exact<U8, TMA>* ex, i
     return ex->z_le(a, lim) & ~late & val;
 }
 
+// bits inputs, small threshold: columns of word a whose last zero is <= lim
+// (outlined: the cold path of the bits format)
+__device__ __noinline__ uint32_t bits_small_e(const uint16_t* zg, int zaa, int a, uint32_t nz, uint32_t val, int lim) {
+    if (!val || lim < 0 || zaa > lim) return 0u;
+    uint32_t e = nz;
+    for (int j = 0; j < 32; ++j)
+        if (!((nz >> j) & 1u) && (int)zg[(size_t)a * 32 + j] <= lim) e |= 1u << j;
+    return e & val;
+}
+
 // mode-S row tests of one thread's words (outlined: keeps the hot loop's
 // register pressure down)
 __device__ __noinline__ uint32_t test_rows_s(const uint32_t* hist, int Wpad, int W, int WPT, int tau, int start_b,
@@ -806,12 +816,12 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 
     // side effects of the zeros of own word k at row rho: last-zero rows
     // (optional), first zeros (e_out) and the never-zeroed masks
-    auto apply_event = [&](int k, int a, int rho, uint32_t zeros, bool do_z) {
-        uint32_t newly = NZ[k] & zeros;
+    auto apply_event = [&](uint32_t& nzk, const uint32_t valk, int zi, int a, int rho, uint32_t zeros, bool do_z) {
+        uint32_t newly = nzk & zeros;
         if (do_z) {
             if (U8) {
-                zplanes_set(zp, k * NT + tau, Wpad, P, zeros, rho);
-            } else if (zeros == VAL[k]) {
+                zplanes_set(zp, zi, Wpad, P, zeros, rho);
+            } else if (zeros == valk) {
                 za[a] = (uint16_t)rho;  // whole word zero: lazy row; first zeros read as <= za
                 uint32_t nn = newly;
                 while (nn) {
@@ -837,8 +847,8 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     p.e_out[cb + j] = (uint16_t)(rho - 1);
                 }
             }
-            NZ[k] &= ~zeros;
-            if (!U8) nzm[a] = NZ[k];
+            nzk &= ~zeros;
+            if (!U8) nzm[a] = nzk;
         }
     };
 
@@ -902,7 +912,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     for (int k = 0; k < WPT; ++k) {
                         const bool z = w[k] != VAL[k];
                         ZW[k] = z ? rho : ZW[k];
-                        zflag |= (z ? 1u : 0u) << (b * WPT + k);
+                        zflag |= (z ? 1u : 0u) << (k * BMAX + b);  // word-major
                         AL[k] &= w[k];
                         const int zi = k * NT + tau;
                         const int lim = rho - t;
@@ -912,16 +922,8 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                             e = (lim >= (1 << P) ? 0xFFFFFFFFu : planes_le(zp, zi, Wpad, P, lim)) & VAL[k];
                         } else {  // bits inputs, small threshold: slow path through global z
                             const int a = tau * WPT + k;
-                            if (z) apply_event(k, a, rho, VAL[k] & ~w[k], true);
-                            e = 0;
-                            if (VAL[k] && lim >= 0) {
-                                if ((int)za[a] <= lim) {
-                                    e = NZ[k];
-                                    for (int j = 0; j < 32; ++j)
-                                        if (!((NZ[k] >> j) & 1u) && (int)zg[(size_t)a * 32 + j] <= lim) e |= 1u << j;
-                                }
-                                e &= VAL[k];
-                            }
+                            if (z) apply_event(NZ[k], VAL[k], k * NT + tau, a, rho, VAL[k] & ~w[k], true);
+                            e = bits_small_e(zg, za[a], a, NZ[k], VAL[k], lim);
                         }
                         if (e & ~EPREV[k]) dirty |= 1u << (b * WPT + k);
                         EPREV[k] = e;
@@ -946,17 +948,16 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     fetch_words<WPT, U8, TMA>(srow, mbase + (size_t)(r0 + row0 + b) * p.ld_bytes, tau, W, p.cols,
                                               p.rs, VAL, w, bad_or);
                     const int lim = rho - t;
-                    uint32_t zn = 0, fn = 0;
+                    uint32_t fn = 0;
 #pragma unroll
                     for (int k = 0; k < WPT; ++k) {
                         const bool z = w[k] != VAL[k];
                         ZW[k] = z ? rho : ZW[k];
-                        zn |= z ? (1u << k) : 0u;
+                        zflag |= z ? (1u << (k * BMAX + b)) : 0u;  // word-major
                         fn |= ZW[k] <= lim ? (1u << k) : 0u;
                         AL[k] &= w[k];
                         if (SUB && !modeL) hist[b * Wpad + tau * WPT + k] = AL[k];
                     }
-                    zflag |= zn << (b * WPT);
                     fn &= fullk & (0u - tmode);
                     if (fn) {
                         const int a0 = tau * WPT;
@@ -1130,19 +1131,22 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 
         // ---------------------------------------------------- phase C
         // last-zero rows (bit-sliced) and first zeros, in row order per word
-        uint32_t zf = zflag;
-        while (zf) {
-            const int bit = __ffs(zf) - 1;
-            zf &= zf - 1;
-            const int b = bit / WPT, k = bit - b * WPT;
-            const int r = row0 + b, rho = r + 1;
+        // words are visited with a compile-time k so VAL/NZ stay in registers
+#pragma unroll
+        for (int k = 0; k < WPT; ++k) {
+            uint32_t rb = (zflag >> (k * BMAX)) & ((1u << BMAX) - 1u);
             const int a = tau * WPT + k;
-            const uint8_t* srow =
-                TMA ? ring + (size_t)(st0 + b >= p.nstage ? st0 + b - p.nstage : st0 + b) * p.rs : nullptr;
-            const uint32_t wv =
-                word_of_row<U8, TMA>(srow, mbase + (size_t)(r0 + r) * p.ld_bytes, a, p.cols, p.rs);
-            const uint32_t zeros = VAL[k] & ~wv;
-            if (!modeS || U8) apply_event(k, a, rho, zeros, !modeS);
+            while (rb) {
+                const int b = __ffs(rb) - 1;
+                rb &= rb - 1;
+                const int r = row0 + b, rho = r + 1;
+                const uint8_t* srow =
+                    TMA ? ring + (size_t)(st0 + b >= p.nstage ? st0 + b - p.nstage : st0 + b) * p.rs : nullptr;
+                const uint32_t wv =
+                    word_of_row<U8, TMA>(srow, mbase + (size_t)(r0 + r) * p.ld_bytes, a, p.cols, p.rs);
+                const uint32_t zeros = VAL[k] & ~wv;
+                if (!modeS || U8) apply_event(NZ[k], VAL[k], k * NT + tau, a, rho, zeros, !modeS);
+            }
         }
         if (modeL)
             for (int i = tau; i < BMAX * fstride; i += NT) fm[i] = 0u;
