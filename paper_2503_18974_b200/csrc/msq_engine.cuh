@@ -880,7 +880,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 
     for (int row0 = 0; row0 < H; ++tile) {
         const int rho0 = row0 + 1;
-        const bool climb = t >= rho0;
+        const bool climb = t >= rho0 && (SUB || t < p.tl);  // large t: mode L handles rho == t rows too
         const bool modeL = !climb && t >= p.tl;
         const bool modeS = !climb && !modeL;
         const int nrows = min(climb ? (SUB ? 1 : p.bl) : (modeL ? p.bl : p.bs), H - row0);
@@ -911,7 +911,6 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 #pragma unroll
                     for (int k = 0; k < WPT; ++k) {
                         const bool z = w[k] != VAL[k];
-                        ZW[k] = z ? rho : ZW[k];
                         zflag |= (z ? 1u : 0u) << (k * BMAX + b);  // word-major
                         AL[k] &= w[k];
                         const int zi = k * NT + tau;
@@ -932,7 +931,6 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 }
             }
         } else {  // ---- climb / mode L: per word one zero test, the last-zero row, F
-            const uint32_t tmode = modeL ? 1u : 0u;
 #pragma unroll
             for (int b = 0; b < BMAX; ++b) {
                 if (b < nrows) {
@@ -947,24 +945,43 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     uint32_t w[WPT];
                     fetch_words<WPT, U8, TMA>(srow, mbase + (size_t)(r0 + row0 + b) * p.ld_bytes, tau, W, p.cols,
                                               p.rs, VAL, w, bad_or);
-                    const int lim = rho - t;
-                    uint32_t fn = 0;
 #pragma unroll
                     for (int k = 0; k < WPT; ++k) {
-                        const bool z = w[k] != VAL[k];
-                        ZW[k] = z ? rho : ZW[k];
-                        zflag |= z ? (1u << (k * BMAX + b)) : 0u;  // word-major
-                        fn |= ZW[k] <= lim ? (1u << k) : 0u;
+                        zflag |= w[k] != VAL[k] ? (1u << (k * BMAX + b)) : 0u;  // word-major
                         AL[k] &= w[k];
                         if (SUB && !modeL) hist[b * Wpad + tau * WPT + k] = AL[k];
                     }
-                    fn &= fullk & (0u - tmode);
-                    if (fn) {
-                        const int a0 = tau * WPT;
-                        atomicOr(&fm[b * fstride + (a0 >> 5)], fn << (a0 & 31));
-                    }
                 }
             }
+            if (modeL) {
+                // F words of row b: zero-free since rho_b - t, i.e. no zero in
+                // the tile up to row b and last zero before the tile <= rho0 + b - t:
+                // one row interval [lo, hi) per word
+                uint32_t fr[WPT], any = 0;
+#pragma unroll
+                for (int k = 0; k < WPT; ++k) {
+                    const uint32_t zb = (zflag >> (k * BMAX)) & ((1u << BMAX) - 1u);
+                    const int hi = zb ? __ffs(zb) - 1 : nrows;
+                    const int lo = max(0, ZW[k] + t - rho0);
+                    fr[k] = (fullk >> k) & 1u && lo < hi ? ((1u << hi) - 1u) & ~((1u << lo) - 1u) : 0u;
+                    any |= fr[k];
+                }
+                const int a0 = tau * WPT;
+                while (any) {
+                    const int b = __ffs(any) - 1;
+                    any &= any - 1;
+                    uint32_t fn = 0;
+#pragma unroll
+                    for (int k = 0; k < WPT; ++k) fn |= ((fr[k] >> b) & 1u) << k;
+                    atomicOr(&fm[b * fstride + (a0 >> 5)], fn << (a0 & 31));
+                }
+            }
+        }
+        // last zero row of each word after the tile
+#pragma unroll
+        for (int k = 0; k < WPT; ++k) {
+            const uint32_t zb = (zflag >> (k * BMAX)) & ((1u << BMAX) - 1u);
+            if (zb) ZW[k] = rho0 + 31 - __clz(zb);
         }
         if (tau == 0 && poll) misc->g = polled;
         MSQ_CK(0)
@@ -1022,6 +1039,10 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     if (lane == 0) misc->cres[b - bfirst] = st;
                 }
                 csync();  // (B)
+                if (prof) {
+                    pc[13] += (unsigned long long)(clock64() - ck);
+                    pc[15] += 1;
+                }
                 int nsucc = 0, last_start = -1;
                 for (int w2 = 0; w2 <= lastb - bfirst; ++w2) {
                     const int st = misc->cres[w2];
@@ -1106,6 +1127,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 if (start_b > lastb) break;
             }
         }
+        if (prof && climb && t - rho0 <= lastb) pc[14] += (unsigned long long)(clock64() - ck);
         if (prof) {
             const int kind = climb ? 0 : (modeL ? 2 : 1);
             pc[8 + kind] += 1;
@@ -1131,21 +1153,32 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 
         // ---------------------------------------------------- phase C
         // last-zero rows (bit-sliced) and first zeros, in row order per word
-        // words are visited with a compile-time k so VAL/NZ stay in registers
+        // one loop over all (word, row) events of the thread (word-major, so
+        // rows stay in order per word); the word's state is selected with
+        // compile-time indices so VAL/NZ stay in registers
+        if (!modeS || U8) {
+            uint32_t zf = zflag;
+            while (zf) {
+                const int bit = __ffs(zf) - 1;
+                zf &= zf - 1;
+                const int k = bit / BMAX, b = bit % BMAX;
+                uint32_t valk = VAL[0], nzk = NZ[0];
 #pragma unroll
-        for (int k = 0; k < WPT; ++k) {
-            uint32_t rb = (zflag >> (k * BMAX)) & ((1u << BMAX) - 1u);
-            const int a = tau * WPT + k;
-            while (rb) {
-                const int b = __ffs(rb) - 1;
-                rb &= rb - 1;
+                for (int kk = 1; kk < WPT; ++kk)
+                    if (k == kk) {
+                        valk = VAL[kk];
+                        nzk = NZ[kk];
+                    }
+                const int a = tau * WPT + k;
                 const int r = row0 + b, rho = r + 1;
                 const uint8_t* srow =
                     TMA ? ring + (size_t)(st0 + b >= p.nstage ? st0 + b - p.nstage : st0 + b) * p.rs : nullptr;
                 const uint32_t wv =
                     word_of_row<U8, TMA>(srow, mbase + (size_t)(r0 + r) * p.ld_bytes, a, p.cols, p.rs);
-                const uint32_t zeros = VAL[k] & ~wv;
-                if (!modeS || U8) apply_event(NZ[k], VAL[k], k * NT + tau, a, rho, zeros, !modeS);
+                apply_event(nzk, valk, k * NT + tau, a, rho, valk & ~wv, !modeS);
+#pragma unroll
+                for (int kk = 0; kk < WPT; ++kk)
+                    if (k == kk) NZ[kk] = nzk;
             }
         }
         if (modeL)
@@ -1172,11 +1205,22 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
             const int a = tau * WPT + k;
             if (a < W) {
                 const size_t cb = sum_base + (size_t)a * 32;
-                uint32_t nz = NZ[k];
-                while (nz) {
-                    const int j = __ffs(nz) - 1;
-                    nz &= nz - 1;
-                    p.e_out[cb + j] = (uint16_t)H;
+                const uint32_t nz = NZ[k];
+                if (nz) {  // never-zeroed columns: e = H (16-byte merges of the first-zero rows)
+                    uint4* eq = (uint4*)(p.e_out + cb);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t nq = (nz >> (8 * q)) & 0xFFu;
+                        if (!nq) continue;
+                        uint4 ev = nq == 0xFFu ? make_uint4(0, 0, 0, 0) : eq[q];
+                        uint32_t v[4] = {ev.x, ev.y, ev.z, ev.w};
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            if ((nq >> (2 * h)) & 1u) v[h] = (v[h] & 0xFFFF0000u) | (uint32_t)H;
+                            if ((nq >> (2 * h + 1)) & 1u) v[h] = (v[h] & 0xFFFFu) | ((uint32_t)H << 16);
+                        }
+                        eq[q] = make_uint4(v[0], v[1], v[2], v[3]);
+                    }
                 }
                 if (U8) {
                     band_bottom_runs(zp, k * NT + tau, Wpad, P, H, p.zb + (size_t)unit * p.cols_pad + (size_t)a * 32);
