@@ -59,6 +59,14 @@ __host__ __device__ __forceinline__ int band_row0(int rows, int nbands, int band
 
 __host__ __device__ __forceinline__ int r16(int x) { return (x + 15) & ~15; }
 
+struct Misc {
+    uint32_t res[3];
+    int g;
+    int cres[BMAX];  // climb: leftmost window start per tile row (-1 = none)
+    int pad[4];
+    alignas(16) unsigned char ex[128];  // Pass1Exact of the team (smem: no local-memory stack)
+};
+
 // ------------------------------------------------------------ smem layouts
 struct P1Layout {
     int ring, bars, ebars, zp, za, nzm, ab, hist, fmap, misc, total;
@@ -89,8 +97,9 @@ __host__ __device__ inline P1Layout p1_layout(int NT, int WPT, int nstage, int r
     off += bs * wpad * 4;
     L.fmap = off;
     off += 2 * BMAX * r16(nfw * 4);
+    off = r16(off);  // Misc holds 8/16-byte members
     L.misc = off;
-    off += 64;
+    off += r16((int)sizeof(Misc));
     L.total = (off + 127) & ~127;
     return L;
 }
@@ -110,8 +119,9 @@ __host__ __device__ inline FixLayout fix_layout(int NT, int WPT, int bs) {
     off += bs * wpad * 4;
     L.fmap = off;
     off += 2 * BMAX * r16(nfw * 4);
+    off = r16(off);  // Misc holds 8/16-byte members
     L.misc = off;
-    off += 64;
+    off += r16((int)sizeof(Misc));
     L.total = (off + 127) & ~127;
     return L;
 }
@@ -308,12 +318,6 @@ __device__ __forceinline__ unsigned long long* res_keyfix(unsigned char* r) {
 __device__ __forceinline__ unsigned int* res_status(unsigned char* r) { return (unsigned int*)(r + 16); }
 __device__ __forceinline__ int* res_best(unsigned char* r) { return (int*)(r + 20); }
 
-struct Misc {
-    uint32_t res[3];
-    int g;
-    int cres[BMAX];  // climb: leftmost window start per tile row (-1 = none)
-    int pad[4];
-};
 
 // bit-sliced saturating increment (reset on zero): planes h[0..P-1]
 template <int P>
@@ -587,7 +591,8 @@ struct Pass1Exact {
         for (int q = 0; q <= b; ++q) zin |= ~word_of_row<U8, TMA>(srow(q), grow(q), a, cols, rs);
         return z_le(a, lim) & val & ~zin;
     }
-    // suffix of word a (a >= 0) and prefix of word c (c < W) at row b, threshold T
+    // suffix of word a (a >= 0) and prefix of word c (c < W) at row b,
+    // threshold T, packed as suffix | prefix << 8
     __device__ __noinline__ int boundary_len(int a, int c, int b, int T) const {
         const int lim = tile_row0 + b + 1 - T;
         if (lim < 0) return 0;
@@ -598,7 +603,7 @@ struct Pass1Exact {
         }
         const uint32_t ma = a >= 0 ? z_le(a, lim) & ~zina : 0u;
         const uint32_t mc = c < W ? z_le(c, lim) & valid_mask(c, W, cols) & ~zinc : 0u;
-        return (a >= 0 ? suffix_ones(ma) : 0) + (c < W ? prefix_ones(mc) : 0);
+        return (a >= 0 ? suffix_ones(ma) : 0) | ((c < W ? prefix_ones(mc) : 0) << 8);
     }
 };
 
@@ -774,6 +779,11 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     const uint64_t pol = TMA ? l2_evict_first_policy() : 0ull;
     // TMA issuer: lane 0 of the last warp of the team (idle during most of phase B)
     const int issuer = SUB ? 0 : NT - 32;
+    static_assert(sizeof(Pass1Exact<U8, TMA>) <= sizeof(Misc::ex), "Misc::ex too small");
+    Pass1Exact<U8, TMA>* exs = reinterpret_cast<Pass1Exact<U8, TMA>*>(misc->ex);
+    if (tau == 0)
+        *exs = Pass1Exact<U8, TMA>{zp, zg, za, nzm, ring, mbase, p.ld_bytes, W, p.cols, p.rs, p.nstage, P, WPT, NT,
+                                   Wpad, 0, r0, 0};
 
     // ---- setup
     for (int i = tau; i < P * Wpad; i += NT) zp[i] = 0u;
@@ -785,6 +795,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     for (int i = tau; i < 2 * BMAX * fstride; i += NT) fmap[i] = 0u;
     if (tau == 0) {
         misc->res[0] = misc->res[1] = misc->res[2] = RES_INF;
+        misc->pad[0] = misc->pad[1] = 0;
         misc->g = p.share ? ld_volatile(res_best(result)) : 0;
         if (TMA) {
             for (int s = 0; s < p.nstage; ++s) mbar_init(&bars[s], 1);
@@ -866,10 +877,11 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     int round_ctr = 0;
     uint32_t bad_or = 0;
     int tile = 0;
-    unsigned long long pc[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) pc[i] = 0;
+    // optional per-phase cycle counters (thread 0), accumulated in global memory
+    unsigned long long* pc = p.prof ? p.prof + (size_t)unit * 16 : nullptr;
     const bool prof = p.prof != nullptr && tau == 0;
+    if (prof)
+        for (int i = 0; i < 16; ++i) pc[i] = 0;
     long long ck = prof ? clock64() : 0;
 #define MSQ_CK(i)                               \
     if (prof) {                                 \
@@ -893,6 +905,10 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         uint32_t dirty = 0, zflag = 0;
         const int st0 = st_base;
         const uint32_t par0 = par_base;
+        if (tau == 0) {  // read only after barrier A; the previous tile's readers passed a barrier
+            exs->tile_row0 = row0;
+            exs->st0 = st0;
+        }
         if (!climb && !modeL) {  // ---- mode S (small threshold): E rows for the tests
 #pragma unroll
             for (int b = 0; b < BMAX; ++b) {
@@ -1001,8 +1017,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         // ---------------------------------------------------- phase B
         const int lastb = nrows - 1;
         int cur_t = t;
-        const Pass1Exact<U8, TMA> ex{zp, zg, za, nzm, ring, mbase, p.ld_bytes, W, p.cols, p.rs, p.nstage, P, WPT, NT, Wpad,
-                                     row0, r0, st0};
+        const Pass1Exact<U8, TMA>& ex = *exs;
         if (climb && SUB) {
             if (t == rho0) {  // E = prefix-AND of the band top; leftmost t-window
                 uint32_t best = RES_INF;
@@ -1039,10 +1054,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     if (lane == 0) misc->cres[b - bfirst] = st;
                 }
                 csync();  // (B)
-                if (prof) {
-                    pc[13] += (unsigned long long)(clock64() - ck);
-                    pc[15] += 1;
-                }
+                if (prof) pc[15] += 1;
                 int nsucc = 0, last_start = -1;
                 for (int w2 = 0; w2 <= lastb - bfirst; ++w2) {
                     const int st = misc->cres[w2];
@@ -1094,14 +1106,16 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
             for (;;) {
                 uint32_t best = RES_INF;
                 const int m = cur_t - t;
+                const long long rc0 = p.prof ? clock64() : 0;
                 if (modeL) {
                     const int n = (lastb - start_b + 1) * nfw;
                     for (int idx = tau; idx < n; idx += NT) {
                         const int b = start_b + idx / nfw, fw = idx % nfw;
                         scan_fword(fm, fstride, W, b, m, fw, cur_t, [&](int cb, int a0, int len) {
+                            if (p.prof) atomicAdd(&misc->pad[0], 1);
                             const int bl2 = ex.boundary_len(a0 - 1, a0 + len, cb, cur_t);
-                            if (bl2 + 32 * len >= cur_t) {
-                                const int suf = a0 > 0 ? suffix_ones(ex.mask(a0 - 1, cb, cur_t)) : 0;
+                            const int suf = bl2 & 0xFF;
+                            if (suf + (bl2 >> 8) + 32 * len >= cur_t) {
                                 best = min(best, enc_res(cb, 32 * a0 - suf));
                             }
                         });
@@ -1112,7 +1126,13 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 const int slot = round_ctr % 3;
                 if (best != RES_INF) atomicMin(&misc->res[slot], best);
                 if (tau == 0) misc->res[(round_ctr + 1) % 3] = RES_INF;
+                if (p.prof && modeL) atomicMax(&misc->pad[1], (int)(clock64() - rc0));
+                if (prof && modeL) pc[7] += 1;
                 csync();  // (B)
+                if (prof && modeL) {
+                    pc[13] += misc->pad[1];
+                    misc->pad[1] = 0;
+                }
                 const uint32_t rr = misc->res[slot];
                 ++round_ctr;
                 if (rr == RES_INF) break;
@@ -1194,7 +1214,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 #undef MSQ_CK
     if (prof) {
         pc[12] = t;
-        for (int i = 0; i < 16; ++i) p.prof[(size_t)unit * 16 + i] = pc[i];
+        pc[14] = misc->pad[0];
     }
     csync();
 
