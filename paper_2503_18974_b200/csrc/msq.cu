@@ -74,7 +74,8 @@ int zplanes_for(const msq_plan* pl) {
     return P;
 }
 
-bool uses_producer_warp(const msq_plan*) { return false; }
+// CTA-team plans reserve smem for the optional phase-cycle counters
+bool cta_plan(const msq_plan* pl) { return pl->teams_per_cta == 1 && pl->team == pl->threads; }
 
 
 template <class K>
@@ -121,7 +122,7 @@ cudaError_t launch_fixup_t(const msq_plan* pl, const msq::FixParams& prm, int nb
 cudaError_t launch_pass1(const msq_plan* pl, const msq::Pass1Params& prm, cudaStream_t st) {
     const bool u8 = pl->fmt == MSQ_FMT_U8;
     const bool tma = pl->nstage > 0;
-    const bool sub = pl->teams_per_cta > 1 || (pl->team < pl->threads && !uses_producer_warp(pl));
+    const bool sub = !cta_plan(pl);
 #define MSQ_P1(W_, U_, T_, S_) \
     if (pl->wpt == W_ && u8 == U_ && tma == T_ && sub == S_) return launch_pass1_t<W_, U_, T_, S_>(pl, prm, st);
     MSQ_P1(1, true, true, true) MSQ_P1(1, true, false, true) MSQ_P1(1, false, true, true)
@@ -148,7 +149,7 @@ cudaError_t launch_fixup(const msq_plan* pl, const msq::FixParams& prm, int nblo
 
 int team_layout_bytes(const msq_plan* pl) {
     return msq::p1_layout(pl->team, pl->wpt, pl->nstage, pl->row_stage_bytes, pl->tile_rows, zplanes_for(pl),
-                          pl->nstage > 0, uses_producer_warp(pl))
+                          pl->nstage > 0, cta_plan(pl))
         .total;
 }
 
@@ -337,7 +338,7 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
         p.nstage = tma_ok ? 2 * 4 : 0;  // ring holds the previous and the current tile
         for (;;) {
             const long long per = msq::p1_layout(ts, 1, p.nstage, (int)row_bytes, p.tile_rows, zplanes_for(&p),
-                                                 p.nstage > 0, false)
+                                                 p.nstage > 0, tpc == 1 && ts >= 32)  // == cta_plan()
                                       .total;
             if (per * tpc <= kSmemMax) break;
             if (p.nstage > 0) {
@@ -381,10 +382,17 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
     const int P = zplanes_for(&p);
     if (tma_ok) {
         // refills happen after the next tile's first barrier, so the ring must
-        // hold the previous tile plus the current one (more = deeper prefetch)
-        const int base = msq::p1_layout(p.threads, p.wpt, 0, (int)row_bytes, p.tile_rows, P, true, false).total;
-        long long ns = (kSmemMax - base - 512) / row_bytes;
-        ns = std::min<long long>(ns, 32);
+        // hold the previous tile plus the current one (more = deeper prefetch);
+        // a single-row small-threshold tile frees one row of E history for it
+        auto stages = [&](int bs) {
+            const int base = msq::p1_layout(p.threads, p.wpt, 0, (int)row_bytes, bs, P, true, true).total;
+            return std::min<long long>((kSmemMax - base - 512) / row_bytes, 32);
+        };
+        long long ns = stages(p.tile_rows);
+        if (ns < 2 * p.tile_rows_l && stages(1) >= 2 * p.tile_rows_l) {
+            p.tile_rows = 1;
+            ns = stages(1);
+        }
         while (p.tile_rows_l > p.tile_rows && ns < 2 * p.tile_rows_l) p.tile_rows_l /= 2;
         if (ns >= 2 * p.tile_rows_l) p.nstage = (int32_t)ns;
     }

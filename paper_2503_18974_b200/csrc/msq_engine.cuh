@@ -69,13 +69,13 @@ struct Misc {
 
 // ------------------------------------------------------------ smem layouts
 struct P1Layout {
-    int ring, bars, ebars, zp, za, nzm, ab, hist, fmap, misc, total;
+    int ring, bars, pcs, zp, za, nzm, ab, hist, fmap, misc, total;
 };
 // per team; zp holds P bit-planes of the last-zero rows, hist bs rows of E
-// words, fmap 2 x BMAX rows of F bits; ebars = empty barriers of the
-// producer-warp ring (CTA teams)
+// words, fmap 2 x BMAX rows of F bits; pcs = optional phase-cycle counters
+// (CTA teams only)
 __host__ __device__ inline P1Layout p1_layout(int NT, int WPT, int nstage, int rs, int bs, int P, bool tma,
-                                              bool ebar) {
+                                              bool pcs) {
     P1Layout L;
     const int wpad = NT * WPT, nfw = (wpad + 31) / 32;
     int off = 0;
@@ -83,8 +83,8 @@ __host__ __device__ inline P1Layout p1_layout(int NT, int WPT, int nstage, int r
     if (tma) off += nstage * rs;
     L.bars = off;
     if (tma) off += r16(nstage * 8);
-    L.ebars = off;
-    if (ebar) off += r16(nstage * 8);
+    L.pcs = off;
+    if (pcs) off += 16 * 8;
     L.zp = off;
     off += P * wpad * 4;
     L.za = off;  // global-z mode: last all-zero row per word
@@ -687,6 +687,38 @@ __device__ __noinline__ uint32_t exact_row_mask(const Pass1Exact<U8, TMA>* ex, i
     return ex->z_le(a, lim) & ~late & val;
 }
 
+// Mode-L candidate check by a whole warp (bits inputs): candidate = F run
+// [a0, a0+len) of tile row cb (packed cb | a0 << 3 | len << 14).  Lanes 0-7 /
+// 8-15 read the tile-row words of the left / right boundary word, lane j tests
+// column j of both boundary words against the last-zero rows (one coalesced
+// 64-byte read per word), ballots give the exact masks.  Returns the encoded
+// leftmost window start or RES_INF.
+template <bool U8, bool TMA>
+__device__ __noinline__ uint32_t coop_check(const Pass1Exact<U8, TMA>* ex, uint32_t cand, int T, int lane) {
+    const int cb = (int)(cand & 7u), a0 = (int)((cand >> 3) & 0x7FFu), len = (int)(cand >> 14);
+    const int W = ex->W;
+    const int a = a0 - 1, c = a0 + len;
+    const int lim = ex->tile_row0 + cb + 1 - T;
+    if (lim < 0) return RES_INF;
+    const int q = lane & 7;
+    const int wsel = lane < 8 ? a : c;
+    uint32_t zin = 0u;
+    if (lane < 16 && q <= cb && wsel >= 0 && wsel < W)
+        zin = ~word_of_row<U8, TMA>(ex->srow(q), ex->grow(q), wsel, ex->cols, ex->rs);
+    const uint32_t zina = __reduce_or_sync(0xFFFFFFFFu, lane < 8 ? zin : 0u);
+    const uint32_t zinc = __reduce_or_sync(0xFFFFFFFFu, lane < 8 ? 0u : zin);
+    bool ea = false, ec = false;
+    if (a >= 0 && (int)ex->za[a] <= lim)
+        ea = ((ex->nzm[a] >> lane) & 1u) || (int)ex->zg[(size_t)a * 32 + lane] <= lim;
+    if (c < W && (int)ex->za[c] <= lim)
+        ec = ((ex->nzm[c] >> lane) & 1u) || (int)ex->zg[(size_t)c * 32 + lane] <= lim;
+    const uint32_t ma = __ballot_sync(0xFFFFFFFFu, ea);
+    const uint32_t mc = __ballot_sync(0xFFFFFFFFu, ec);
+    const int suf = a >= 0 ? suffix_ones(ma & ~zina) : 0;
+    const int pre = c < W ? prefix_ones(mc & ~zinc & valid_mask(c, W, ex->cols)) : 0;
+    return suf + pre + 32 * len >= T ? enc_res(cb, 32 * a0 - suf) : RES_INF;
+}
+
 // bits inputs, small threshold: columns of word a whose last zero is <= lim
 // (outlined: the cold path of the bits format)
 __device__ __noinline__ uint32_t bits_small_e(const uint16_t* zg, int zaa, int a, uint32_t nz, uint32_t val, int lim) {
@@ -762,7 +794,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     const int P = U8 ? p.zplanes : 0;  // bit planes only for u8 inputs
     unsigned char* result = p.results + (size_t)mat * 32;
 
-    const P1Layout Lo = p1_layout(NT, WPT, p.nstage, p.rs, p.bs, P, TMA, false);
+    const P1Layout Lo = p1_layout(NT, WPT, p.nstage, p.rs, p.bs, P, TMA, !SUB);
     uint8_t* tsm = smem + (size_t)team_idx * p.layout_bytes;
     uint8_t* ring = tsm + Lo.ring;
     uint64_t* bars = (uint64_t*)(tsm + Lo.bars);
@@ -795,7 +827,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     for (int i = tau; i < 2 * BMAX * fstride; i += NT) fmap[i] = 0u;
     if (tau == 0) {
         misc->res[0] = misc->res[1] = misc->res[2] = RES_INF;
-        misc->pad[0] = misc->pad[1] = 0;
+        misc->pad[0] = misc->pad[1] = misc->pad[2] = 0;
         misc->g = p.share ? ld_volatile(res_best(result)) : 0;
         if (TMA) {
             for (int s = 0; s < p.nstage; ++s) mbar_init(&bars[s], 1);
@@ -877,8 +909,9 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     int round_ctr = 0;
     uint32_t bad_or = 0;
     int tile = 0;
-    // optional per-phase cycle counters (thread 0), accumulated in global memory
-    unsigned long long* pc = p.prof ? p.prof + (size_t)unit * 16 : nullptr;
+    // optional per-phase cycle counters (thread 0): smem for CTA teams, global for sub-warp teams
+    unsigned long long* pc = SUB ? (p.prof ? p.prof + (size_t)unit * 16 : nullptr)
+                                 : (unsigned long long*)(tsm + Lo.pcs);
     const bool prof = p.prof != nullptr && tau == 0;
     if (prof)
         for (int i = 0; i < 16; ++i) pc[i] = 0;
@@ -947,25 +980,45 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 }
             }
         } else {  // ---- climb / mode L: per word one zero test, the last-zero row, F
+            // rows in groups of RG: all barrier waits first, then all loads,
+            // then the tests (one latency chain per group instead of per row)
+            constexpr int RG = 4;
 #pragma unroll
-            for (int b = 0; b < BMAX; ++b) {
-                if (b < nrows) {
-                    const int rho = row0 + b + 1;
-                    const uint8_t* srow = nullptr;
-                    if (TMA) {
-                        const bool wrap = st0 + b >= p.nstage;
-                        const int sb = wrap ? st0 + b - p.nstage : st0 + b;
-                        mbar_wait(&bars[sb], wrap ? par0 ^ 1u : par0);
-                        srow = ring + (size_t)sb * p.rs;
+            for (int h = 0; h < BMAX; h += RG) {
+                if (h < nrows) {
+                    const uint8_t* srow[RG];
+#pragma unroll
+                    for (int g = 0; g < RG; ++g) {
+                        const int b = h + g;
+                        srow[g] = nullptr;
+                        if (TMA && b < nrows) {
+                            const bool wrap = st0 + b >= p.nstage;
+                            const int sb = wrap ? st0 + b - p.nstage : st0 + b;
+                            mbar_wait(&bars[sb], wrap ? par0 ^ 1u : par0);
+                            srow[g] = ring + (size_t)sb * p.rs;
+                        }
                     }
-                    uint32_t w[WPT];
-                    fetch_words<WPT, U8, TMA>(srow, mbase + (size_t)(r0 + row0 + b) * p.ld_bytes, tau, W, p.cols,
-                                              p.rs, VAL, w, bad_or);
+                    uint32_t w[RG][WPT];
 #pragma unroll
-                    for (int k = 0; k < WPT; ++k) {
-                        zflag |= w[k] != VAL[k] ? (1u << (k * BMAX + b)) : 0u;  // word-major
-                        AL[k] &= w[k];
-                        if (SUB && !modeL) hist[b * Wpad + tau * WPT + k] = AL[k];
+                    for (int g = 0; g < RG; ++g) {
+                        const int b = h + g;
+                        if (b < nrows) {
+                            fetch_words<WPT, U8, TMA>(srow[g], mbase + (size_t)(r0 + row0 + b) * p.ld_bytes, tau, W,
+                                                      p.cols, p.rs, VAL, w[g], bad_or);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < WPT; ++k) w[g][k] = VAL[k];
+                        }
+                    }
+#pragma unroll
+                    for (int g = 0; g < RG; ++g) {
+                        const int b = h + g;
+#pragma unroll
+                        for (int k = 0; k < WPT; ++k) {
+                            zflag |= w[g][k] != VAL[k] ? (1u << (k * BMAX + b)) : 0u;  // word-major
+                            AL[k] &= w[g][k];
+                            if (SUB && !modeL && b < nrows) hist[b * Wpad + tau * WPT + k] = AL[k];
+                        }
                     }
                 }
             }
@@ -1054,7 +1107,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     if (lane == 0) misc->cres[b - bfirst] = st;
                 }
                 csync();  // (B)
-                if (prof) pc[15] += 1;
+
                 int nsucc = 0, last_start = -1;
                 for (int w2 = 0; w2 <= lastb - bfirst; ++w2) {
                     const int st = misc->cres[w2];
@@ -1108,17 +1161,59 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 const int m = cur_t - t;
                 const long long rc0 = p.prof ? clock64() : 0;
                 if (modeL) {
+                    // CTA teams with bits inputs (last-zero rows in L2) queue up to
+                    // two candidates per lane for the warp-cooperative check (one
+                    // L2 round trip per candidate instead of a serial chain per
+                    // lane) when the warp has few; otherwise, and for every u8
+                    // candidate (smem planes), the lane checks its own
+                    constexpr uint32_t NONE = 0xFFFFFFFFu;
+                    constexpr bool COOP = !SUB && !U8;
+                    uint32_t cq0 = NONE, cq1 = NONE;
+                    auto direct = [&](int cb, int a0, int len) {
+                        const int bl2 = ex.boundary_len(a0 - 1, a0 + len, cb, cur_t);
+                        const int suf = bl2 & 0xFF;
+                        if (suf + (bl2 >> 8) + 32 * len >= cur_t) best = min(best, enc_res(cb, 32 * a0 - suf));
+                    };
                     const int n = (lastb - start_b + 1) * nfw;
                     for (int idx = tau; idx < n; idx += NT) {
                         const int b = start_b + idx / nfw, fw = idx % nfw;
                         scan_fword(fm, fstride, W, b, m, fw, cur_t, [&](int cb, int a0, int len) {
                             if (p.prof) atomicAdd(&misc->pad[0], 1);
-                            const int bl2 = ex.boundary_len(a0 - 1, a0 + len, cb, cur_t);
-                            const int suf = bl2 & 0xFF;
-                            if (suf + (bl2 >> 8) + 32 * len >= cur_t) {
-                                best = min(best, enc_res(cb, 32 * a0 - suf));
+                            const uint32_t cand = (uint32_t)cb | ((uint32_t)a0 << 3) | ((uint32_t)len << 14);
+                            if (COOP && cq0 == NONE) {
+                                cq0 = cand;
+                            } else if (COOP && cq1 == NONE) {
+                                cq1 = cand;
+                            } else {
+                                direct(cb, a0, len);
                             }
                         });
+                    }
+                    if (p.prof) atomicMax(&misc->pad[2], (int)(clock64() - rc0));
+                    if (COOP) {
+                        const uint32_t bal0 = __ballot_sync(0xFFFFFFFFu, cq0 != NONE);
+                        const uint32_t bal1 = __ballot_sync(0xFFFFFFFFu, cq1 != NONE);
+                        if (__popc(bal0) + __popc(bal1) <= 4) {
+#pragma unroll
+                            for (int qi = 0; qi < 2; ++qi) {
+                                const uint32_t mine = qi ? cq1 : cq0;
+                                uint32_t bal = qi ? bal1 : bal0;
+                                while (bal) {
+                                    const int l = __ffs(bal) - 1;
+                                    bal &= bal - 1;
+                                    const uint32_t cand = __shfl_sync(0xFFFFFFFFu, mine, l);
+                                    const uint32_t r = coop_check<U8, TMA>(exs, cand, cur_t, lane);
+                                    if (lane == l) best = min(best, r);
+                                }
+                            }
+                        } else {  // many candidates in this warp: lanes in parallel
+#pragma unroll
+                            for (int qi = 0; qi < 2; ++qi) {
+                                const uint32_t cand = qi ? cq1 : cq0;
+                                if (cand != NONE)
+                                    direct((int)(cand & 7u), (int)((cand >> 3) & 0x7FFu), (int)(cand >> 14));
+                            }
+                        }
                     }
                 } else {
                     best = test_rows_s(hist, Wpad, W, WPT, tau, start_b, lastb, full_from, dirty, m, cur_t);
@@ -1131,7 +1226,8 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 csync();  // (B)
                 if (prof && modeL) {
                     pc[13] += misc->pad[1];
-                    misc->pad[1] = 0;
+                    pc[15] += misc->pad[2];
+                    misc->pad[1] = misc->pad[2] = 0;
                 }
                 const uint32_t rr = misc->res[slot];
                 ++round_ctr;
@@ -1215,6 +1311,8 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     if (prof) {
         pc[12] = t;
         pc[14] = misc->pad[0];
+        if (!SUB)
+            for (int i = 0; i < 16; ++i) p.prof[(size_t)unit * 16 + i] = pc[i];
     }
     csync();
 

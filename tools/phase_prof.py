@@ -27,7 +27,7 @@ N.load().msq_debug_set_profile(None)
 torch.cuda.synchronize()
 pc = buf.cpu().numpy().reshape(units, 16).astype(np.float64)
 names = ["A(work+waits)", "barrierA", "tma issue", "B climb", "B modeS", "B modeL", "C", "L rounds",
-         "tiles climb", "tiles S", "tiles L", "raises", "final t", "L max work", "L candidates", "climb tested"]
+         "tiles climb", "tiles S", "tiles L", "raises", "final t", "L max work", "L candidates", "L max scan"]
 tot = pc[:, :7].sum(axis=1)
 print(cfg, r[0], "bands", units)
 print("total cycles per band: mean %.0f max %.0f" % (tot.mean(), tot.max()))
