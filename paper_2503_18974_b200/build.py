@@ -43,6 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-shared", "-Xcompiler", "-fPIC", "-cudart", "shared",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC,
            "-Xlinker", "-rpath,/usr/local/cuda/lib64",
+           *os.environ.get("MSQ_NVCC_EXTRA", "").split(),  # experiments only
            "-o", LIB + ".tmp", *SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

@@ -39,6 +39,9 @@ constexpr int KEY_DIM_BITS = 21;
 constexpr unsigned long long KEY_DIM_MASK = (1ull << KEY_DIM_BITS) - 1ull;
 constexpr uint32_t RES_INF = 0xFFFFFFFFu;
 constexpr int NPLANES = 7;   // mode S counters saturate at 127
+#ifndef MSQ_ABLATE
+#define MSQ_ABLATE 0  // experiments: bit 0 = no zero events, bit 1 = no mode-L candidates, bit 2 = no F build, bit 3 = no climb tests
+#endif
 constexpr int BMAX = 8;      // max rows per tile
 constexpr int FIX_XPL = 6;   // fix-up mode X planes (c, e clamped at 63)
 constexpr int FIX_TL = 63;   // fix-up mode L threshold (runs then contain a full word)
@@ -63,7 +66,7 @@ struct Misc {
     uint32_t res[3];
     int g;
     int cres[BMAX];  // climb: leftmost window start per tile row (-1 = none)
-    int pad[4];
+    int pad[8];
     alignas(16) unsigned char ex[128];  // Pass1Exact of the team (smem: no local-memory stack)
 };
 
@@ -166,6 +169,40 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) {
+    }
+}
+__device__ __forceinline__ uint32_t mbar_test_s(uint32_t bar_s, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar_s), "r"(parity)
+        : "memory");
+    return ok;
+}
+// shared-window (32-bit) address forms for the hot row loop
+__device__ int g_spin_dbg;  // debug: failed barrier polls (profiling builds only)
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar_s, uint32_t parity, int* spins = nullptr) {
+    uint32_t ok;
+    do {
+        if (spins) ++*spins;
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(bar_s), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+template <int N>
+__device__ __forceinline__ void lds_words(uint32_t addr, uint32_t (&w)[N]) {
+    if (N == 4) {
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(w[0]), "=r"(w[(1) % N]), "=r"(w[(2) % N]), "=r"(w[(3) % N])
+                     : "r"(addr));
+    } else if (N == 2) {
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w[0]), "=r"(w[(1) % N]) : "r"(addr));
+    } else {
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w[0]) : "r"(addr));
     }
 }
 __device__ __forceinline__ int ld_volatile(const int* p) { return *(const volatile int*)p; }
@@ -763,6 +800,129 @@ __device__ __noinline__ void band_bottom_runs(const uint32_t* zp, int zbase, int
     }
 }
 
+// Rows b < nrows of a tile (stages st0.. of the ring, phase parity par0):
+// barrier waits for RG rows first, then their loads, then the zero tests
+// (one latency chain per group).  Returns the word-major zero flags (bit
+// k*BMAX + b: row b has a zero in word k); optionally folds the rows into the
+// prefix-AND AL and records it per row in hist (sub-warp climb tiles).
+template <int WPT, bool U8, bool TMA>
+__device__ __forceinline__ uint32_t tile_zero_flags(const Pass1Params& p, uint64_t* bars, const uint8_t* ring,
+                                                    const uint8_t* rows_base, int st0, uint32_t par0, int nrows,
+                                                    int tau, int W, const uint32_t (&VAL)[WPT], uint32_t (&AL)[WPT],
+                                                    bool do_al, uint32_t* hist, int Wpad, uint32_t& bad_or) {
+    constexpr int RG = 4;
+    uint32_t zflag = 0;
+#pragma unroll
+    for (int h = 0; h < BMAX; h += RG) {
+        if (h < nrows) {
+            const uint8_t* srow[RG];
+#pragma unroll
+            for (int g = 0; g < RG; ++g) {
+                const int b = h + g;
+                srow[g] = nullptr;
+                if (TMA && b < nrows) {
+                    const bool wrap = st0 + b >= p.nstage;
+                    const int sb = wrap ? st0 + b - p.nstage : st0 + b;
+                    mbar_wait(&bars[sb], wrap ? par0 ^ 1u : par0);
+                    srow[g] = ring + (size_t)sb * p.rs;
+                }
+            }
+            uint32_t w[RG][WPT];
+#pragma unroll
+            for (int g = 0; g < RG; ++g) {
+                const int b = h + g;
+                if (b < nrows) {
+                    fetch_words<WPT, U8, TMA>(srow[g], rows_base + (size_t)b * p.ld_bytes, tau, W, p.cols, p.rs, VAL,
+                                              w[g], bad_or);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < WPT; ++k) w[g][k] = VAL[k];
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < RG; ++g) {
+                const int b = h + g;
+#pragma unroll
+                for (int k = 0; k < WPT; ++k) {
+                    zflag |= w[g][k] != VAL[k] ? (1u << (k * BMAX + b)) : 0u;  // word-major
+                    if (do_al) {
+                        AL[k] &= w[g][k];
+                        if (hist && b < nrows) hist[b * Wpad + tau * WPT + k] = AL[k];
+                    }
+                }
+            }
+        }
+    }
+    return zflag;
+}
+
+// Lean form of tile_zero_flags for bit-packed TMA-staged rows (CTA teams):
+// per row one vector smem load and one "any zero in my words" flag; the
+// per-word flags are rebuilt only for the (few) rows that had a zero.
+// ring_s = shared address of the thread's words in ring stage 0, bars_s =
+// shared address of barrier 0, inv = ~valid mask per word.
+template <int WPT>
+__device__ __forceinline__ uint32_t tile_zero_flags_bits(uint32_t ring_s, uint32_t bars_s, int rs, int nstage, int st0,
+                                                         uint32_t par0, int nrows, bool active,
+                                                         const uint32_t (&inv)[WPT], uint32_t (&AL)[WPT],
+                                                         bool do_al, int* spins) {
+    constexpr int RG = 4;
+    uint32_t rowflag = 0;
+#pragma unroll
+    for (int h = 0; h < BMAX; h += RG) {
+        if (h < nrows) {
+            uint32_t addr[RG], bar[RG], par[RG];
+            uint32_t ready = 1u;
+#pragma unroll
+            for (int g = 0; g < RG; ++g) {  // non-blocking tests of the group's barriers, back to back
+                const int b = h + g;
+                const bool wrap = st0 + b >= nstage;
+                const int sb = wrap ? st0 + b - nstage : st0 + b;
+                addr[g] = ring_s + (uint32_t)(sb * rs);
+                bar[g] = bars_s + 8u * (uint32_t)sb;
+                par[g] = wrap ? par0 ^ 1u : par0;
+                if (b < nrows) ready &= mbar_test_s(bar[g], par[g]);
+            }
+            if (!ready) {
+#pragma unroll
+                for (int g = 0; g < RG; ++g)
+                    if (h + g < nrows) mbar_wait_s(bar[g], par[g], spins);
+            }
+            uint32_t w[RG][WPT];
+#pragma unroll
+            for (int g = 0; g < RG; ++g) {
+                if (h + g < nrows && active) {
+                    lds_words<WPT>(addr[g], w[g]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < WPT; ++k) w[g][k] = 0xFFFFFFFFu;
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < RG; ++g) {
+                uint32_t all = 0xFFFFFFFFu;
+#pragma unroll
+                for (int k = 0; k < WPT; ++k) {
+                    all &= w[g][k] | inv[k];
+                    if (do_al) AL[k] &= w[g][k];
+                }
+                rowflag |= all != 0xFFFFFFFFu ? (1u << (h + g)) : 0u;
+            }
+        }
+    }
+    uint32_t zflag = 0;
+    while (rowflag) {  // rows with a zero somewhere in the thread's words
+        const int b = __ffs(rowflag) - 1;
+        rowflag &= rowflag - 1;
+        const int sb = st0 + b >= nstage ? st0 + b - nstage : st0 + b;
+        uint32_t w[WPT];
+        lds_words<WPT>(ring_s + (uint32_t)(sb * rs), w);
+#pragma unroll
+        for (int k = 0; k < WPT; ++k) zflag |= (w[k] | inv[k]) != 0xFFFFFFFFu ? (1u << (k * BMAX + b)) : 0u;
+    }
+    return zflag;
+}
+
 // ============================================================= pass 1 kernel
 // Tile kinds: CLIMB (t >= rho: heights <= rho, so E = prefix-AND of the band
 // top when t == rho; 1 row per tile, one warp finds the leftmost window),
@@ -827,7 +987,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     for (int i = tau; i < 2 * BMAX * fstride; i += NT) fmap[i] = 0u;
     if (tau == 0) {
         misc->res[0] = misc->res[1] = misc->res[2] = RES_INF;
-        misc->pad[0] = misc->pad[1] = misc->pad[2] = 0;
+        for (int i = 0; i < 8; ++i) misc->pad[i] = 0;
         misc->g = p.share ? ld_volatile(res_best(result)) : 0;
         if (TMA) {
             for (int s = 0; s < p.nstage; ++s) mbar_init(&bars[s], 1);
@@ -895,6 +1055,11 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         }
     };
 
+    uint32_t INV[WPT];  // ~valid mask per word (lean bits row loop)
+#pragma unroll
+    for (int k = 0; k < WPT; ++k) INV[k] = ~VAL[k];
+    const uint32_t ring_s = smem_addr(ring) + (uint32_t)(tau * WPT * 4);
+    const uint32_t bars_s = smem_addr(bars);
     uint32_t fullk = 0;  // words whose 32 columns are all valid (only those can be F)
 #pragma unroll
     for (int k = 0; k < WPT; ++k) fullk |= (VAL[k] == 0xFFFFFFFFu ? 1u : 0u) << k;
@@ -909,6 +1074,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     int round_ctr = 0;
     uint32_t bad_or = 0;
     int tile = 0;
+    long long tB = p.prof ? clock64() : 0;  // profiling: end of phase B of this warp
     // optional per-phase cycle counters (thread 0): smem for CTA teams, global for sub-warp teams
     unsigned long long* pc = SUB ? (p.prof ? p.prof + (size_t)unit * 16 : nullptr)
                                  : (unsigned long long*)(tsm + Lo.pcs);
@@ -980,49 +1146,20 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 }
             }
         } else {  // ---- climb / mode L: per word one zero test, the last-zero row, F
-            // rows in groups of RG: all barrier waits first, then all loads,
-            // then the tests (one latency chain per group instead of per row)
-            constexpr int RG = 4;
-#pragma unroll
-            for (int h = 0; h < BMAX; h += RG) {
-                if (h < nrows) {
-                    const uint8_t* srow[RG];
-#pragma unroll
-                    for (int g = 0; g < RG; ++g) {
-                        const int b = h + g;
-                        srow[g] = nullptr;
-                        if (TMA && b < nrows) {
-                            const bool wrap = st0 + b >= p.nstage;
-                            const int sb = wrap ? st0 + b - p.nstage : st0 + b;
-                            mbar_wait(&bars[sb], wrap ? par0 ^ 1u : par0);
-                            srow[g] = ring + (size_t)sb * p.rs;
-                        }
-                    }
-                    uint32_t w[RG][WPT];
-#pragma unroll
-                    for (int g = 0; g < RG; ++g) {
-                        const int b = h + g;
-                        if (b < nrows) {
-                            fetch_words<WPT, U8, TMA>(srow[g], mbase + (size_t)(r0 + row0 + b) * p.ld_bytes, tau, W,
-                                                      p.cols, p.rs, VAL, w[g], bad_or);
-                        } else {
-#pragma unroll
-                            for (int k = 0; k < WPT; ++k) w[g][k] = VAL[k];
-                        }
-                    }
-#pragma unroll
-                    for (int g = 0; g < RG; ++g) {
-                        const int b = h + g;
-#pragma unroll
-                        for (int k = 0; k < WPT; ++k) {
-                            zflag |= w[g][k] != VAL[k] ? (1u << (k * BMAX + b)) : 0u;  // word-major
-                            AL[k] &= w[g][k];
-                            if (SUB && !modeL && b < nrows) hist[b * Wpad + tau * WPT + k] = AL[k];
-                        }
-                    }
+            if (!U8 && TMA && !SUB) {
+                const long long ta0 = p.prof ? clock64() : 0;
+                zflag = tile_zero_flags_bits<WPT>(ring_s, bars_s, p.rs, p.nstage, st0, par0, nrows, tau * WPT < W, INV,
+                                                  AL, !modeL, nullptr);
+                if (p.prof && lane == 0) {
+                    atomicMax(&misc->pad[5], (int)(clock64() - ta0));
+                    atomicMax(&misc->pad[6], (int)(ta0 - tB));
                 }
+            } else {
+                zflag = tile_zero_flags<WPT, U8, TMA>(p, bars, ring, mbase + (size_t)(r0 + row0) * p.ld_bytes, st0,
+                                                      par0, nrows, tau, W, VAL, AL, true,
+                                                      SUB && !modeL ? hist : nullptr, Wpad, bad_or);
             }
-            if (modeL) {
+            if (modeL && !(MSQ_ABLATE & 4)) {
                 // F words of row b: zero-free since rho_b - t, i.e. no zero in
                 // the tile up to row b and last zero before the tile <= rho0 + b - t:
                 // one row interval [lo, hi) per word
@@ -1036,13 +1173,31 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     any |= fr[k];
                 }
                 const int a0 = tau * WPT;
-                while (any) {
-                    const int b = __ffs(any) - 1;
-                    any &= any - 1;
-                    uint32_t fn = 0;
+                if (!SUB) {
+                    // the 32/WPT lanes that own one F word OR their bits together
+                    // and one of them stores it (no atomics, no clearing)
+                    constexpr int LPF = 32 / WPT;
 #pragma unroll
-                    for (int k = 0; k < WPT; ++k) fn |= ((fr[k] >> b) & 1u) << k;
-                    atomicOr(&fm[b * fstride + (a0 >> 5)], fn << (a0 & 31));
+                    for (int b = 0; b < BMAX; ++b) {
+                        if (b < nrows) {
+                            uint32_t v = 0;
+#pragma unroll
+                            for (int k = 0; k < WPT; ++k) v |= ((fr[k] >> b) & 1u) << k;
+                            v <<= (a0 & 31);
+#pragma unroll
+                            for (int o = 1; o < LPF; o <<= 1) v |= __shfl_xor_sync(0xFFFFFFFFu, v, o);
+                            if ((lane & (LPF - 1)) == 0) fm[b * fstride + (a0 >> 5)] = v;
+                        }
+                    }
+                } else {
+                    while (any) {
+                        const int b = __ffs(any) - 1;
+                        any &= any - 1;
+                        uint32_t fn = 0;
+#pragma unroll
+                        for (int k = 0; k < WPT; ++k) fn |= ((fr[k] >> b) & 1u) << k;
+                        atomicOr(&fm[b * fstride + (a0 >> 5)], fn << (a0 & 31));
+                    }
                 }
             }
         }
@@ -1053,9 +1208,18 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
             if (zb) ZW[k] = rho0 + 31 - __clz(zb);
         }
         if (tau == 0 && poll) misc->g = polled;
+        if (p.prof && lane == 0) atomicMax(&misc->pad[4], (int)(clock64() - tB));
         MSQ_CK(0)
         csync();  // (A)
         MSQ_CK(1)
+        if (prof) {
+            pc[4] += misc->pad[3];
+            pc[9] += misc->pad[4];
+            pc[12] += misc->pad[5];
+            pc[14] += misc->pad[6];
+            misc->pad[3] = misc->pad[4] = misc->pad[5] = misc->pad[6] = 0;
+        }
+        const long long ti0 = p.prof ? clock64() : 0;
         if (TMA && tau == issuer) {  // stages of the previous tile are free now
             const int upto = min(row0 + p.nstage, H);
             for (; issued < upto; ++issued) {
@@ -1065,6 +1229,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 if (++iss_s == p.nstage) iss_s = 0;
             }
         }
+        if (p.prof && tau == issuer) atomicAdd(&misc->pad[7], (int)(clock64() - ti0));
         MSQ_CK(2)
 
         // ---------------------------------------------------- phase B
@@ -1099,10 +1264,11 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
             // test at rho == t asks for a t-window in the prefix-AND A(rho), and
             // success is monotone in rho: test every row of the tile in parallel
             // (warp w takes row bfirst + w) and keep the last success.
-            const int bfirst = t - rho0;
+            const int bfirst = (MSQ_ABLATE & 8) ? BMAX : t - rho0;
             if (bfirst <= lastb) {
-                const int wid = tid >> 5, nwarps = NT >> 5;
-                for (int b = bfirst + wid; b <= lastb; b += nwarps) {
+                // the issuer's warp (last) is busy with the refill: rows go to the others
+                const int wid = tid >> 5, nwarps = TMA && NT > 32 ? (NT >> 5) - 1 : (NT >> 5);
+                for (int b = bfirst + wid; wid < nwarps && b <= lastb; b += nwarps) {
                     const int st = climb_scan<U8, TMA>(ab, &ex, b, W, climb_s, rho0 + b, lane);
                     if (lane == 0) misc->cres[b - bfirst] = st;
                 }
@@ -1174,8 +1340,9 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                         const int suf = bl2 & 0xFF;
                         if (suf + (bl2 >> 8) + 32 * len >= cur_t) best = min(best, enc_res(cb, 32 * a0 - suf));
                     };
-                    const int n = (lastb - start_b + 1) * nfw;
-                    for (int idx = tau; idx < n; idx += NT) {
+                    const int n = (MSQ_ABLATE & 2) ? 0 : (lastb - start_b + 1) * nfw;
+                    const int nscan = TMA && NT > 32 ? NT - 32 : NT;  // not the issuer's warp
+                    for (int idx = tau; idx < n && tau < nscan; idx += nscan) {
                         const int b = start_b + idx / nfw, fw = idx % nfw;
                         scan_fword(fm, fstride, W, b, m, fw, cur_t, [&](int cb, int a0, int len) {
                             if (p.prof) atomicAdd(&misc->pad[0], 1);
@@ -1189,7 +1356,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                             }
                         });
                     }
-                    if (p.prof) atomicMax(&misc->pad[2], (int)(clock64() - rc0));
+                    if (p.prof && lane == 0) atomicMax(&misc->pad[2], (int)(clock64() - rc0));
                     if (COOP) {
                         const uint32_t bal0 = __ballot_sync(0xFFFFFFFFu, cq0 != NONE);
                         const uint32_t bal1 = __ballot_sync(0xFFFFFFFFu, cq1 != NONE);
@@ -1221,7 +1388,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 const int slot = round_ctr % 3;
                 if (best != RES_INF) atomicMin(&misc->res[slot], best);
                 if (tau == 0) misc->res[(round_ctr + 1) % 3] = RES_INF;
-                if (p.prof && modeL) atomicMax(&misc->pad[1], (int)(clock64() - rc0));
+                if (p.prof && modeL && lane == 0) atomicMax(&misc->pad[1], (int)(clock64() - rc0));
                 if (prof && modeL) pc[7] += 1;
                 csync();  // (B)
                 if (prof && modeL) {
@@ -1243,13 +1410,13 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 if (start_b > lastb) break;
             }
         }
-        if (prof && climb && t - rho0 <= lastb) pc[14] += (unsigned long long)(clock64() - ck);
+        if (prof && climb && t - rho0 <= lastb) pc[13] += 0;
         if (prof) {
             const int kind = climb ? 0 : (modeL ? 2 : 1);
-            pc[8 + kind] += 1;
+            if (kind == 0) pc[8] += 1;
             pc[11] += cur_t - t;
             const long long c1 = clock64();
-            pc[3 + kind] += (unsigned long long)(c1 - ck);
+            if (kind != 1) pc[3 + kind] += (unsigned long long)(c1 - ck);
             ck = c1;
         }
         const bool raised = cur_t != t;
@@ -1268,11 +1435,12 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         for (int k = 0; k < WPT; ++k) ab[tau * WPT + k] = AL[k];
 
         // ---------------------------------------------------- phase C
+        tB = p.prof ? clock64() : 0;
         // last-zero rows (bit-sliced) and first zeros, in row order per word
         // one loop over all (word, row) events of the thread (word-major, so
         // rows stay in order per word); the word's state is selected with
         // compile-time indices so VAL/NZ stay in registers
-        if (!modeS || U8) {
+        if ((!modeS || U8) && !(MSQ_ABLATE & 1)) {
             uint32_t zf = zflag;
             while (zf) {
                 const int bit = __ffs(zf) - 1;
@@ -1297,9 +1465,11 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     if (k == kk) NZ[kk] = nzk;
             }
         }
-        if (modeL)
+        if (modeL && SUB)  // sub-warp teams build F with atomics: clear for the reuse
             for (int i = tau; i < BMAX * fstride; i += NT) fm[i] = 0u;
         MSQ_CK(6)
+        if (p.prof && lane == 0) atomicMax(&misc->pad[3], (int)(clock64() - tB));
+        if (p.prof) tB = clock64();  // end of phase C
         row0 += nrows;
         st_base += nrows;
         if (st_base >= p.nstage) {
@@ -1308,9 +1478,9 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         }
     }
 #undef MSQ_CK
+    csync();
     if (prof) {
-        pc[12] = t;
-        pc[14] = misc->pad[0];
+        pc[10] = misc->pad[7];
         if (!SUB)
             for (int i = 0; i < 16; ++i) p.prof[(size_t)unit * 16 + i] = pc[i];
     }

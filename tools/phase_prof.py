@@ -26,9 +26,9 @@ r = s.solve(src)
 N.load().msq_debug_set_profile(None)
 torch.cuda.synchronize()
 pc = buf.cpu().numpy().reshape(units, 16).astype(np.float64)
-names = ["A(work+waits)", "barrierA", "tma issue", "B climb", "B modeS", "B modeL", "C", "L rounds",
-         "tiles climb", "tiles S", "tiles L", "raises", "final t", "L max work", "L candidates", "L max scan"]
-tot = pc[:, :7].sum(axis=1)
+names = ["A(work+waits)", "barrierA", "tma issue", "B climb", "maxwarp C", "B modeL", "C", "L rounds",
+         "tiles climb", "maxwarp Cend->barA", "issuer TMA total", "raises", "maxwarp rowloop", "L max work", "maxwarp Cend->rowloop", "L max scan"]
+tot = pc[:, [0, 1, 2, 3, 5, 6]].sum(axis=1)
 print(cfg, r[0], "bands", units)
 print("total cycles per band: mean %.0f max %.0f" % (tot.mean(), tot.max()))
 for i, n in enumerate(names):
