@@ -108,7 +108,7 @@ __host__ __device__ inline P1Layout p1_layout(int NT, int WPT, int nstage, int r
 }
 
 struct FixLayout {
-    int us, e8, hist, fmap, misc, total;
+    int us, e8, wmin, hist, fmap, misc, total;
 };
 __host__ __device__ inline FixLayout fix_layout(int NT, int WPT, int bs) {
     FixLayout L;
@@ -118,6 +118,8 @@ __host__ __device__ inline FixLayout fix_layout(int NT, int WPT, int bs) {
     off += wpad * 32 * 2;
     L.e8 = off;
     off += wpad * 32;
+    L.wmin = off;  // per word: min carry, min leading-ones depth (uint16 pairs)
+    off += wpad * 4;
     L.hist = off;
     off += bs * wpad * 4;
     L.fmap = off;
@@ -1619,60 +1621,80 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
     }
     for (int i = tau; i < 2 * BMAX * fstride; i += NT) fmap[i] = 0u;
 
+    // ---- prologue: carry-in heights (carry_scan_kernel) and leading-ones
+    // depths of the band top, coalesced 16-byte chunks (8 columns) per thread;
+    // the 4 chunk-threads of a word combine its minima by shuffles
+    uint32_t* wmin = (uint32_t*)(smem + Lo.wmin);
+    {
+        const uint4* cp4 = (const uint4*)(p.carry_in + (size_t)band * p.cols_pad);
+        const uint4* ep4 = (const uint4*)e_g;
+        uint4* us4 = (uint4*)us;
+        uint2* e82 = (uint2*)e8;
+        const int nchunk = Wpad * 4;  // multiple of 32: 4 lanes per word
+        for (int i = tau; i < nchunk; i += NT) {
+            const int a = i >> 2;
+            const uint32_t val = valid_mask(a, W, p.cols) >> (8 * (i & 3));
+            uint4 c4 = make_uint4(0, 0, 0, 0), e4 = make_uint4(0, 0, 0, 0);
+            if (a < W) {
+                c4 = cp4[i];
+                e4 = ep4[i];
+            }
+            us4[i] = c4;
+            const uint32_t cw[4] = {c4.x, c4.y, c4.z, c4.w}, ew[4] = {e4.x, e4.y, e4.z, e4.w};
+            uint32_t e8w[2] = {0u, 0u};
+            int minc = 0xFFFF, mine = 0xFFFF;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int c = (int)((cw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+                const int e = (int)((ew[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+                const bool v = (val >> j) & 1u;
+                e8w[j >> 2] |= (uint32_t)(v ? min(e, 255) : 0) << (8 * (j & 3));
+                if (v) {
+                    minc = min(minc, c);
+                    mine = min(mine, e);
+                }
+            }
+            e82[i] = make_uint2(e8w[0], e8w[1]);
+#pragma unroll
+            for (int o = 1; o < 4; o <<= 1) {
+                minc = min(minc, __shfl_xor_sync(0xFFFFFFFFu, minc, o));
+                mine = min(mine, __shfl_xor_sync(0xFFFFFFFFu, mine, o));
+            }
+            if ((i & 3) == 0) wmin[a] = (uint32_t)minc | ((uint32_t)mine << 16);
+        }
+    }
+    __syncthreads();
     uint32_t VAL[WPT];
     int MINC[WPT], MINE[WPT];
-    uint32_t CP[WPT][FIX_XPL], EP[WPT][FIX_XPL];  // mode X planes: min(c,63), min(e,63)
 #pragma unroll
     for (int k = 0; k < WPT; ++k) {
         const int a = tau * WPT + k;
-        const uint32_t v = valid_mask(a, W, p.cols);
-        VAL[k] = v;
-        MINC[k] = -0x3FFFFFFF;
-        MINE[k] = -1;
+        VAL[k] = valid_mask(a, W, p.cols);
+        const uint32_t mm = wmin[a];
+        const bool full = VAL[k] == 0xFFFFFFFFu;  // a partial word is never F
+        MINC[k] = full ? (int)(mm & 0xFFFFu) : -0x3FFFFFFF;
+        MINE[k] = full ? (int)(mm >> 16) : -1;
+    }
+    // mode X planes (min(c,63), min(e,63)) only matter for thresholds < FIX_TL
+    uint32_t CP[WPT][FIX_XPL], EP[WPT][FIX_XPL];
+#pragma unroll
+    for (int k = 0; k < WPT; ++k)
 #pragma unroll
         for (int q = 0; q < FIX_XPL; ++q) CP[k][q] = EP[k][q] = 0;
-        if (!v) continue;
-        uint16_t* uw = us + (size_t)a * 32;
-        // ---- carry-in heights (carry_scan_kernel) for this band
-        {
-            const uint4* cp4 = (const uint4*)(p.carry_in + (size_t)band * p.cols_pad + (size_t)32 * a);
-            uint4* up4 = (uint4*)uw;
+    if (max(1, misc->g) < FIX_TL) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) up4[q] = cp4[q];
-        }
-        // ---- leading-ones depth of the band top, per-word minima, mode X planes
-        const uint4* ep = (const uint4*)(e_g + (size_t)32 * a);
-        int minc = 0x7FFFFFFF, mine = 0x7FFFFFFF;
+        for (int k = 0; k < WPT; ++k) {
+            const int a = tau * WPT + k;
+            if (!VAL[k]) continue;
+            for (int j = 0; j < 32; ++j) {
+                if (!((VAL[k] >> j) & 1u)) continue;
+                const int e63 = min((int)e8[(size_t)a * 32 + j], 63), c63 = min((int)us[(size_t)a * 32 + j], 63);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint4 v4 = ep[q];
-            const uint32_t pr[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-#pragma unroll
-                for (int s = 0; s < 2; ++s) {
-                    const int j = 8 * q + 2 * h + s;
-                    if ((v >> j) & 1u) {
-                        const int e = (int)((pr[h] >> (16 * s)) & 0xFFFFu);
-                        e8[(size_t)a * 32 + j] = (uint8_t)min(e, 255);
-                        const int c = uw[j];
-                        mine = min(mine, e);
-                        minc = min(minc, c);
-                        const int e63 = min(e, 63), c63 = min(c, 63);
-#pragma unroll
-                        for (int pl = 0; pl < FIX_XPL; ++pl) {
-                            EP[k][pl] |= (uint32_t)((e63 >> pl) & 1) << j;
-                            CP[k][pl] |= (uint32_t)((c63 >> pl) & 1) << j;
-                        }
-                    } else {
-                        e8[(size_t)a * 32 + j] = 0;
-                    }
+                for (int pl = 0; pl < FIX_XPL; ++pl) {
+                    EP[k][pl] |= (uint32_t)((e63 >> pl) & 1) << j;
+                    CP[k][pl] |= (uint32_t)((c63 >> pl) & 1) << j;
                 }
             }
-        }
-        if (v == 0xFFFFFFFFu) {  // a partial word is never F
-            MINC[k] = minc;
-            MINE[k] = mine;
         }
     }
     __syncthreads();
@@ -1774,9 +1796,13 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
                             hist[b * Wpad + tau * WPT + k] = e;
                         }
                     }
-                    if (modeL && fnib) {
+                    if (modeL) {  // the 32/WPT lanes of one F word OR their bits, one stores
+                        constexpr int LPF = 32 / WPT;
                         const int a0 = tau * WPT;
-                        atomicOr(&fm[b * fstride + (a0 >> 5)], fnib << (a0 & 31));
+                        uint32_t v = fnib << (a0 & 31);
+#pragma unroll
+                        for (int o = 1; o < LPF; o <<= 1) v |= __shfl_xor_sync(0xFFFFFFFFu, v, o);
+                        if ((lane & (LPF - 1)) == 0) fm[b * fstride + (a0 >> 5)] = v;
                     }
                 }
             }
@@ -1843,8 +1869,6 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
             }
             t = cur_t;
             if (p.share) t = max(t, misc->g);
-            if (modeL)
-                for (int i = tau; i < BMAX * fstride; i += NT) fm[i] = 0u;
             d0 += nrows;
         }
     }
