@@ -221,8 +221,7 @@ int cuda_status(cudaError_t e) {
 cudaError_t launch_carry(const msq_plan* pl, void* ws, const uint32_t* base, cudaStream_t st) {
     WsLayout L = ws_layout(pl);
     uint8_t* w = (uint8_t*)ws;
-    const int threads = 256;
-    msq::carry_scan_kernel<<<(int)ceil_div(pl->cols, threads), threads, 0, st>>>(
+    msq::carry_scan_kernel<<<(int)ceil_div(pl->words * 32, 256), dim3(32, msq::CARRY_SEG), 0, st>>>(
         (int)pl->rows, (int)pl->cols, pl->words, pl->nbands, pl->words * 32, (const uint16_t*)(w + L.zb),
         (const uint32_t*)(w + L.ao), base, (uint16_t*)(w + L.carry));
     return cudaGetLastError();

@@ -43,7 +43,6 @@ constexpr int NPLANES = 7;   // mode S counters saturate at 127
 #define MSQ_ABLATE 0  // experiments: bit 0 = no zero events, bit 1 = no mode-L candidates, bit 2 = no F build, bit 3 = no climb tests
 #endif
 constexpr int BMAX = 8;      // max rows per tile
-constexpr int FIX_XPL = 6;   // fix-up mode X planes (c, e clamped at 63)
 constexpr int FIX_TL = 63;   // fix-up mode L threshold (runs then contain a full word)
 constexpr int MAXP = 12;     // last-zero bit planes: bands are <= 4095 rows
 
@@ -1675,29 +1674,6 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
         MINC[k] = full ? (int)(mm & 0xFFFFu) : -0x3FFFFFFF;
         MINE[k] = full ? (int)(mm >> 16) : -1;
     }
-    // mode X planes (min(c,63), min(e,63)) only matter for thresholds < FIX_TL
-    uint32_t CP[WPT][FIX_XPL], EP[WPT][FIX_XPL];
-#pragma unroll
-    for (int k = 0; k < WPT; ++k)
-#pragma unroll
-        for (int q = 0; q < FIX_XPL; ++q) CP[k][q] = EP[k][q] = 0;
-    if (max(1, misc->g) < FIX_TL) {
-#pragma unroll
-        for (int k = 0; k < WPT; ++k) {
-            const int a = tau * WPT + k;
-            if (!VAL[k]) continue;
-            for (int j = 0; j < 32; ++j) {
-                if (!((VAL[k] >> j) & 1u)) continue;
-                const int e63 = min((int)e8[(size_t)a * 32 + j], 63), c63 = min((int)us[(size_t)a * 32 + j], 63);
-#pragma unroll
-                for (int pl = 0; pl < FIX_XPL; ++pl) {
-                    EP[k][pl] |= (uint32_t)((e63 >> pl) & 1) << j;
-                    CP[k][pl] |= (uint32_t)((c63 >> pl) & 1) << j;
-                }
-            }
-        }
-    }
-    __syncthreads();
     int t = max(1, misc->g);
     FixExact ex{us, e8, e_g, W, p.cols, 1};
 
@@ -1781,30 +1757,29 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
             uint32_t* fm = fmap + (tile & 1) * BMAX * fstride;
             int polled = 0;
             if (p.share && tau == 0 && (tile & 7) == 7) polled = ld_volatile(res_best(result));
-#pragma unroll
-            for (int b = 0; b < BMAX; ++b) {
-                if (b < nrows) {
+            if (modeL) {
+                // F words: every column eligible at depth d (word minima); the
+                // 32/WPT lanes of one F word OR their bits and one stores
+                constexpr int LPF = 32 / WPT;
+                const int a0 = tau * WPT;
+                for (int b = 0; b < nrows; ++b) {
                     const int d = d0 + b;
                     uint32_t fnib = 0;
 #pragma unroll
-                    for (int k = 0; k < WPT; ++k) {
-                        if (modeL) {
-                            fnib |= ((d <= MINE[k] && MINC[k] + d >= t) ? 1u : 0u) << k;
-                        } else {  // t <= 62: exact E from the clamped planes
-                            const uint32_t e = planes_ge<FIX_XPL>(CP[k], max(t - d, 0)) &
-                                               planes_ge<FIX_XPL>(EP[k], d) & VAL[k];
-                            hist[b * Wpad + tau * WPT + k] = e;
-                        }
-                    }
-                    if (modeL) {  // the 32/WPT lanes of one F word OR their bits, one stores
-                        constexpr int LPF = 32 / WPT;
-                        const int a0 = tau * WPT;
-                        uint32_t v = fnib << (a0 & 31);
+                    for (int k = 0; k < WPT; ++k) fnib |= ((d <= MINE[k] && MINC[k] + d >= t) ? 1u : 0u) << k;
+                    uint32_t v = fnib << (a0 & 31);
 #pragma unroll
-                        for (int o = 1; o < LPF; o <<= 1) v |= __shfl_xor_sync(0xFFFFFFFFu, v, o);
-                        if ((lane & (LPF - 1)) == 0) fm[b * fstride + (a0 >> 5)] = v;
-                    }
+                    for (int o = 1; o < LPF; o <<= 1) v |= __shfl_xor_sync(0xFFFFFFFFu, v, o);
+                    if ((lane & (LPF - 1)) == 0) fm[b * fstride + (a0 >> 5)] = v;
                 }
+            } else {  // t < FIX_TL: exact E rows from the smem copies of c and e
+                ex.d0 = d0;
+                for (int b = 0; b < nrows; ++b)
+#pragma unroll
+                    for (int k = 0; k < WPT; ++k) {
+                        const int a = tau * WPT + k;
+                        hist[b * Wpad + a] = a < W ? ex.mask(a, b, t) : 0u;
+                    }
             }
             if (tau == 0 && (tile & 7) == 7) misc->g = polled;
             __syncthreads();
@@ -1882,31 +1857,73 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
 // carry[k][j] = true height of column j at the row above band k (clamped to
 // 65535; exact for cols <= 65536): fold (b, all-ones) of the
 // bands above, starting from base[j] (rows above this rank; 0 on one GPU).
-__global__ void carry_scan_kernel(int rows, int cols, int W, int nbands, int cols_pad, const uint16_t* b_in,
-                                  const uint32_t* ao_in, const uint32_t* base, uint16_t* carry_out) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= cols) return;
-    unsigned c = base ? base[j] : 0u;
-    carry_out[j] = (uint16_t)min(c, 65535u);
-    constexpr int U = 8;
-    for (int q0 = 0; q0 < nbands - 1; q0 += U) {
-        uint32_t fw[U];
-        uint16_t bv[U];
+// Segmented over bands: block = 32 threads x CARRY_SEG band segments, 8
+// columns per thread (16-byte loads/stores of the uint16 rows).  Each band is
+// the map c -> (all ones ? c + h_q : b_q); a segment composes its maps
+// (pass 1), then folds the maps of the segments above from base and writes
+// its carries (pass 2) -- 2 reads of the summaries, CARRY_SEG-way parallel.
+constexpr int CARRY_SEG = 8;
+__global__ void __launch_bounds__(32 * CARRY_SEG) carry_scan_kernel(int rows, int cols, int W, int nbands,
+                                                                    int cols_pad, const uint16_t* b_in,
+                                                                    const uint32_t* ao_in, const uint32_t* base,
+                                                                    uint16_t* carry_out) {
+    __shared__ uint32_t fval[CARRY_SEG][32][8];
+    __shared__ uint8_t fconst[CARRY_SEG][32];
+    const int lane = threadIdx.x, sg = threadIdx.y;
+    const int j0 = (blockIdx.x * 32 + lane) * 8;  // 8 columns; cols_pad is a multiple of 32
+    const int nq = nbands - 1;                     // transitions: carry of band q+1 from band q
+    const int L = (nq + CARRY_SEG - 1) / CARRY_SEG;
+    const int q0 = min(nq, sg * L), q1 = min(nq, q0 + L);
+    const bool ok = j0 < cols_pad;
+    unsigned v[8];
+    uint32_t isc = 0;  // bit i: column j0+i's composed map is constant
 #pragma unroll
-        for (int s = 0; s < U; ++s) {
-            const int q = q0 + s;
-            fw[s] = q < nbands - 1 ? ao_in[(size_t)q * W + (j >> 5)] : 0u;
-            bv[s] = q < nbands - 1 ? b_in[(size_t)q * cols_pad + j] : (uint16_t)0;
-        }
+    for (int i = 0; i < 8; ++i) v[i] = 0;
+    auto step = [&](int q, uint32_t& cmask) {
+        const uint32_t full8 = (ao_in[(size_t)q * W + (j0 >> 5)] >> (j0 & 31)) & 0xFFu;
+        const uint4 b4 = *(const uint4*)(b_in + (size_t)q * cols_pad + j0);
+        const uint32_t bw[4] = {b4.x, b4.y, b4.z, b4.w};
+        const unsigned hq = (unsigned)(band_row0(rows, nbands, q + 1) - band_row0(rows, nbands, q));
 #pragma unroll
-        for (int s = 0; s < U; ++s) {
-            const int q = q0 + s;
-            if (q < nbands - 1) {
-                const unsigned hq = (unsigned)(band_row0(rows, nbands, q + 1) - band_row0(rows, nbands, q));
-                c = ((fw[s] >> (j & 31)) & 1u) ? min(c + hq, 0x7FFFFFFFu) : (unsigned)bv[s];
-                carry_out[(size_t)(q + 1) * cols_pad + j] = (uint16_t)min(c, 65535u);
-            }
+        for (int i = 0; i < 8; ++i) {
+            const unsigned bq = (bw[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
+            v[i] = ((full8 >> i) & 1u) ? min(v[i] + hq, 0x7FFFFFFFu) : bq;
         }
+        cmask |= ~full8 & 0xFFu;
+    };
+    if (ok)
+        for (int q = q0; q < q1; ++q) step(q, isc);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) fval[sg][lane][i] = v[i];
+    fconst[sg][lane] = (uint8_t)isc;
+    __syncthreads();
+    if (!ok) return;
+    // pass 2: carries at the segment start, then the segment's rows
+    if (base) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = j0 + i < cols ? base[j0 + i] : 0u;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = 0;
+    }
+    for (int s2 = 0; s2 < sg; ++s2) {
+        const uint32_t cm = fconst[s2][lane];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            v[i] = ((cm >> i) & 1u) ? fval[s2][lane][i] : min(v[i] + fval[s2][lane][i], 0x7FFFFFFFu);
+    }
+    auto emit = [&](int row) {
+        uint32_t o[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+            o[h] = min(v[2 * h], 65535u) | (min(v[2 * h + 1], 65535u) << 16);
+        *(uint4*)(carry_out + (size_t)row * cols_pad + j0) = make_uint4(o[0], o[1], o[2], o[3]);
+    };
+    if (sg == 0) emit(0);
+    for (int q = q0; q < q1; ++q) {
+        uint32_t dummy = 0;
+        step(q, dummy);
+        emit(q + 1);
     }
 }
 
