@@ -1497,11 +1497,17 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 const uint32_t nz = NZ[k];
                 if (nz) {  // never-zeroed columns: e = H (16-byte merges of the first-zero rows)
                     uint4* eq = (uint4*)(p.e_out + cb);
+                    uint4 evs[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {  // all loads first (one round trip)
+                        const uint32_t nq = (nz >> (8 * q)) & 0xFFu;
+                        evs[q] = nq == 0u || nq == 0xFFu ? make_uint4(0, 0, 0, 0) : eq[q];
+                    }
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const uint32_t nq = (nz >> (8 * q)) & 0xFFu;
                         if (!nq) continue;
-                        uint4 ev = nq == 0xFFu ? make_uint4(0, 0, 0, 0) : eq[q];
+                        const uint4 ev = evs[q];
                         uint32_t v[4] = {ev.x, ev.y, ev.z, ev.w};
 #pragma unroll
                         for (int h = 0; h < 4; ++h) {
