@@ -227,6 +227,30 @@ cudaError_t launch_carry(const msq_plan* pl, void* ws, const uint32_t* base, cud
     return cudaGetLastError();
 }
 
+// Lower-bound seed before pass 1 (shared-threshold mode only): strips of
+// SEED_ROWS rows x 1024-column chunks, one warp each; about 2% of the input
+// bytes.  Skipped for small matrices, batches and deterministic plans.
+int seeds_launched(const msq_plan* pl) {
+    return (pl->deterministic || pl->batch != 1 || pl->rows < 8 * msq::SEED_ROWS || pl->cols < 256) ? 0 : 1;
+}
+cudaError_t launch_seed(const msq_plan* pl, const void* d_src, msq_devresult* d_result, cudaStream_t st) {
+    if (pl->deterministic || pl->batch != 1 || pl->rows < 8 * msq::SEED_ROWS || pl->cols < 256) return cudaSuccess;
+    const int chunks = (int)ceil_div(pl->words, 32);
+    const long long nstrips = std::max<long long>(1, std::min<long long>(pl->rows / 6400, std::max(1, 1024 / chunks)));
+    const long long warps = nstrips * chunks;
+    const long long ld_bytes = pl->fmt == MSQ_FMT_U8 ? pl->ld : pl->ld * 4;
+    const int blocks = (int)ceil_div(warps * 32, 256);
+    if (pl->fmt == MSQ_FMT_U8)
+        msq::seed_climb_kernel<true><<<blocks, 256, 0, st>>>((const uint8_t*)d_src, ld_bytes, (int)pl->rows,
+                                                              (int)pl->cols, pl->words, (int)nstrips, chunks,
+                                                              (unsigned char*)d_result);
+    else
+        msq::seed_climb_kernel<false><<<blocks, 256, 0, st>>>((const uint8_t*)d_src, ld_bytes, (int)pl->rows,
+                                                               (int)pl->cols, pl->words, (int)nstrips, chunks,
+                                                               (unsigned char*)d_result);
+    return cudaGetLastError();
+}
+
 // --------------------------------------------------- internal workspace
 struct DevCache {
     std::mutex mu;
@@ -415,17 +439,19 @@ int msq_launch(const msq_plan* pl, const void* d_src, void* d_ws, msq_devresult*
     if (cudaMemsetAsync(d_result, 0, sizeof(msq_devresult) * (size_t)pl->batch, st) != cudaSuccess)
         return MSQ_ECUDA;
     const bool multi = pl->batch == 1 && pl->nbands > 1;
-    msq::Pass1Params p1 = make_pass1(pl, d_src, d_ws, d_result, multi);
-    cudaError_t e = launch_pass1(pl, p1, st);
+    cudaError_t e = launch_seed(pl, d_src, d_result, st);
     if (e != cudaSuccess) return cuda_status(e);
-    g_last_launches = 1;
+    msq::Pass1Params p1 = make_pass1(pl, d_src, d_ws, d_result, multi);
+    e = launch_pass1(pl, p1, st);
+    if (e != cudaSuccess) return cuda_status(e);
+    g_last_launches = 1 + seeds_launched(pl);
     if (multi) {
         e = launch_carry(pl, d_ws, nullptr, st);
         if (e != cudaSuccess) return cuda_status(e);
         msq::FixParams f = make_fix(pl, d_ws, nullptr, d_result);
         e = launch_fixup(pl, f, pl->nbands - 1, st);
         if (e != cudaSuccess) return cuda_status(e);
-        g_last_launches = 3;
+        g_last_launches = 3 + seeds_launched(pl);
     }
     return MSQ_OK;
 }
@@ -499,8 +525,10 @@ int msq_rank_pass1(const msq_plan* pl, const void* d_src, void* d_ws, msq_devres
     }
     cudaStream_t st = (cudaStream_t)stream;
     if (cudaMemsetAsync(d_result, 0, sizeof(msq_devresult), st) != cudaSuccess) return MSQ_ECUDA;
+    cudaError_t e = launch_seed(pl, d_src, d_result, st);
+    if (e != cudaSuccess) return cuda_status(e);
     msq::Pass1Params p1 = make_pass1(pl, d_src, d_ws, d_result, true);
-    g_last_launches = 1;
+    g_last_launches = 1 + seeds_launched(pl);
     return cuda_status(launch_pass1(pl, p1, st));
 }
 

@@ -40,7 +40,7 @@ constexpr unsigned long long KEY_DIM_MASK = (1ull << KEY_DIM_BITS) - 1ull;
 constexpr uint32_t RES_INF = 0xFFFFFFFFu;
 constexpr int NPLANES = 7;   // mode S counters saturate at 127
 #ifndef MSQ_ABLATE
-#define MSQ_ABLATE 0  // experiments: bit 0 = no zero events, bit 1 = no mode-L candidates, bit 2 = no F build, bit 3 = no climb tests
+#define MSQ_ABLATE 0  // experiments: bit 0 = no zero events, bit 1 = no mode-L candidates, bit 2 = no F build, bit 3 = no climb tests, bit 4 = seed t=120, bit 5 = no band-end summaries
 #endif
 constexpr int BMAX = 8;      // max rows per tile
 constexpr int FIX_TL = 63;   // fix-up mode L threshold (runs then contain a full word)
@@ -990,6 +990,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         misc->res[0] = misc->res[1] = misc->res[2] = RES_INF;
         for (int i = 0; i < 8; ++i) misc->pad[i] = 0;
         misc->g = p.share ? ld_volatile(res_best(result)) : 0;
+        if (MSQ_ABLATE & 16) misc->g = max(misc->g, 120);
         if (TMA) {
             for (int s = 0; s < p.nstage; ++s) mbar_init(&bars[s], 1);
             fence_mbar_init();
@@ -1488,7 +1489,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     csync();
 
     // ---------------------------------------------------------- band outputs
-    if (p.write_summaries) {
+    if (p.write_summaries && !(MSQ_ABLATE & 32)) {
 #pragma unroll
         for (int k = 0; k < WPT; ++k) {
             const int a = tau * WPT + k;
@@ -1931,6 +1932,85 @@ __global__ void __launch_bounds__(32 * CARRY_SEG) carry_scan_kernel(int rows, in
         step(q, dummy);
         emit(q + 1);
     }
+}
+
+// ======================================================= lower-bound seed
+// A proven lower bound for the shared best side before pass 1: each warp runs
+// Algorithm 1 on a strip of SEED_ROWS rows x 32 words (1024 columns), heights
+// local to the strip (bit-sliced, 8 planes per lane), one threshold test per
+// row.  Any square it finds is a real square of the matrix, so the bands may
+// start testing at the largest one (ties included) -- the same argument as the
+// shared best side (P2); rows whose local heights cannot reach it need no test.
+constexpr int SEED_ROWS = 128;  // strip height (squares found are <= this)
+constexpr int SEED_BATCH = 16;  // rows loaded per batch (next batch in flight while one is processed)
+constexpr int SEED_STEP = 4;    // test every SEED_STEP rows at best + SEED_STEP (a lower bound needs no exactness)
+template <bool U8>
+__device__ __forceinline__ uint32_t seed_word(const uint8_t* rp, int w, int W, int cols) {
+    if (w >= W) return 0u;
+    if (!U8) return ((const uint32_t*)rp)[w];
+    const int c0 = 32 * w;
+    if (c0 + 32 <= cols && ((uintptr_t)(rp + c0) & 15) == 0)
+        return bits16(*(const uint4*)(rp + c0)) | (bits16(*(const uint4*)(rp + c0 + 16)) << 16);
+    uint32_t word = 0;
+    for (int j = 0; j < 32 && c0 + j < cols; ++j) word |= (uint32_t)(rp[c0 + j] & 1u) << j;
+    return word;
+}
+template <bool U8>
+__global__ void __launch_bounds__(256) seed_climb_kernel(const uint8_t* src, long long ld_bytes, int rows, int cols,
+                                                         int W, int nstrips, int chunks, unsigned char* result) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (gw >= nstrips * chunks) return;
+    const int strip = gw / chunks, chunk = gw - strip * chunks;
+    const int r0 = (int)((long long)rows * strip / nstrips);
+    const int nr = min(SEED_ROWS, rows - r0);
+    const int w = chunk * 32 + lane;
+    const uint32_t val = valid_mask(w, W, cols);
+    constexpr int P = 7;  // heights saturate at 127 (the strip is 128 rows)
+    uint32_t h[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) h[p] = 0u;
+    int best = 0;
+    uint32_t nxt[SEED_BATCH];
+#pragma unroll
+    for (int q = 0; q < SEED_BATCH; ++q) nxt[q] = q < nr ? seed_word<U8>(src + (size_t)(r0 + q) * ld_bytes, w, W, cols) : 0u;
+    for (int i0 = 0; i0 < nr; i0 += SEED_BATCH) {
+        uint32_t rw[SEED_BATCH];
+#pragma unroll
+        for (int q = 0; q < SEED_BATCH; ++q) {
+            rw[q] = nxt[q];
+            const int i = i0 + SEED_BATCH + q;
+            nxt[q] = i < nr ? seed_word<U8>(src + (size_t)(r0 + i) * ld_bytes, w, W, cols) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < SEED_BATCH; ++q) {
+            if (i0 + q >= nr) break;
+            planes_step<P>(h, rw[q] & val);
+            if ((q % SEED_STEP) != SEED_STEP - 1) continue;
+            const int T = min(best + SEED_STEP, (1 << P) - 1);
+            const uint32_t acc = planes_ge<P>(h, T) & val;
+            // run of eligible columns ending at the end of this lane's word (segmented warp scan)
+            const bool full = acc == 0xFFFFFFFFu;
+            int v = full ? 32 : __clz(~acc);
+            int f = full ? 1 : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v2 = __shfl_up_sync(0xFFFFFFFFu, v, o);
+                const int f2 = __shfl_up_sync(0xFFFFFFFFu, f, o);
+                if (lane >= o) {
+                    if (f) v += v2;
+                    f &= f2;
+                }
+            }
+            int rin = __shfl_up_sync(0xFFFFFFFFu, v, 1);
+            if (lane == 0) rin = 0;
+            const int pre = full ? 32 : __ffs(~acc) - 1;
+            bool ok = rin + pre >= T || v >= T;
+            if (!ok && T <= 32) ok = windows_in_word(acc, T) != 0u;
+            if (__any_sync(0xFFFFFFFFu, ok)) best = T;
+        }
+    }
+    if (lane == 0 && best > 0) atomicMax(res_best(result), best);
 }
 
 // ======================================================= row-band sharding

@@ -73,7 +73,7 @@ class GpuBackend:
         N.check(self.lib.msq_rank_pass1(ctypes.byref(self.plan), ctypes.c_void_p(src.data_ptr()),
                                         ctypes.c_void_p(self.ws.data_ptr()),
                                         ctypes.c_void_p(self.res.data_ptr()), self._stream()))
-        self.launches += 1
+        self.launches += int(self.lib.msq_last_launch_count())  # lower-bound seed + band pass
 
     def rank_summary(self):
         N.check(self.lib.msq_rank_summary(ctypes.byref(self.plan),

@@ -257,3 +257,29 @@ def test_row_band_ranks_on_one_gpu(torch, world):
             ks = torch.stack(keys).max(dim=0).values.cpu().numpy()
             got = decode_key(int(ks[0]), int(ks[1]), rows, cols)
             _same(got, oracle.freq(a))
+
+
+@pytest.mark.parametrize("fmt", ["u8", "bits"])
+def test_seed_lower_bound_keeps_ties_exact(torch, fmt):
+    """Matrices big enough for the lower-bound seed (strip-top climbs before
+    pass 1): the seed may equal the answer, and the reported location must
+    still be the lexicographically smallest maximal square."""
+    rng = np.random.default_rng(11 if fmt == "u8" else 12)
+    rows, cols = 2048, 1024
+    cases = [
+        [(0, 900, 60), (0, 100, 60)],      # both hang from the strip top: left decides
+        [(0, 500, 60), (5, 20, 60)],       # seed square is the answer (top 0)
+        [(0, 500, 60), (300, 20, 61)],     # a larger square elsewhere
+        [(700, 40, 75), (0, 200, 75), (1900, 900, 75)],
+        [(0, 0, 128)],                     # climb runs to the strip height
+    ]
+    for squares in cases:
+        a = (rng.random((rows, cols)) < 0.9).astype(np.uint8)
+        for (t_, l_, k) in squares:
+            a[t_:t_ + k, l_:l_ + k] = 1
+        want = oracle.freq(a)
+        if fmt == "u8":
+            got = freq_square(a)
+        else:
+            got = freq_square_bits(grid.pack_bits(a), cols)
+        _same(got, want)
