@@ -417,7 +417,8 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
             ns = stages(1);
         }
         while (p.tile_rows_l > p.tile_rows && ns < 2 * p.tile_rows_l) p.tile_rows_l /= 2;
-        if (ns >= 2 * p.tile_rows_l) p.nstage = (int32_t)ns;
+        // the ring is a whole number of tile-sized slots (one mbarrier, one bulk copy each)
+        if (ns >= 2 * p.tile_rows_l) p.nstage = (int32_t)(ns / p.tile_rows_l * p.tile_rows_l);
     }
     p.smem_pass1 = team_layout_bytes(&p);
     p.smem_fixup = msq::fix_layout(p.fix_threads, p.fix_wpt, p.tile_rows).total;

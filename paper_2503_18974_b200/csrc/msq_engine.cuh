@@ -801,39 +801,27 @@ __device__ __noinline__ void band_bottom_runs(const uint32_t* zp, int zbase, int
     }
 }
 
-// Rows b < nrows of a tile (stages st0.. of the ring, phase parity par0):
-// barrier waits for RG rows first, then their loads, then the zero tests
-// (one latency chain per group).  Returns the word-major zero flags (bit
-// k*BMAX + b: row b has a zero in word k); optionally folds the rows into the
-// prefix-AND AL and records it per row in hist (sub-warp climb tiles).
+// Rows b < nrows of a tile (ring stages st0.., already waited for): loads of
+// RG rows first, then their zero tests.  Returns the word-major zero flags
+// (bit k*BMAX + b: row b has a zero in word k); optionally folds the rows
+// into the prefix-AND AL and records it per row in hist (sub-warp climbs).
 template <int WPT, bool U8, bool TMA>
-__device__ __forceinline__ uint32_t tile_zero_flags(const Pass1Params& p, uint64_t* bars, const uint8_t* ring,
-                                                    const uint8_t* rows_base, int st0, uint32_t par0, int nrows,
-                                                    int tau, int W, const uint32_t (&VAL)[WPT], uint32_t (&AL)[WPT],
-                                                    bool do_al, uint32_t* hist, int Wpad, uint32_t& bad_or) {
+__device__ __forceinline__ uint32_t tile_zero_flags(const Pass1Params& p, const uint8_t* ring,
+                                                    const uint8_t* rows_base, int st0, int nrows, int tau, int W,
+                                                    const uint32_t (&VAL)[WPT], uint32_t (&AL)[WPT], bool do_al,
+                                                    uint32_t* hist, int Wpad, uint32_t& bad_or) {
     constexpr int RG = 4;
     uint32_t zflag = 0;
 #pragma unroll
     for (int h = 0; h < BMAX; h += RG) {
         if (h < nrows) {
-            const uint8_t* srow[RG];
-#pragma unroll
-            for (int g = 0; g < RG; ++g) {
-                const int b = h + g;
-                srow[g] = nullptr;
-                if (TMA && b < nrows) {
-                    const bool wrap = st0 + b >= p.nstage;
-                    const int sb = wrap ? st0 + b - p.nstage : st0 + b;
-                    mbar_wait(&bars[sb], wrap ? par0 ^ 1u : par0);
-                    srow[g] = ring + (size_t)sb * p.rs;
-                }
-            }
             uint32_t w[RG][WPT];
 #pragma unroll
             for (int g = 0; g < RG; ++g) {
                 const int b = h + g;
                 if (b < nrows) {
-                    fetch_words<WPT, U8, TMA>(srow[g], rows_base + (size_t)b * p.ld_bytes, tau, W, p.cols, p.rs, VAL,
+                    const uint8_t* srow = TMA ? ring + (size_t)(st0 + b) * p.rs : nullptr;
+                    fetch_words<WPT, U8, TMA>(srow, rows_base + (size_t)b * p.ld_bytes, tau, W, p.cols, p.rs, VAL,
                                               w[g], bad_or);
                 } else {
 #pragma unroll
@@ -860,40 +848,23 @@ __device__ __forceinline__ uint32_t tile_zero_flags(const Pass1Params& p, uint64
 // Lean form of tile_zero_flags for bit-packed TMA-staged rows (CTA teams):
 // per row one vector smem load and one "any zero in my words" flag; the
 // per-word flags are rebuilt only for the (few) rows that had a zero.
-// ring_s = shared address of the thread's words in ring stage 0, bars_s =
-// shared address of barrier 0, inv = ~valid mask per word.
+// ring_s = shared address of the thread's words in ring stage 0, inv = ~valid
+// mask per word.
 template <int WPT>
-__device__ __forceinline__ uint32_t tile_zero_flags_bits(uint32_t ring_s, uint32_t bars_s, int rs, int nstage, int st0,
-                                                         uint32_t par0, int nrows, bool active,
-                                                         const uint32_t (&inv)[WPT], uint32_t (&AL)[WPT],
-                                                         bool do_al, int* spins) {
+__device__ __forceinline__ uint32_t tile_zero_flags_bits(uint32_t ring_s, int rs, int st0, int nrows, bool active,
+                                                         const uint32_t (&inv)[WPT], uint32_t (&AL)[WPT], bool do_al,
+                                                         unsigned long long* trp = nullptr) {
     constexpr int RG = 4;
     uint32_t rowflag = 0;
+    const uint32_t base = ring_s + (uint32_t)(st0 * rs);
 #pragma unroll
     for (int h = 0; h < BMAX; h += RG) {
         if (h < nrows) {
-            uint32_t addr[RG], bar[RG], par[RG];
-            uint32_t ready = 1u;
-#pragma unroll
-            for (int g = 0; g < RG; ++g) {  // non-blocking tests of the group's barriers, back to back
-                const int b = h + g;
-                const bool wrap = st0 + b >= nstage;
-                const int sb = wrap ? st0 + b - nstage : st0 + b;
-                addr[g] = ring_s + (uint32_t)(sb * rs);
-                bar[g] = bars_s + 8u * (uint32_t)sb;
-                par[g] = wrap ? par0 ^ 1u : par0;
-                if (b < nrows) ready &= mbar_test_s(bar[g], par[g]);
-            }
-            if (!ready) {
-#pragma unroll
-                for (int g = 0; g < RG; ++g)
-                    if (h + g < nrows) mbar_wait_s(bar[g], par[g], spins);
-            }
             uint32_t w[RG][WPT];
 #pragma unroll
             for (int g = 0; g < RG; ++g) {
                 if (h + g < nrows && active) {
-                    lds_words<WPT>(addr[g], w[g]);
+                    lds_words<WPT>(base + (uint32_t)((h + g) * rs), w[g]);
                 } else {
 #pragma unroll
                     for (int k = 0; k < WPT; ++k) w[g][k] = 0xFFFFFFFFu;
@@ -911,13 +882,13 @@ __device__ __forceinline__ uint32_t tile_zero_flags_bits(uint32_t ring_s, uint32
             }
         }
     }
+    if (trp) *trp = (unsigned long long)clock64();
     uint32_t zflag = 0;
     while (rowflag) {  // rows with a zero somewhere in the thread's words
         const int b = __ffs(rowflag) - 1;
         rowflag &= rowflag - 1;
-        const int sb = st0 + b >= nstage ? st0 + b - nstage : st0 + b;
         uint32_t w[WPT];
-        lds_words<WPT>(ring_s + (uint32_t)(sb * rs), w);
+        lds_words<WPT>(base + (uint32_t)(b * rs), w);
 #pragma unroll
         for (int k = 0; k < WPT; ++k) zflag |= (w[k] | inv[k]) != 0xFFFFFFFFu ? (1u << (k * BMAX + b)) : 0u;
     }
@@ -992,21 +963,35 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         misc->g = p.share ? ld_volatile(res_best(result)) : 0;
         if (MSQ_ABLATE & 16) misc->g = max(misc->g, 120);
         if (TMA) {
-            for (int s = 0; s < p.nstage; ++s) mbar_init(&bars[s], 1);
+            for (int s = 0; s < p.nstage / p.bl; ++s) mbar_init(&bars[s], 1);
             fence_mbar_init();
         }
     }
     auto csync = [&]() { tsync<SUB>(tmask); };
     csync();
 
-    int issued = 0;  // rows staged so far (issuer thread)
-    if (TMA && tau == issuer) {
-        for (; issued < min(p.nstage, H); ++issued) {
-            mbar_expect_tx(&bars[issued], (uint32_t)p.row_bytes);
-            tma_row(ring + (size_t)issued * p.rs, mbase + (size_t)(r0 + issued) * p.ld_bytes, (uint32_t)p.row_bytes,
-                    &bars[issued], pol);
+    // TMA ring of slots: SR = p.bl consecutive band rows per slot, one mbarrier
+    // per slot, one bulk copy per slot when the rows are contiguous in memory
+    // (else one copy per row, all on the slot's barrier).  Tiles never straddle
+    // a slot; a slot is refilled once every row of it went through phase C.
+    const int SR = p.bl;
+    const int nslots = TMA ? p.nstage / SR : 1;
+    auto issue_slot = [&](int first) {
+        const int sl = (first / SR) % nslots;
+        const int n = min(SR, H - first);
+        mbar_expect_tx(&bars[sl], (uint32_t)(n * p.row_bytes));
+        uint8_t* dst = ring + (size_t)sl * SR * p.rs;
+        const uint8_t* srcp = mbase + (size_t)(r0 + first) * p.ld_bytes;
+        if (p.ld_bytes == (long long)p.rs && p.rs == p.row_bytes) {
+            tma_row(dst, srcp, (uint32_t)(n * p.row_bytes), &bars[sl], pol);
+        } else {
+            for (int q = 0; q < n; ++q)
+                tma_row(dst + (size_t)q * p.rs, srcp + (size_t)q * p.ld_bytes, (uint32_t)p.row_bytes, &bars[sl], pol);
         }
-    }
+    };
+    int issued = 0;  // issuer: first band row not yet staged (a multiple of SR)
+    if (TMA && tau == issuer)
+        for (; issued < H && issued < p.nstage; issued += SR) issue_slot(issued);
 
     uint32_t VAL[WPT], NZ[WPT], EPREV[WPT], AL[WPT];
     int ZW[WPT];
@@ -1065,9 +1050,6 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     uint32_t fullk = 0;  // words whose 32 columns are all valid (only those can be F)
 #pragma unroll
     for (int k = 0; k < WPT; ++k) fullk |= (VAL[k] == 0xFFFFFFFFu ? 1u : 0u) << k;
-    int st_base = 0;          // ring stage of the tile's first row
-    uint32_t par_base = 0u;   // its mbarrier phase parity
-    int iss_s = 0;            // issuer: stage of the next row to stage
 
     int t = max(1, misc->g);
     bool full_next = false;
@@ -1084,6 +1066,22 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     if (prof)
         for (int i = 0; i < 16; ++i) pc[i] = 0;
     long long ck = prof ? clock64() : 0;
+    // debug timeline (builds with -DMSQ_TRACE only): band 0, tiles [TR_T0, TR_T0+8),
+    // lane 0 of every warp, 16 stamps per tile kept in registers, stored at the tile end
+    constexpr int TR_T0 = 40;
+#ifdef MSQ_TRACE
+    unsigned long long* trace = p.prof ? p.prof + (size_t)p.units * 16 : nullptr;
+    long long trv[16];
+#define MSQ_TR(i) { trv[i] = clock64(); }
+#define MSQ_TR_FLUSH()                                                                                    \
+    if (trace && unit == 0 && tile >= TR_T0 && tile < TR_T0 + 8 && lane == 0)                            \
+        for (int q = 0; q < 16; ++q)                                                                      \
+            trace[(((size_t)(tile - TR_T0) * (NT >> 5) + (tau >> 5)) * 16) + q] = (unsigned long long)trv[q];
+#else
+    unsigned long long* trace = nullptr;
+#define MSQ_TR(i) {}
+#define MSQ_TR_FLUSH() {}
+#endif
 #define MSQ_CK(i)                               \
     if (prof) {                                 \
         const long long c1 = clock64();         \
@@ -1092,11 +1090,13 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     }
 
     for (int row0 = 0; row0 < H; ++tile) {
+        MSQ_TR(0)
         const int rho0 = row0 + 1;
         const bool climb = t >= rho0 && (SUB || t < p.tl);  // large t: mode L handles rho == t rows too
         const bool modeL = !climb && t >= p.tl;
         const bool modeS = !climb && !modeL;
-        const int nrows = min(climb ? (SUB ? 1 : p.bl) : (modeL ? p.bl : p.bs), H - row0);
+        const int slot_row0 = (row0 / SR) * SR;
+        const int nrows = min(min(climb ? (SUB ? 1 : p.bl) : (modeL ? p.bl : p.bs), H - row0), slot_row0 + SR - row0);
         uint32_t* fm = fmap + (tile & 1) * BMAX * fstride;
         int polled = 0;
         const bool poll = p.share && ((tile & 7) == 7 || (!climb && !modeL));
@@ -1104,8 +1104,10 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 
         // ---------------------------------------------------- phase A
         uint32_t dirty = 0, zflag = 0;
-        const int st0 = st_base;
-        const uint32_t par0 = par_base;
+        const int st0 = TMA ? ((row0 / SR) % nslots) * SR + (row0 - slot_row0) : 0;  // ring stage of tile row 0
+        if (TMA && row0 == slot_row0)  // first tile of a slot: wait for its rows (every thread)
+            mbar_wait(&bars[(row0 / SR) % nslots], (uint32_t)((row0 / SR) / nslots) & 1u);
+        MSQ_TR(12)
         if (tau == 0) {  // read only after barrier A; the previous tile's readers passed a barrier
             exs->tile_row0 = row0;
             exs->st0 = st0;
@@ -1117,11 +1119,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     const int r = row0 + b;
                     const int rho = r + 1;
                     const uint8_t* srow = nullptr;
-                    if (TMA) {
-                        const int sb = st0 + b >= p.nstage ? st0 + b - p.nstage : st0 + b;
-                        mbar_wait(&bars[sb], st0 + b >= p.nstage ? par0 ^ 1u : par0);
-                        srow = ring + (size_t)sb * p.rs;
-                    }
+                    if (TMA) srow = ring + (size_t)(st0 + b) * p.rs;
                     uint32_t w[WPT];
                     fetch_words<WPT, U8, TMA>(srow, mbase + (size_t)(r0 + r) * p.ld_bytes, tau, W, p.cols, p.rs,
                                               VAL, w, bad_or);
@@ -1150,16 +1148,17 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         } else {  // ---- climb / mode L: per word one zero test, the last-zero row, F
             if (!U8 && TMA && !SUB) {
                 const long long ta0 = p.prof ? clock64() : 0;
-                zflag = tile_zero_flags_bits<WPT>(ring_s, bars_s, p.rs, p.nstage, st0, par0, nrows, tau * WPT < W, INV,
-                                                  AL, !modeL, nullptr);
+                zflag = tile_zero_flags_bits<WPT>(ring_s, p.rs, st0, nrows, tau * WPT < W, INV, AL, !modeL);
+                MSQ_TR(11)
                 if (p.prof && lane == 0) {
                     atomicMax(&misc->pad[5], (int)(clock64() - ta0));
                     atomicMax(&misc->pad[6], (int)(ta0 - tB));
                 }
+                MSQ_TR(1)
             } else {
-                zflag = tile_zero_flags<WPT, U8, TMA>(p, bars, ring, mbase + (size_t)(r0 + row0) * p.ld_bytes, st0,
-                                                      par0, nrows, tau, W, VAL, AL, true,
-                                                      SUB && !modeL ? hist : nullptr, Wpad, bad_or);
+                zflag = tile_zero_flags<WPT, U8, TMA>(p, ring, mbase + (size_t)(r0 + row0) * p.ld_bytes, st0, nrows,
+                                                      tau, W, VAL, AL, true, SUB && !modeL ? hist : nullptr, Wpad,
+                                                      bad_or);
             }
             if (modeL && !(MSQ_ABLATE & 4)) {
                 // F words of row b: zero-free since rho_b - t, i.e. no zero in
@@ -1203,6 +1202,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 }
             }
         }
+        MSQ_TR(13)
         // last zero row of each word after the tile
 #pragma unroll
         for (int k = 0; k < WPT; ++k) {
@@ -1211,8 +1211,10 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         }
         if (tau == 0 && poll) misc->g = polled;
         if (p.prof && lane == 0) atomicMax(&misc->pad[4], (int)(clock64() - tB));
+        MSQ_TR(2)
         MSQ_CK(0)
         csync();  // (A)
+        MSQ_TR(3)
         MSQ_CK(1)
         if (prof) {
             pc[4] += misc->pad[3];
@@ -1222,16 +1224,10 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
             misc->pad[3] = misc->pad[4] = misc->pad[5] = misc->pad[6] = 0;
         }
         const long long ti0 = p.prof ? clock64() : 0;
-        if (TMA && tau == issuer) {  // stages of the previous tile are free now
-            const int upto = min(row0 + p.nstage, H);
-            for (; issued < upto; ++issued) {
-                mbar_expect_tx(&bars[iss_s], (uint32_t)p.row_bytes);
-                tma_row(ring + (size_t)iss_s * p.rs, mbase + (size_t)(r0 + issued) * p.ld_bytes,
-                        (uint32_t)p.row_bytes, &bars[iss_s], pol);
-                if (++iss_s == p.nstage) iss_s = 0;
-            }
-        }
+        if (TMA && tau == issuer)  // slots below the current one are consumed: refill them
+            for (; issued < H && issued < slot_row0 + p.nstage; issued += SR) issue_slot(issued);
         if (p.prof && tau == issuer) atomicAdd(&misc->pad[7], (int)(clock64() - ti0));
+        MSQ_TR(4)
         MSQ_CK(2)
 
         // ---------------------------------------------------- phase B
@@ -1324,6 +1320,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
             }
         } else {
             int start_b = 0, full_from = full_next ? 0 : BMAX;
+            bool round_ctr_first = true;
             for (;;) {
                 uint32_t best = RES_INF;
                 const int m = cur_t - t;
@@ -1359,6 +1356,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                         });
                     }
                     if (p.prof && lane == 0) atomicMax(&misc->pad[2], (int)(clock64() - rc0));
+                    if (round_ctr_first) MSQ_TR(5)
                     if (COOP) {
                         const uint32_t bal0 = __ballot_sync(0xFFFFFFFFu, cq0 != NONE);
                         const uint32_t bal1 = __ballot_sync(0xFFFFFFFFu, cq1 != NONE);
@@ -1387,12 +1385,16 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 } else {
                     best = test_rows_s(hist, Wpad, W, WPT, tau, start_b, lastb, full_from, dirty, m, cur_t);
                 }
+                if (round_ctr_first) MSQ_TR(6)
                 const int slot = round_ctr % 3;
                 if (best != RES_INF) atomicMin(&misc->res[slot], best);
                 if (tau == 0) misc->res[(round_ctr + 1) % 3] = RES_INF;
                 if (p.prof && modeL && lane == 0) atomicMax(&misc->pad[1], (int)(clock64() - rc0));
+                if (round_ctr_first) MSQ_TR(7)
                 if (prof && modeL) pc[7] += 1;
                 csync();  // (B)
+                if (round_ctr_first) MSQ_TR(8)
+                round_ctr_first = false;
                 if (prof && modeL) {
                     pc[13] += misc->pad[1];
                     pc[15] += misc->pad[2];
@@ -1421,6 +1423,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
             if (kind != 1) pc[3 + kind] += (unsigned long long)(c1 - ck);
             ck = c1;
         }
+        MSQ_TR(14)
         const bool raised = cur_t != t;
         t = cur_t;
         bool jumped = false;
@@ -1437,6 +1440,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         for (int k = 0; k < WPT; ++k) ab[tau * WPT + k] = AL[k];
 
         // ---------------------------------------------------- phase C
+        MSQ_TR(9)
         tB = p.prof ? clock64() : 0;
         // last-zero rows (bit-sliced) and first zeros, in row order per word
         // one loop over all (word, row) events of the thread (word-major, so
@@ -1470,16 +1474,15 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         if (modeL && SUB)  // sub-warp teams build F with atomics: clear for the reuse
             for (int i = tau; i < BMAX * fstride; i += NT) fm[i] = 0u;
         MSQ_CK(6)
+        MSQ_TR(10)
+        MSQ_TR_FLUSH()
         if (p.prof && lane == 0) atomicMax(&misc->pad[3], (int)(clock64() - tB));
         if (p.prof) tB = clock64();  // end of phase C
         row0 += nrows;
-        st_base += nrows;
-        if (st_base >= p.nstage) {
-            st_base -= p.nstage;
-            par_base ^= 1u;
-        }
     }
 #undef MSQ_CK
+#undef MSQ_TR
+#undef MSQ_TR_FLUSH
     csync();
     if (prof) {
         pc[10] = misc->pad[7];
