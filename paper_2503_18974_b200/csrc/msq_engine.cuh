@@ -598,7 +598,7 @@ struct Pass1Exact {
     int r0;         // band top row (matrix)
     int st0;        // ring stage of tile row 0
     __device__ __forceinline__ const uint8_t* srow(int b) const {
-        return TMA ? ring + (size_t)(st0 + b >= nstage ? st0 + b - nstage : st0 + b) * rs : nullptr;
+        return TMA ? ring + (size_t)(st0 + b) * rs : nullptr;  // a tile never wraps the ring (slots)
     }
     __device__ __forceinline__ const uint8_t* grow(int b) const {
         return mbase + (size_t)(r0 + tile_row0 + b) * ld_bytes;
@@ -850,9 +850,9 @@ __device__ __forceinline__ uint32_t tile_zero_flags(const Pass1Params& p, const 
 // per-word flags are rebuilt only for the (few) rows that had a zero.
 // ring_s = shared address of the thread's words in ring stage 0, inv = ~valid
 // mask per word.
-template <int WPT>
+template <int WPT, bool DO_AL>
 __device__ __forceinline__ uint32_t tile_zero_flags_bits(uint32_t ring_s, int rs, int st0, int nrows, bool active,
-                                                         const uint32_t (&inv)[WPT], uint32_t (&AL)[WPT], bool do_al,
+                                                         const uint32_t (&inv)[WPT], uint32_t (&AL)[WPT],
                                                          unsigned long long* trp = nullptr) {
     constexpr int RG = 4;
     uint32_t rowflag = 0;
@@ -876,7 +876,7 @@ __device__ __forceinline__ uint32_t tile_zero_flags_bits(uint32_t ring_s, int rs
 #pragma unroll
                 for (int k = 0; k < WPT; ++k) {
                     all &= w[g][k] | inv[k];
-                    if (do_al) AL[k] &= w[g][k];
+                    if (DO_AL) AL[k] &= w[g][k];
                 }
                 rowflag |= all != 0xFFFFFFFFu ? (1u << (h + g)) : 0u;
             }
@@ -1045,7 +1045,8 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     uint32_t INV[WPT];  // ~valid mask per word (lean bits row loop)
 #pragma unroll
     for (int k = 0; k < WPT; ++k) INV[k] = ~VAL[k];
-    const uint32_t ring_s = smem_addr(ring) + (uint32_t)(tau * WPT * 4);
+    const uint32_t ring_s0 = smem_addr(ring);
+    const uint32_t ring_s = ring_s0 + (uint32_t)(tau * WPT * 4);
     const uint32_t bars_s = smem_addr(bars);
     uint32_t fullk = 0;  // words whose 32 columns are all valid (only those can be F)
 #pragma unroll
@@ -1148,7 +1149,8 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         } else {  // ---- climb / mode L: per word one zero test, the last-zero row, F
             if (!U8 && TMA && !SUB) {
                 const long long ta0 = p.prof ? clock64() : 0;
-                zflag = tile_zero_flags_bits<WPT>(ring_s, p.rs, st0, nrows, tau * WPT < W, INV, AL, !modeL);
+                zflag = modeL ? tile_zero_flags_bits<WPT, false>(ring_s, p.rs, st0, nrows, tau * WPT < W, INV, AL)
+                              : tile_zero_flags_bits<WPT, true>(ring_s, p.rs, st0, nrows, tau * WPT < W, INV, AL);
                 MSQ_TR(11)
                 if (p.prof && lane == 0) {
                     atomicMax(&misc->pad[5], (int)(clock64() - ta0));
@@ -1178,12 +1180,20 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     // the 32/WPT lanes that own one F word OR their bits together
                     // and one of them stores it (no atomics, no clearing)
                     constexpr int LPF = 32 / WPT;
+                    // WPT == 4: the 4x8 bit matrix (word k, row b) as bytes of X; the
+                    // nibble of row b = bits b, 8+b, 16+b, 24+b gathered by one multiply
+                    uint32_t X = 0;
+                    if (WPT == 4) X = fr[0] | (fr[(1) % WPT] << 8) | (fr[(2) % WPT] << 16) | (fr[(3) % WPT] << 24);
 #pragma unroll
                     for (int b = 0; b < BMAX; ++b) {
                         if (b < nrows) {
                             uint32_t v = 0;
+                            if (WPT == 4) {
+                                v = (((X >> b) & 0x01010101u) * 0x01020408u) >> 24;
+                            } else {
 #pragma unroll
-                            for (int k = 0; k < WPT; ++k) v |= ((fr[k] >> b) & 1u) << k;
+                                for (int k = 0; k < WPT; ++k) v |= ((fr[k] >> b) & 1u) << k;
+                            }
                             v <<= (a0 & 31);
 #pragma unroll
                             for (int o = 1; o < LPF; o <<= 1) v |= __shfl_xor_sync(0xFFFFFFFFu, v, o);
@@ -1461,10 +1471,15 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     }
                 const int a = tau * WPT + k;
                 const int r = row0 + b, rho = r + 1;
-                const uint8_t* srow =
-                    TMA ? ring + (size_t)(st0 + b >= p.nstage ? st0 + b - p.nstage : st0 + b) * p.rs : nullptr;
-                const uint32_t wv =
-                    word_of_row<U8, TMA>(srow, mbase + (size_t)(r0 + r) * p.ld_bytes, a, p.cols, p.rs);
+                uint32_t wv;
+                if (TMA && !U8) {  // the tile's rows never wrap the ring (slots)
+                    uint32_t w1[1];
+                    lds_words<1>(ring_s0 + (uint32_t)((st0 + b) * p.rs + a * 4), w1);
+                    wv = w1[0];
+                } else {
+                    const uint8_t* srow = TMA ? ring + (size_t)(st0 + b) * p.rs : nullptr;
+                    wv = word_of_row<U8, TMA>(srow, mbase + (size_t)(r0 + r) * p.ld_bytes, a, p.cols, p.rs);
+                }
                 apply_event(nzk, valk, k * NT + tau, a, rho, valk & ~wv, !modeS);
 #pragma unroll
                 for (int kk = 0; kk < WPT; ++kk)
