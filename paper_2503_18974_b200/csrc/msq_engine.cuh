@@ -920,6 +920,8 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     const int W = p.W;
     const int Wpad = NT * WPT;
     const int nfw = (Wpad + 31) / 32;
+    const bool nfw_pow2 = (nfw & (nfw - 1)) == 0;
+    const int nfw_sh = __ffs(nfw) - 1;
     const int fstride = r16(nfw * 4) / 4;
     const int r0 = band_row0(p.rows, p.nbands, band);
     const int H = band_row0(p.rows, p.nbands, band + 1) - r0;
@@ -989,16 +991,17 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 tma_row(dst + (size_t)q * p.rs, srcp + (size_t)q * p.ld_bytes, (uint32_t)p.row_bytes, &bars[sl], pol);
         }
     };
+    int slot_no = 0, slot_idx = 0;  // slot of the current tile: band slot number, ring slot
+    uint32_t slot_par = 0u;         // its mbarrier phase parity
     int issued = 0;  // issuer: first band row not yet staged (a multiple of SR)
     if (TMA && tau == issuer)
         for (; issued < H && issued < p.nstage; issued += SR) issue_slot(issued);
 
-    uint32_t VAL[WPT], NZ[WPT], EPREV[WPT], AL[WPT];
+    uint32_t VAL[WPT], EPREV[WPT], AL[WPT];  // never-zeroed masks live in smem (nzm)
     int ZW[WPT];
 #pragma unroll
     for (int k = 0; k < WPT; ++k) {
         VAL[k] = valid_mask(tau * WPT + k, W, p.cols);
-        NZ[k] = VAL[k];
         AL[k] = VAL[k];
         EPREV[k] = 0;
         ZW[k] = 0;
@@ -1038,7 +1041,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 }
             }
             nzk &= ~zeros;
-            if (!U8) nzm[a] = nzk;
+            nzm[a] = nzk;
         }
     };
 
@@ -1048,6 +1051,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     const uint32_t ring_s0 = smem_addr(ring);
     const uint32_t ring_s = ring_s0 + (uint32_t)(tau * WPT * 4);
     const uint32_t bars_s = smem_addr(bars);
+    const uint32_t lastval = valid_mask(W - 1, W, p.cols);  // the only word that may be partial
     uint32_t fullk = 0;  // words whose 32 columns are all valid (only those can be F)
 #pragma unroll
     for (int k = 0; k < WPT; ++k) fullk |= (VAL[k] == 0xFFFFFFFFu ? 1u : 0u) << k;
@@ -1096,7 +1100,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         const bool climb = t >= rho0 && (SUB || t < p.tl);  // large t: mode L handles rho == t rows too
         const bool modeL = !climb && t >= p.tl;
         const bool modeS = !climb && !modeL;
-        const int slot_row0 = (row0 / SR) * SR;
+        const int slot_row0 = slot_no * SR;  // slot_no = row0 / SR (kept incrementally)
         const int nrows = min(min(climb ? (SUB ? 1 : p.bl) : (modeL ? p.bl : p.bs), H - row0), slot_row0 + SR - row0);
         uint32_t* fm = fmap + (tile & 1) * BMAX * fstride;
         int polled = 0;
@@ -1105,9 +1109,9 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 
         // ---------------------------------------------------- phase A
         uint32_t dirty = 0, zflag = 0;
-        const int st0 = TMA ? ((row0 / SR) % nslots) * SR + (row0 - slot_row0) : 0;  // ring stage of tile row 0
+        const int st0 = TMA ? slot_idx * SR + (row0 - slot_row0) : 0;  // ring stage of tile row 0
         if (TMA && row0 == slot_row0)  // first tile of a slot: wait for its rows (every thread)
-            mbar_wait(&bars[(row0 / SR) % nslots], (uint32_t)((row0 / SR) / nslots) & 1u);
+            mbar_wait(&bars[slot_idx], slot_par);
         MSQ_TR(12)
         if (tau == 0) {  // read only after barrier A; the previous tile's readers passed a barrier
             exs->tile_row0 = row0;
@@ -1137,8 +1141,9 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                             e = (lim >= (1 << P) ? 0xFFFFFFFFu : planes_le(zp, zi, Wpad, P, lim)) & VAL[k];
                         } else {  // bits inputs, small threshold: slow path through global z
                             const int a = tau * WPT + k;
-                            if (z) apply_event(NZ[k], VAL[k], k * NT + tau, a, rho, VAL[k] & ~w[k], true);
-                            e = bits_small_e(zg, za[a], a, NZ[k], VAL[k], lim);
+                            uint32_t nzk = nzm[a];
+                            if (z) apply_event(nzk, VAL[k], k * NT + tau, a, rho, VAL[k] & ~w[k], true);
+                            e = bits_small_e(zg, za[a], a, nzk, VAL[k], lim);
                         }
                         if (e & ~EPREV[k]) dirty |= 1u << (b * WPT + k);
                         EPREV[k] = e;
@@ -1352,7 +1357,8 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     const int n = (MSQ_ABLATE & 2) ? 0 : (lastb - start_b + 1) * nfw;
                     const int nscan = TMA && NT > 32 ? NT - 32 : NT;  // not the issuer's warp
                     for (int idx = tau; idx < n && tau < nscan; idx += nscan) {
-                        const int b = start_b + idx / nfw, fw = idx % nfw;
+                        const int b = start_b + (nfw_pow2 ? idx >> nfw_sh : idx / nfw);
+                        const int fw = nfw_pow2 ? idx & (nfw - 1) : idx % nfw;
                         scan_fword(fm, fstride, W, b, m, fw, cur_t, [&](int cb, int a0, int len) {
                             if (p.prof) atomicAdd(&misc->pad[0], 1);
                             const uint32_t cand = (uint32_t)cb | ((uint32_t)a0 << 3) | ((uint32_t)len << 14);
@@ -1462,14 +1468,9 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 const int bit = __ffs(zf) - 1;
                 zf &= zf - 1;
                 const int k = bit / BMAX, b = bit % BMAX;
-                uint32_t valk = VAL[0], nzk = NZ[0];
-#pragma unroll
-                for (int kk = 1; kk < WPT; ++kk)
-                    if (k == kk) {
-                        valk = VAL[kk];
-                        nzk = NZ[kk];
-                    }
                 const int a = tau * WPT + k;
+                const uint32_t valk = a == W - 1 ? lastval : 0xFFFFFFFFu;  // events only occur in valid words
+                uint32_t nzk = nzm[a];
                 const int r = row0 + b, rho = r + 1;
                 uint32_t wv;
                 if (TMA && !U8) {  // the tile's rows never wrap the ring (slots)
@@ -1481,9 +1482,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                     wv = word_of_row<U8, TMA>(srow, mbase + (size_t)(r0 + r) * p.ld_bytes, a, p.cols, p.rs);
                 }
                 apply_event(nzk, valk, k * NT + tau, a, rho, valk & ~wv, !modeS);
-#pragma unroll
-                for (int kk = 0; kk < WPT; ++kk)
-                    if (k == kk) NZ[kk] = nzk;
+
             }
         }
         if (modeL && SUB)  // sub-warp teams build F with atomics: clear for the reuse
@@ -1494,6 +1493,13 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
         if (p.prof && lane == 0) atomicMax(&misc->pad[3], (int)(clock64() - tB));
         if (p.prof) tB = clock64();  // end of phase C
         row0 += nrows;
+        if (row0 == slot_row0 + SR) {  // next slot
+            ++slot_no;
+            if (++slot_idx == nslots) {
+                slot_idx = 0;
+                slot_par ^= 1u;
+            }
+        }
     }
 #undef MSQ_CK
 #undef MSQ_TR
@@ -1513,7 +1519,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
             const int a = tau * WPT + k;
             if (a < W) {
                 const size_t cb = sum_base + (size_t)a * 32;
-                const uint32_t nz = NZ[k];
+                const uint32_t nz = nzm[a];
                 if (nz) {  // never-zeroed columns: e = H (16-byte merges of the first-zero rows)
                     uint4* eq = (uint4*)(p.e_out + cb);
                     uint4 evs[4];
@@ -1549,14 +1555,14 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 #pragma unroll
                         for (int h = 0; h < 4; ++h) {
                             const int j0 = 8 * q + 2 * h;
-                            const int u0 = ((NZ[k] >> j0) & 1u) ? 0 : max((int)(pr[h] & 0xFFFFu), zaa);
-                            const int u1 = ((NZ[k] >> (j0 + 1)) & 1u) ? 0 : max((int)(pr[h] >> 16), zaa);
+                            const int u0 = ((nz >> j0) & 1u) ? 0 : max((int)(pr[h] & 0xFFFFu), zaa);
+                            const int u1 = ((nz >> (j0 + 1)) & 1u) ? 0 : max((int)(pr[h] >> 16), zaa);
                             v[h] = (uint32_t)(H - u0) | ((uint32_t)(H - u1) << 16);
                         }
                         zq[q] = make_uint4(v[0], v[1], v[2], v[3]);
                     }
                 }
-                p.ao_out[(size_t)band * W + a] = NZ[k];
+                p.ao_out[(size_t)band * W + a] = nz;
             }
         }
     }
