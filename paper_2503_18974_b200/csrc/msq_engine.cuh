@@ -107,7 +107,7 @@ __host__ __device__ inline P1Layout p1_layout(int NT, int WPT, int nstage, int r
 }
 
 struct FixLayout {
-    int us, e8, wmin, hist, fmap, misc, total;
+    int us, e8, wmin, hist, fmap, dmark, misc, total;
 };
 __host__ __device__ inline FixLayout fix_layout(int NT, int WPT, int bs) {
     FixLayout L;
@@ -123,6 +123,8 @@ __host__ __device__ inline FixLayout fix_layout(int NT, int WPT, int bs) {
     off += bs * wpad * 4;
     L.fmap = off;
     off += 2 * BMAX * r16(nfw * 4);
+    L.dmark = off;  // depth filter bitmap (band heights <= 4095)
+    off += r16((4096 / 32 + 1) * 4);
     off = r16(off);  // Misc holds 8/16-byte members
     L.misc = off;
     off += r16((int)sizeof(Misc));
@@ -1708,6 +1710,54 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
     int t = max(1, misc->g);
     FixExact ex{us, e8, e_g, W, p.cols, 1};
 
+    // Depth filter (t >= FIX_TL): a window at depth d contains a run of at
+    // least len_min words whose 32 columns are all eligible, and word a is
+    // such an F word exactly on the depths [t - minc_a, mine_a].  Mark the
+    // depths covered by the intersection of len_min consecutive intervals;
+    // unmarked depths (and the depth-1 probe) need no test.  t only grows, so
+    // marks made with the starting t stay a superset.
+    const bool dfilt = t >= FIX_TL;
+    uint32_t* dmark = (uint32_t*)(smem + Lo.dmark);
+    if (dfilt) {
+        const int nmw = (H >> 5) + 1;
+        for (int i = tau; i < nmw; i += NT) dmark[i] = 0u;
+        __syncthreads();
+        const int len_min = max(1, (t - 63 + 31) / 32);
+        const bool last_full = valid_mask(W - 1, W, p.cols) == 0xFFFFFFFFu;
+#pragma unroll
+        for (int k = 0; k < WPT; ++k) {
+            const int a = tau * WPT + k;
+            if (a >= W || VAL[k] != 0xFFFFFFFFu) continue;
+            int LO = max(1, t - MINC[k]), HI = min(MINE[k], H), len = 1;
+            for (int a2 = a + 1; LO <= HI && len < len_min && a2 < W; ++a2, ++len) {
+                if (a2 == W - 1 && !last_full) {
+                    LO = HI + 1;
+                    break;
+                }
+                const uint32_t mm = wmin[a2];
+                LO = max(LO, t - (int)(mm & 0xFFFFu));
+                HI = min(HI, (int)(mm >> 16));
+            }
+            if (LO <= HI && len >= len_min)
+                for (int d = LO; d <= HI;) {
+                    const int wd = d >> 5, lo_b = d & 31, hi_b = min(31, lo_b + (HI - d));
+                    const uint32_t bits = (hi_b == 31 ? 0xFFFFFFFFu : ((1u << (hi_b + 1)) - 1u)) & ~((1u << lo_b) - 1u);
+                    atomicOr(&dmark[wd], bits);
+                    d += hi_b - lo_b + 1;
+                }
+        }
+        __syncthreads();
+    }
+    auto dmarked = [&](int d0, int n) -> bool {  // any marked depth in [d0, d0 + n)
+        const int d1 = d0 + n - 1;
+        for (int wd = d0 >> 5; wd <= (d1 >> 5); ++wd) {
+            const int lo_b = wd == (d0 >> 5) ? (d0 & 31) : 0, hi_b = wd == (d1 >> 5) ? (d1 & 31) : 31;
+            const uint32_t bits = (hi_b == 31 ? 0xFFFFFFFFu : ((1u << (hi_b + 1)) - 1u)) & ~((1u << lo_b) - 1u);
+            if (dmark[wd] & bits) return true;
+        }
+        return false;
+    };
+
     int round_ctr = 0;
     auto round_result = [&](uint32_t best) -> uint32_t {
         const int slot = round_ctr % 3;
@@ -1742,7 +1792,7 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
     unsigned long long fixkey = 0ull;
     if (H >= 1) {
         // ---------------------------------------------- depth 1, exact seeding
-        const uint32_t r = probe(t);
+        const uint32_t r = (!dfilt || dmarked(1, 1)) ? probe(t) : RES_INF;
         if (r != RES_INF) {
             int lo = t, hi = -1;
             uint32_t rlo = r;
@@ -1785,6 +1835,10 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
         for (int d0 = 2; d0 <= H && d0 < t; ++tile) {
             const bool modeL = t >= FIX_TL;
             const int nrows = min(modeL ? p.bl : p.bs, H - d0 + 1);
+            if (dfilt && !dmarked(d0, nrows)) {  // no run of F words at these depths
+                d0 += nrows;
+                continue;
+            }
             uint32_t* fm = fmap + (tile & 1) * BMAX * fstride;
             int polled = 0;
             if (p.share && tau == 0 && (tile & 7) == 7) polled = ld_volatile(res_best(result));
