@@ -1662,15 +1662,25 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
         const uint4* ep4 = (const uint4*)e_g;
         uint4* us4 = (uint4*)us;
         uint2* e82 = (uint2*)e8;
-        const int nchunk = Wpad * 4;  // multiple of 32: 4 lanes per word
-        for (int i = tau; i < nchunk; i += NT) {
+        const int nchunk = Wpad * 4;  // a multiple of 4 * NT: 4 lanes per word, 4 chunks per thread in flight
+        constexpr int U = 4;
+        for (int i0 = tau; i0 < nchunk; i0 += U * NT) {
+          uint4 c4s[U], e4s[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {  // all loads of the group first
+              const int i = i0 + u * NT;
+              c4s[u] = e4s[u] = make_uint4(0, 0, 0, 0);
+              if ((i >> 2) < W) {
+                  c4s[u] = cp4[i];
+                  e4s[u] = ep4[i];
+              }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * NT;
             const int a = i >> 2;
             const uint32_t val = valid_mask(a, W, p.cols) >> (8 * (i & 3));
-            uint4 c4 = make_uint4(0, 0, 0, 0), e4 = make_uint4(0, 0, 0, 0);
-            if (a < W) {
-                c4 = cp4[i];
-                e4 = ep4[i];
-            }
+            const uint4 c4 = c4s[u], e4 = e4s[u];
             us4[i] = c4;
             const uint32_t cw[4] = {c4.x, c4.y, c4.z, c4.w}, ew[4] = {e4.x, e4.y, e4.z, e4.w};
             uint32_t e8w[2] = {0u, 0u};
@@ -1693,6 +1703,7 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
                 mine = min(mine, __shfl_xor_sync(0xFFFFFFFFu, mine, o));
             }
             if ((i & 3) == 0) wmin[a] = (uint32_t)minc | ((uint32_t)mine << 16);
+          }
         }
     }
     __syncthreads();
