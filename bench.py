@@ -277,13 +277,17 @@ def main():
     lib = N.load()
 
     # ---- solver for this rank
-    if batch > 1:
-        local_batch = src.shape[0]
+    # batches, and single matrices the plan gives to the register team engine,
+    # go through msq_launch (one kernel); larger single matrices through the
+    # row-band pipeline (pass 1 + carry scan + fix-up, NCCL between ranks)
+    use_solver = batch > 1 or (world == 1 and int(Solver(fmt, rows, cols).plan.engine) == 1)
+    if use_solver:
+        local_batch = src.shape[0] if batch > 1 else 1
         solver = Solver(fmt, rows, cols, batch=local_batch)
         band_solver = None
         cells_per_step_local = local_batch * rows * cols
         cells_total = batch * rows * cols
-        bytes_per_cell = 1.0
+        bytes_per_cell = 0.125 if fmt == N.FMT_BITS else 1.0
     else:
         local_rows = src.shape[0]
         if world > 1:
@@ -308,7 +312,7 @@ def main():
     def step(instrument=False):
         if flush is not None:
             flush.fill_(1)
-        if batch > 1:
+        if use_solver:
             if instrument:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
@@ -345,7 +349,7 @@ def main():
         return 0
 
     def result():
-        if batch > 1:
+        if use_solver:
             return solver.result()
         return [band_solver.result()]
 
@@ -359,7 +363,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    launches_before = be.launches if batch == 1 else 0
+    launches_before = be.launches if not use_solver else 0
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -376,10 +380,10 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     ms_per_step = ms_total / args.steps
-    if batch == 1:
+    if not use_solver:
         gpu_launches = be.launches - launches_before
     else:
-        gpu_launches = args.steps  # one batched pass-1 launch per step
+        gpu_launches = args.steps * int(lib.msq_last_launch_count())  # msq_launch kernels per step
     value = cells_total / (ms_per_step * 1e-3) / 1e9
 
     # ---- dominant kernel duration (band pass), measured separately with events
@@ -393,7 +397,8 @@ def main():
     achieved = alg_bytes / (p1_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
-                "kernel": "msq::pass1_kernel (timed with the seed_climb_kernel before it)",
+                "kernel": ("msq::team_kernel" if use_solver and int(solver.plan.engine) == 1 else
+                           "msq::pass1_kernel (timed with the seed_climb_kernel before it)"),
                 "kernel_ms": round(p1_ms, 5),
                 "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": int(alg_bytes)}
@@ -472,8 +477,9 @@ def main():
             "dtype": "u32" if fmt == N.FMT_BITS else "u8", "data": "synthetic",
             "config": {"workload": spec["workload"], "rows": rows, "cols": cols, "batch": batch,
                        "format": "bits" if fmt == N.FMT_BITS else "u8",
-                       "parallelism": f"row-bands x{world}" if batch == 1 else f"matrices x{world}",
-                       "nbands_per_rank": int(be.plan.nbands) if batch == 1 else 1,
+                       "parallelism": (f"matrices x{world}" if batch > 1 else
+                                       "one team (register engine)" if use_solver else f"row-bands x{world}"),
+                       "nbands_per_rank": int(be.plan.nbands) if not use_solver else 1,
                        "l2": ("input > 126 MB L2, no flush" if flush is None
                               else "256 MiB L2 flush between steps"),
                        "answer": {"side": a0.side, "top": a0.top, "left": a0.left}},

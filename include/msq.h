@@ -83,7 +83,7 @@ typedef struct {
     int32_t grid;         /* pass-1 CTAs                                    */
     int32_t fix_threads;  /* fix-up CTA size                                */
     int32_t fix_wpt;      /* fix-up words per thread                        */
-    int32_t reserved;
+    int32_t engine;       /* 0: band engine; 1: register team engine (small matrices, no workspace) */
 } msq_plan;
 
 /* Build a plan.  nbands <= 0 picks a default (one band per SM, bands of

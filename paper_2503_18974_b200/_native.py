@@ -41,7 +41,7 @@ class MsqPlan(ctypes.Structure):
                 ("ws_bytes", ctypes.c_int64), ("team", ctypes.c_int32),
                 ("teams_per_cta", ctypes.c_int32), ("tile_rows_l", ctypes.c_int32),
                 ("tl", ctypes.c_int32), ("grid", ctypes.c_int32), ("fix_threads", ctypes.c_int32),
-                ("fix_wpt", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("fix_wpt", ctypes.c_int32), ("engine", ctypes.c_int32)]
 
 
 _lib = None

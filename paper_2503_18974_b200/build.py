@@ -5,6 +5,7 @@ dynamically so it shares torch's runtime instance when both are loaded.
 """
 from __future__ import annotations
 
+import glob
 import os
 import shutil
 import subprocess
@@ -16,7 +17,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libmsq.so")
 SOURCES = [os.path.join(CSRC, "msq.cu")]
-HEADERS = [os.path.join(CSRC, "msq_engine.cuh"), os.path.join(ROOT, "include", "msq.h")]
+HEADERS = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "msq.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

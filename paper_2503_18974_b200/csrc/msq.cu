@@ -7,11 +7,13 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 #include "msq.h"
 #include "msq_engine.cuh"
+#include "msq_team.cuh"
 
 namespace {
 
@@ -320,10 +322,100 @@ int solve_sync(int32_t fmt, int64_t batch, const void* d_src, int64_t rows, int6
 
 }  // namespace
 
-extern "C" {
 
-int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld, int32_t nbands,
-                  int32_t deterministic, msq_plan* plan) {
+namespace {
+int plan_band(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld, int32_t nbands,
+              int32_t deterministic, msq_plan* plan);
+
+// ---- register team engine (msq_team.cuh): small matrices, one team per matrix
+constexpr int kTeamThreads = 32;  // one warp per CTA: fine-grained spread over the SMs
+
+int team_planes(long long rows) { return rows <= 504 ? 9 : 11; }  // rows <= 2^PB - 8
+
+bool team_applies(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int32_t nbands) {
+    if (const char* f = getenv("MSQ_ENGINE")) {  // experiments: force one engine where both apply
+        if (f[0] == '0') return false;
+    }
+    const bool forced = getenv("MSQ_ENGINE") && getenv("MSQ_ENGINE")[0] == '1';
+    if (nbands > 0 || cols > 1024 || rows > 2040) return false;
+    (void)fmt;
+    // single matrices: one team is a serial row chain, faster than the band
+    // pipeline only while the matrix is short (measured: 512^2 123 vs 150 us,
+    // 1024^2 233 vs 207 us)
+    return batch > 1 || forced || rows <= 600;
+}
+
+template <int TEAM, int PB>
+cudaError_t launch_team_t(const msq_plan* pl, const void* d_src, msq_devresult* d_result, cudaStream_t st) {
+    const int mpb = (kTeamThreads / 32) * (32 / TEAM);
+    const int blocks = (int)ceil_div(pl->batch, mpb);
+    const bool u8 = pl->fmt == MSQ_FMT_U8;
+    const long long ld_bytes = u8 ? pl->ld : pl->ld * 4;
+    const long long mstride = pl->rows * ld_bytes;
+    const bool vec = u8 && pl->cols % 32 == 0 && ld_bytes % 16 == 0 && ((uintptr_t)d_src % 16) == 0;
+    const uint8_t* s = (const uint8_t*)d_src;
+    unsigned char* r = (unsigned char*)d_result;
+    const int R = (int)pl->rows, C = (int)pl->cols, W = pl->words, B = pl->batch;
+    if (!u8)
+        msq::team_kernel<TEAM, PB, false, false, 16><<<blocks, kTeamThreads, 0, st>>>(s, mstride, ld_bytes, R, C, W, B, r);
+    else if (vec)
+        msq::team_kernel<TEAM, PB, true, true, 8><<<blocks, kTeamThreads, 0, st>>>(s, mstride, ld_bytes, R, C, W, B, r);
+    else
+        msq::team_kernel<TEAM, PB, true, false, 8><<<blocks, kTeamThreads, 0, st>>>(s, mstride, ld_bytes, R, C, W, B, r);
+    return cudaGetLastError();
+}
+
+template <int PB>
+cudaError_t launch_team_pb(const msq_plan* pl, const void* d_src, msq_devresult* d_result, cudaStream_t st) {
+    int ts = 1;
+    while (ts < pl->words) ts *= 2;
+    switch (ts) {
+        case 1: return launch_team_t<1, PB>(pl, d_src, d_result, st);
+        case 2: return launch_team_t<2, PB>(pl, d_src, d_result, st);
+        case 4: return launch_team_t<4, PB>(pl, d_src, d_result, st);
+        case 8: return launch_team_t<8, PB>(pl, d_src, d_result, st);
+        case 16: return launch_team_t<16, PB>(pl, d_src, d_result, st);
+        case 32: return launch_team_t<32, PB>(pl, d_src, d_result, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_team(const msq_plan* pl, const void* d_src, msq_devresult* d_result, cudaStream_t st) {
+    return team_planes(pl->rows) == 9 ? launch_team_pb<9>(pl, d_src, d_result, st)
+                                      : launch_team_pb<11>(pl, d_src, d_result, st);
+}
+}  // namespace
+
+extern "C" int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld, int32_t nbands,
+                             int32_t deterministic, msq_plan* plan) {
+    if (!plan) return MSQ_EINVAL;
+    msq_plan p{};
+    int rc = plan_band(fmt, batch, rows, cols, ld, nbands, deterministic, &p);
+    const bool shape_ok = (fmt == MSQ_FMT_U8 || fmt == MSQ_FMT_BITS) && batch >= 1 && rows >= 1 && cols >= 1 &&
+                          (fmt == MSQ_FMT_U8 ? ld >= cols : ld >= (cols + 31) / 32);
+    if (shape_ok && team_applies(fmt, batch, rows, cols, nbands)) {
+        if (rc != MSQ_OK) {  // the band plan does not fit: the team engine needs no workspace
+            p = msq_plan{};
+            p.fmt = fmt;
+            p.batch = batch;
+            p.rows = rows;
+            p.cols = cols;
+            p.ld = ld;
+            p.words = (int32_t)ceil_div(cols, 32);
+            p.nbands = 1;
+            p.deterministic = deterministic ? 1 : 0;
+        }
+        p.engine = 1;  // the band fields stay valid for the rank (row-band) entry points
+        *plan = p;
+        return MSQ_OK;
+    }
+    if (rc == MSQ_OK) *plan = p;
+    return rc;
+}
+
+namespace {
+int plan_band(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld, int32_t nbands,
+              int32_t deterministic, msq_plan* plan) {
     if (!plan || (fmt != MSQ_FMT_U8 && fmt != MSQ_FMT_BITS) || batch < 1) return MSQ_EINVAL;
     if (rows < 1 || cols < 1 || rows >= (1ll << 21) || cols > 65536) return MSQ_EINVAL;
     const int64_t words = ceil_div(cols, 32);
@@ -428,7 +520,22 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
     return MSQ_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
 int msq_launch(const msq_plan* pl, const void* d_src, void* d_ws, msq_devresult* d_result, void* stream) {
+    if (pl && pl->engine == 1) {  // register team engine: one launch, no workspace
+        if (!d_src || !d_result) return MSQ_EINVAL;
+        cudaStream_t st = (cudaStream_t)stream;
+        g_last_launches = 0;
+        if (cudaMemsetAsync(d_result, 0, sizeof(msq_devresult) * (size_t)pl->batch, st) != cudaSuccess)
+            return MSQ_ECUDA;
+        cudaError_t e = launch_team(pl, d_src, d_result, st);
+        if (e != cudaSuccess) return cuda_status(e);
+        g_last_launches = 1;
+        return MSQ_OK;
+    }
     if (!pl || !d_src || !d_result || (!d_ws && pl->ws_bytes > 0)) return MSQ_EINVAL;
     if (pl->nstage > 0 && ((uintptr_t)d_src % 16) != 0) {
         msq_plan q = *pl;  // misaligned base: fall back to direct loads
@@ -518,7 +625,7 @@ int msq_solve_bits_host(const uint32_t* h_words, int64_t rows, int64_t cols, int
 }
 
 int msq_rank_pass1(const msq_plan* pl, const void* d_src, void* d_ws, msq_devresult* d_result, void* stream) {
-    if (!pl || pl->batch != 1 || !d_src || !d_ws || !d_result) return MSQ_EINVAL;
+    if (!pl || pl->batch != 1 || !d_src || !d_ws || !d_result || pl->ws_bytes <= 0) return MSQ_EINVAL;
     if (pl->nstage > 0 && ((uintptr_t)d_src % 16) != 0) {
         msq_plan q = *pl;
         q.nstage = 0;

@@ -283,3 +283,58 @@ def test_seed_lower_bound_keeps_ties_exact(torch, fmt):
         else:
             got = freq_square_bits(grid.pack_bits(a), cols)
         _same(got, want)
+
+
+@pytest.fixture
+def team_engine(monkeypatch):
+    """Force the register team engine (msq_team.cuh) for single matrices too."""
+    monkeypatch.setenv("MSQ_ENGINE", "1")
+
+
+def test_team_engine_single_matrices(torch, team_engine):
+    """Team engine on one matrix at a time: odd widths, strides, both formats."""
+    rng = np.random.default_rng(31)
+    for it in range(400):
+        rows = int(rng.integers(1, 1200))
+        cols = int(rng.integers(1, 1025)) if it % 4 else int(rng.choice([32, 64, 256, 512, 1024]))
+        p = float(rng.choice([0.3, 0.7, 0.9, 0.97, 0.995, 1.0]))
+        a = _planted(rng, rows, cols, p, int(rng.integers(0, 200)))
+        want = oracle.freq(a)
+        pad = int(rng.choice([0, 0, 16, 5]))
+        wide = np.zeros((rows, cols + pad), np.uint8)
+        wide[:, :cols] = a
+        s = Solver(N.FMT_U8, rows, cols, ld=cols + pad)
+        assert int(s.plan.engine) == 1
+        _same(s.solve(torch.from_numpy(wide).cuda())[0], want)
+        if it % 2 == 0:
+            w = grid.pack_bits(a)
+            sb = Solver(N.FMT_BITS, rows, cols, ld=w.shape[1])
+            assert int(sb.plan.engine) == 1
+            _same(sb.solve(torch.from_numpy(w.view(np.int32)).cuda())[0], want)
+
+
+def test_team_engine_batches(torch):
+    """Batched solves (team engine by default) for every team width and both plane counts."""
+    rng = np.random.default_rng(32)
+    for rows, cols in ((7, 3), (40, 33), (100, 64), (256, 256), (300, 130), (511, 512), (600, 1000),
+                       (1500, 96), (2040, 40)):
+        batch = int(rng.integers(2, 70))
+        p = float(rng.choice([0.5, 0.9, 0.99]))
+        cells = np.stack([_planted(rng, rows, cols, p, int(rng.integers(0, min(rows, cols) + 1)))
+                          for _ in range(batch)])
+        got = solve_batch(cells)
+        for g_, w_ in zip(got, oracle.freq_batch(cells)):
+            _same(g_, w_)
+        words = (cols + 31) // 32
+        wb = np.stack([grid.pack_bits(c) for c in cells]).reshape(batch, rows, words)
+        s = Solver(N.FMT_BITS, rows, cols, batch=batch)
+        assert int(s.plan.engine) == 1
+        for g_, w_ in zip(s.solve(torch.from_numpy(wb.view(np.int32)).cuda()), oracle.freq_batch(cells)):
+            _same(g_, w_)
+
+
+def test_team_engine_invalid_cells(torch):
+    cells = np.ones((5, 64, 64), np.uint8)
+    cells[3, 10, 7] = 3
+    with pytest.raises(ValueError):
+        solve_batch(cells)
