@@ -14,6 +14,7 @@
 #include "msq.h"
 #include "msq_engine.cuh"
 #include "msq_team.cuh"
+#include "msq_strip.cuh"
 
 namespace {
 
@@ -42,8 +43,27 @@ int num_sms() {
 }
 
 struct WsLayout {
-    size_t band_keys, fix_keys, zb, e, ao, carry, total;
+    size_t band_keys, fix_keys, zb, e, ao, carry, zw, redo, total;
 };
+
+// ---- strip pass (msq_strip.cuh): bit-packed single matrices, several bands
+int strip_warps(const msq_plan* p) { return (int)ceil_div(p->words, msq::STRIP_STRIDE); }
+int strip_slots(const msq_plan* p) {
+    const long long slot = (long long)msq::STRIP_TR * p->row_stage_bytes;
+    return (int)std::min<long long>(msq::STRIP_MAXSLOTS, (kSmemMax - 256) / slot);
+}
+int strip_smem(const msq_plan* p) {
+    return strip_slots(p) * msq::STRIP_TR * p->row_stage_bytes + 2 * msq::STRIP_MAXSLOTS * 8 + 64;
+}
+bool strip_applies(const msq_plan* p) {
+    if (const char* f = getenv("MSQ_STRIP"))  // experiments: MSQ_STRIP=0 disables
+        if (f[0] == '0') return false;
+    const long long ld_bytes = p->ld * 4;
+    return p->fmt == MSQ_FMT_BITS && p->batch == 1 && p->nbands > 1 && !p->deterministic &&
+           p->words >= 2 * msq::STRIP_WORDS && p->words % 4 == 0 && p->row_stage_bytes % 16 == 0 &&
+           ld_bytes % 16 == 0 && (strip_warps(p) + 1) * 32 <= 640 && strip_slots(p) >= 2 &&
+           ceil_div(p->rows, p->nbands) <= 65535;
+}
 
 WsLayout ws_layout(const msq_plan* p) {
     WsLayout L{};
@@ -63,6 +83,9 @@ WsLayout ws_layout(const msq_plan* p) {
     L.e = take(summaries ? nb * cols_pad * 2 : 0);
     L.ao = take(summaries ? nb * (size_t)p->words * 4 : 0);
     L.carry = take(summaries ? nb * cols_pad * 2 : 0);
+    const bool strip = strip_applies(p);
+    L.zw = take(strip ? nb * (size_t)strip_warps(p) * msq::STRIP_WORDS * 32 * 2 : 0);
+    L.redo = take(strip ? nb * 4 : 0);
     L.total = off;
     return L;
 }
@@ -137,6 +160,54 @@ cudaError_t launch_pass1(const msq_plan* pl, const msq::Pass1Params& prm, cudaSt
     MSQ_P1(4, false, false, false)
 #undef MSQ_P1
     return cudaErrorInvalidValue;
+}
+
+// band passes: the strip pass (when it applies) and pass1_kernel for the bands it left
+cudaError_t launch_band_pass(const msq_plan* pl, msq::Pass1Params prm, void* ws, const void* src, cudaStream_t st,
+                             int* nlaunch) {
+    *nlaunch = 1;
+    if (prm.write_summaries && strip_applies(pl) && ((uintptr_t)src % 16) == 0) {
+        WsLayout L = ws_layout(pl);
+        uint8_t* w = (uint8_t*)ws;
+        msq::StripParams sp{};
+        sp.src = (const uint8_t*)src;
+        sp.ld_bytes = pl->ld * 4;
+        sp.rows = (int)pl->rows;
+        sp.cols = (int)pl->cols;
+        sp.W = pl->words;
+        sp.nbands = pl->nbands;
+        sp.cols_pad = pl->words * 32;
+        sp.row_base = pl->row_base;
+        sp.nslots = strip_slots(pl);
+        sp.row_bytes = pl->row_stage_bytes;
+        sp.nwarps = strip_warps(pl);
+        sp.zw = (uint16_t*)(w + L.zw);
+        sp.zb = prm.zb;
+        sp.e_out = prm.e_out;
+        sp.ao_out = prm.ao_out;
+        sp.band_keys = prm.band_keys;
+        sp.results = prm.results;
+        sp.redo = (int*)(w + L.redo);
+        static bool attr_set[64] = {false};
+        cudaError_t e = set_smem_attr(msq::strip_kernel, attr_set);
+        if (e != cudaSuccess) return e;
+        msq::strip_kernel<<<pl->nbands, (sp.nwarps + 1) * 32, strip_smem(pl), st>>>(sp);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        prm.redo = sp.redo;
+        *nlaunch = 2;
+    }
+    return launch_pass1(pl, prm, st);
+}
+
+// tests only: MSQ_TEST_FLOOR=k presets the shared best side to k (a lower
+// bound the caller vouches for, k <= answer), as if the seed had found it
+cudaError_t apply_test_floor(const msq_plan* pl, msq_devresult* d_result, cudaStream_t st) {
+    const char* f = getenv("MSQ_TEST_FLOOR");
+    if (!f || pl->batch != 1) return cudaSuccess;
+    const int32_t v = atoi(f);
+    if (v <= 0) return cudaSuccess;
+    return cudaMemcpyAsync(&d_result->best_side, &v, sizeof(v), cudaMemcpyHostToDevice, st);
 }
 
 cudaError_t launch_fixup(const msq_plan* pl, const msq::FixParams& prm, int nblocks, cudaStream_t st) {
@@ -547,19 +618,22 @@ int msq_launch(const msq_plan* pl, const void* d_src, void* d_ws, msq_devresult*
     if (cudaMemsetAsync(d_result, 0, sizeof(msq_devresult) * (size_t)pl->batch, st) != cudaSuccess)
         return MSQ_ECUDA;
     const bool multi = pl->batch == 1 && pl->nbands > 1;
-    cudaError_t e = launch_seed(pl, d_src, d_result, st);
+    cudaError_t e = apply_test_floor(pl, d_result, st);
+    if (e != cudaSuccess) return cuda_status(e);
+    e = launch_seed(pl, d_src, d_result, st);
     if (e != cudaSuccess) return cuda_status(e);
     msq::Pass1Params p1 = make_pass1(pl, d_src, d_ws, d_result, multi);
-    e = launch_pass1(pl, p1, st);
+    int nl = 1;
+    e = launch_band_pass(pl, p1, d_ws, d_src, st, &nl);
     if (e != cudaSuccess) return cuda_status(e);
-    g_last_launches = 1 + seeds_launched(pl);
+    g_last_launches = nl + seeds_launched(pl);
     if (multi) {
         e = launch_carry(pl, d_ws, nullptr, st);
         if (e != cudaSuccess) return cuda_status(e);
         msq::FixParams f = make_fix(pl, d_ws, nullptr, d_result);
         e = launch_fixup(pl, f, pl->nbands - 1, st);
         if (e != cudaSuccess) return cuda_status(e);
-        g_last_launches = 3 + seeds_launched(pl);
+        g_last_launches = nl + 2 + seeds_launched(pl);
     }
     return MSQ_OK;
 }
@@ -633,11 +707,15 @@ int msq_rank_pass1(const msq_plan* pl, const void* d_src, void* d_ws, msq_devres
     }
     cudaStream_t st = (cudaStream_t)stream;
     if (cudaMemsetAsync(d_result, 0, sizeof(msq_devresult), st) != cudaSuccess) return MSQ_ECUDA;
-    cudaError_t e = launch_seed(pl, d_src, d_result, st);
+    cudaError_t e = apply_test_floor(pl, d_result, st);
+    if (e != cudaSuccess) return cuda_status(e);
+    e = launch_seed(pl, d_src, d_result, st);
     if (e != cudaSuccess) return cuda_status(e);
     msq::Pass1Params p1 = make_pass1(pl, d_src, d_ws, d_result, true);
-    g_last_launches = 1 + seeds_launched(pl);
-    return cuda_status(launch_pass1(pl, p1, st));
+    int nl = 1;
+    e = launch_band_pass(pl, p1, d_ws, d_src, st, &nl);
+    g_last_launches = nl + seeds_launched(pl);
+    return cuda_status(e);
 }
 
 int msq_rank_summary(const msq_plan* pl, const void* d_ws, uint32_t* d_summary, void* stream) {

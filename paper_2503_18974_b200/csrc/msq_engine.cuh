@@ -335,6 +335,7 @@ struct Pass1Params {
     unsigned long long* band_keys;
     unsigned char* results;
     unsigned long long* prof;  // optional [units][16] phase-cycle counters (thread 0)
+    const int* redo;           // optional [nbands]: bands the strip pass left over (0 = done)
 };
 
 struct FixParams {
@@ -907,6 +908,7 @@ __device__ __forceinline__ uint32_t tile_zero_flags_bits(uint32_t ring_s, int rs
 template <int WPT, bool U8, bool TMA, bool SUB>
 __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     extern __shared__ __align__(128) uint8_t smem[];
+    if (!SUB && p.redo && ld_volatile(p.redo + blockIdx.x) == 0) return;  // done by strip_kernel
     const int NT = p.team;
     const int tid = threadIdx.x;
     const int lane = tid & 31;

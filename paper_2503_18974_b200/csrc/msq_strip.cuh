@@ -1,0 +1,388 @@
+// msq_strip.cuh -- barrier-free band pass for bit-packed matrices (sm_100a).
+//
+// Same band outputs as pass1_kernel (band key, first-zero depths e, bottom
+// runs b, all-ones masks), for bit-packed bands whose threshold starts (from
+// the lower-bound seed or the shared best side) in [STRIP_TMIN, STRIP_TMAX].
+//
+// Why it is exact without any CTA-wide synchronisation: let g_w(r) be the
+// largest side of a square whose bottom-right cell lies in row r and in the
+// column strip owned by warp w.  A k-square ending at (r, c) contains a
+// (k-1)-square ending at (r-1, c), so g_w(r) <= g_w(r-1) + 1 (SURVEY P2 per
+// strip) and Algorithm 1 (squares.py:84-103) run on the strip alone -- one
+// test per row at t = best_w + 1 -- finds max_r g_w(r) and the first row and
+// leftmost end where it occurs.  The band answer is the max of the strips'
+// keys.  Thresholds may jump to a side M found elsewhere (tested as a tie, at
+// t = M), exactly as the band engine shares its best side.
+//
+// Layout: warp w reads the window of 128 words [120w - 8, 120w + 120) of each
+// row (4 words per lane, one 16-byte smem load), owns the 120 words from
+// 120w on, and uses the 8 words to the left as a halo: every window of
+// t <= STRIP_TMAX columns ending in its own words lies in the window.  Rows
+// arrive through a TMA ring of 8-row slots (one bulk copy, one full and one
+// empty mbarrier per slot); a producer warp refills a slot once every
+// consumer warp released it.  No __syncthreads in the row loop.
+//
+// Per 8-row tile and word (threshold t >= 96, so any t-run of eligible
+// columns contains >= Lmin = ceil((t-62)/32) whole "F" words, i.e. words with
+// no zero in the last t rows -- the band engine's mode L):
+//   zm  = rows of the tile with a zero in the word (8 flags)
+//   F rows = [Z + t - rho0, first zero in the tile)   (Z = last zero row before)
+//   a shuffle brings the left lane's 4 words; runs of Lmin F words are found
+//   with byte-wise ANDs over the 8 row masks at once.
+// Runs (rare) are checked exactly from per-column last-zero rows that each
+// warp keeps for its own window in global scratch (written on zero events).
+#pragma once
+
+namespace msq {
+
+constexpr int STRIP_WORDS = 128;  // words in a warp's window
+constexpr int STRIP_HALO = 8;     // of which the first 8 are the halo
+constexpr int STRIP_STRIDE = STRIP_WORDS - STRIP_HALO;
+constexpr int STRIP_TR = 8;       // rows per tile (= per ring slot)
+constexpr int STRIP_TMIN = 96;    // word-level filter valid (runs contain >= 2 whole words)
+constexpr int STRIP_TMAX = 222;   // Lmin <= 5 (one neighbour lane) and t - 1 <= 32 * 7 (halo)
+constexpr int STRIP_MAXSLOTS = 4;
+
+struct StripParams {
+    const uint8_t* src;
+    long long ld_bytes;
+    int rows, cols, W, nbands, cols_pad;
+    long long row_base;
+    int nslots, row_bytes, nwarps;
+    uint16_t* zw;  // [nbands][nwarps][128*32] last-zero rows of each warp's window
+    uint16_t* zb;  // [nbands][cols_pad] bottom runs (band output)
+    uint16_t* e_out;
+    uint32_t* ao_out;
+    unsigned long long* band_keys;
+    unsigned char* results;
+    int* redo;  // [nbands]: 1 = band left to pass1_kernel (threshold outside the strip range)
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ int strip_lmin(int t) { return (t - 62 + 31) / 32; }
+
+__global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int band = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r0 = band_row0(p.rows, p.nbands, band);
+    const int H = band_row0(p.rows, p.nbands, band + 1) - r0;
+    const int ntiles = (H + STRIP_TR - 1) / STRIP_TR;
+    const int slot_bytes = STRIP_TR * p.row_bytes;
+    uint8_t* ring = smem;
+    uint64_t* full = (uint64_t*)(smem + (size_t)p.nslots * slot_bytes);
+    uint64_t* empty = full + STRIP_MAXSLOTS;
+    int* sh = (int*)(empty + STRIP_MAXSLOTS);  // [0] start threshold, [1] CTA best, [2] abort
+    unsigned long long* skey = (unsigned long long*)(sh + 4);
+    unsigned char* result = p.results;
+
+    if (tid == 0) {
+        const int t0 = max(1, ld_volatile(res_best(result)));
+        sh[0] = t0;
+        sh[1] = t0;
+        sh[2] = 0;
+        *skey = 0ull;
+        const bool ok = t0 >= STRIP_TMIN && t0 <= STRIP_TMAX;
+        p.redo[band] = ok ? 0 : 1;
+        for (int s = 0; s < p.nslots; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], p.nwarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int t0 = sh[0];
+    if (t0 < STRIP_TMIN || t0 > STRIP_TMAX) return;  // pass1_kernel redoes this band
+
+    // ------------------------------------------------------------ producer
+    if (warp == p.nwarps) {
+        if (lane == 0) {
+            const uint64_t pol = l2_evict_first_policy();
+            const uint8_t* bsrc = p.src + (size_t)r0 * p.ld_bytes;
+            const bool contiguous = p.ld_bytes == (long long)p.row_bytes;
+            for (int q = 0; q < ntiles; ++q) {
+                const int s = q % p.nslots;
+                if (q >= p.nslots) mbar_wait(&empty[s], (uint32_t)((q / p.nslots - 1) & 1));
+                const int n = min(STRIP_TR, H - q * STRIP_TR);
+                mbar_expect_tx(&full[s], (uint32_t)(n * p.row_bytes));
+                uint8_t* dst = ring + (size_t)s * slot_bytes;
+                const uint8_t* srow = bsrc + (size_t)q * STRIP_TR * p.ld_bytes;
+                if (contiguous) {
+                    tma_row(dst, srow, (uint32_t)(n * p.row_bytes), &full[s], pol);
+                } else {
+                    for (int b = 0; b < n; ++b)
+                        tma_row(dst + (size_t)b * p.row_bytes, srow + (size_t)b * p.ld_bytes, (uint32_t)p.row_bytes,
+                                &full[s], pol);
+                }
+            }
+        }
+        return;
+    }
+
+    // ------------------------------------------------------------ consumers
+    const int base_word = STRIP_STRIDE * warp - STRIP_HALO;
+    const int i0 = 4 * lane;  // first window index of this lane
+    uint32_t VAL[4], NZ[4];
+    int ZW[4];
+    uint32_t fullk = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int a = base_word + i0 + k;
+        VAL[k] = (a >= 0 && a < p.W) ? valid_mask(a, p.W, p.cols) : 0u;
+        NZ[k] = VAL[k];
+        ZW[k] = 0;
+        fullk |= (VAL[k] == 0xFFFFFFFFu ? 1u : 0u) << k;
+    }
+    uint32_t own_mask = 0;  // words of this lane the warp owns (not halo, inside the matrix)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) own_mask |= (i0 + k >= STRIP_HALO && VAL[k] != 0u ? 1u : 0u) << k;
+    // smem byte offset of the lane's 4 words inside a row (clamped for words outside the row)
+    const int a_ld = min(max(base_word + i0, 0), p.W - 4);
+    const uint32_t ring_s = smem_addr(ring) + (uint32_t)(a_ld * 4);
+    uint16_t* zwin = p.zw + ((size_t)band * p.nwarps + warp) * (STRIP_WORDS * 32);
+    const size_t sum_base = (size_t)band * p.cols_pad;
+
+    int t = t0;
+    int lmin = strip_lmin(t);
+    unsigned long long key = 0ull;
+    bool aborted = false;
+
+    const uint32_t rb_bytes = (uint32_t)p.row_bytes;
+    int s = 0;          // ring slot of tile q
+    uint32_t par = 0u;  // its full-barrier phase parity
+    for (int q = 0; q < ntiles; ++q, s = (s + 1 == p.nslots) ? 0 : s + 1, par ^= (s == 0) ? 1u : 0u) {
+        const int row0 = q * STRIP_TR;
+        const int nrows = min(STRIP_TR, H - row0);
+        const int rho0 = row0 + 1;
+        const uint32_t slot_s = ring_s + (uint32_t)(s * slot_bytes);
+        mbar_wait(&full[s], par);
+        if (aborted) {  // keep the ring moving; pass1_kernel redoes the band
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            continue;
+        }
+        // ---- zero rows of each word over the tile
+        // N: nibble b = which of the 4 words have a zero in tile row b
+        // (all 8 rows of the slot are read; rows past the band end are masked off)
+        uint32_t N = 0u;
+#pragma unroll
+        for (int b = 0; b < STRIP_TR; ++b) {
+            uint32_t w[4];
+            lds_words<4>(slot_s + (uint32_t)b * rb_bytes, w);
+            uint32_t nb = 0u;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) nb |= ((~w[k] & VAL[k]) != 0u ? 1u : 0u) << k;
+            N |= nb << (4 * b);
+        }
+        if (nrows < STRIP_TR) N &= (1u << (4 * nrows)) - 1u;
+        // zm[k]: rows of word k with a zero, spread 4 bits apart (bit 4b)
+        uint32_t zm[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) zm[k] = (N >> k) & 0x11111111u;
+        // ---- F rows per word at t (before this tile's zeros move Z)
+        uint32_t X = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int hi = zm[k] ? (__ffs(zm[k]) - 1) >> 2 : nrows;
+            const int lo = max(0, ZW[k] + t - rho0);
+            const uint32_t fr = ((fullk >> k) & 1u) && lo < hi ? ((1u << hi) - 1u) & ~((1u << lo) - 1u) : 0u;
+            X |= fr << (8 * k);
+        }
+        // runs of lmin F words ending in this lane's words: bytes = row masks of
+        // the 8 words (left lane's 4, then ours); AND over lmin consecutive bytes
+        const uint32_t PX = __shfl_up_sync(0xFFFFFFFFu, X, 1);
+        const unsigned long long S = (unsigned long long)(lane ? PX : 0u) | ((unsigned long long)X << 32);
+        unsigned long long A = S;
+        for (int i = 1; i < lmin; ++i) A &= S << (8 * i);
+        uint32_t cm = (uint32_t)(A >> 32);
+        cm |= cm >> 16;
+        cm |= cm >> 8;
+        const uint32_t crows = __reduce_or_sync(0xFFFFFFFFu, cm & 0xFFu);
+
+        if (crows) {
+            // ---- rare path: rows with a candidate run, in order, at the running t.
+            // Column state is the pre-tile state (zwin, NZ) plus the tile's own
+            // rows up to the tested one, read back from the ring slot.
+            for (int b = 0; b < nrows; ++b) {
+                if (!((crows >> b) & 1u)) continue;  // warp-uniform
+                const int rho = rho0 + b;
+                uint32_t nib = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const bool f = ((fullk >> k) & 1u) && !(zm[k] & ((2u << (4 * b)) - 1u)) && ZW[k] + t <= rho;
+                    nib |= (f ? 1u : 0u) << k;
+                }
+                // F words reaching the top of each lane's nibble (segmented scan)
+                int R = __clz(~(nib << 28));
+                bool allf = nib == 0xFu;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int o = __shfl_up_sync(0xFFFFFFFFu, R | (allf ? 0x10000 : 0), d);
+                    if (lane >= d && allf) {
+                        R += o & 0xFFFF;
+                        allf = (o >> 16) & 1;
+                    }
+                }
+                int cin = __shfl_up_sync(0xFFFFFFFFu, R, 1);
+                if (lane == 0) cin = 0;
+                const uint32_t nb0 = __shfl_down_sync(0xFFFFFFFFu, nib & 1u, 1);
+                const uint32_t ends = nib & ~((nib >> 1) | ((lane < 31 ? nb0 : 0u) << 3));
+                int cand0 = -1, cand1 = -1;  // at most two runs end in a nibble
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if ((ends >> k) & 1u) {
+                        const int ones = __clz(~(nib << (31 - k)));
+                        const int L = ones == k + 1 ? ones + cin : ones;
+                        if (L >= lmin) {
+                            const int c = ((i0 + k - L + 1) << 8) | L;
+                            if (cand0 < 0) cand0 = c; else cand1 = c;
+                        }
+                    }
+                }
+                // eligibility of column `lane` of window word i at row rho
+                auto elig = [&](int i) -> uint32_t {
+                    if (i < 0 || i >= STRIP_WORDS) return 0u;
+                    const int kk = i & 3;
+                    const uint32_t nzs = kk == 0 ? NZ[0] : kk == 1 ? NZ[1] : kk == 2 ? NZ[2] : NZ[3];
+                    const uint32_t vls = kk == 0 ? VAL[0] : kk == 1 ? VAL[1] : kk == 2 ? VAL[2] : VAL[3];
+                    const uint32_t nzw = __shfl_sync(0xFFFFFFFFu, nzs, i >> 2);
+                    const uint32_t vlw = __shfl_sync(0xFFFFFFFFu, vls, i >> 2);
+                    const int zr = zwin[i * 32 + lane];
+                    // a zero in the tile up to this row: never eligible (t > 8)
+                    const int aw = min(max(base_word + i, 0), p.W - 1);
+                    const uint32_t wsl = smem_addr(ring) + (uint32_t)(s * slot_bytes + aw * 4);
+                    uint32_t tz = 0u;
+                    for (int bb = 0; bb <= b; ++bb) {
+                        uint32_t w1[1];
+                        lds_words<1>(wsl + (uint32_t)(bb * p.row_bytes), w1);
+                        tz |= ~w1[0];
+                    }
+                    const bool e = !((tz >> lane) & 1u) && (((nzw >> lane) & 1u) ? rho >= t : zr + t <= rho);
+                    return __ballot_sync(0xFFFFFFFFu, e) & vlw;
+                };
+                int beste = 0x7FFFFFFF;
+#pragma unroll
+                for (int ci = 0; ci < 2; ++ci) {
+                    const int mine = ci ? cand1 : cand0;
+                    unsigned bal = __ballot_sync(0xFFFFFFFFu, mine >= 0);
+                    while (bal) {
+                        const int l = __ffs(bal) - 1;
+                        bal &= bal - 1;
+                        const int c = __shfl_sync(0xFFFFFFFFu, mine, l);
+                        const int a0 = c >> 8, L = c & 0xFF, a1 = a0 + L;
+                        const uint32_t el = elig(a0 - 1), er = elig(a1);
+                        const int suf = __clz(~el);
+                        const int pre = er == 0xFFFFFFFFu ? 32 : __ffs(~er) - 1;
+                        if (suf + 32 * L + pre >= t) {
+                            const int st = 32 * a0 - suf;
+                            const int e = max(st + t - 1, 32 * STRIP_HALO);
+                            if (e <= 32 * a1 + pre - 1) beste = min(beste, e);
+                        }
+                    }
+                }
+                if (beste != 0x7FFFFFFF) {  // warp-uniform: raise at this row
+                    key = pack_key(t, p.row_base + r0 + rho - 1, (long long)32 * base_word + beste);
+                    ++t;
+                    if (t > STRIP_TMAX) aborted = true;
+                    lmin = strip_lmin(t);
+                    if (lane == 0) {
+                        atomicMax(&sh[1], t - 1);
+                        atomicMax(res_best(result), t - 1);
+                    }
+                }
+            }
+        }
+        // ---- zero events, one (word, row) event or one zero bit per lane and
+        // step, so the lanes' events share the steps: per-column last-zero rows
+        // of the window, first zeros (e) of own columns, never-zeroed masks
+        {
+            uint32_t EV = N;  // bit 4b + k: word k, row b (rows in order per word)
+            uint32_t cz = 0u, cn = 0u;
+            int cidx = 0, crho = 0;
+            while (__any_sync(0xFFFFFFFFu, (EV | cz) != 0u)) {
+                if (cz == 0u && EV != 0u) {
+                    const int bit = __ffs(EV) - 1;
+                    EV &= EV - 1;
+                    const int k = bit & 3, b = bit >> 2;
+                    uint32_t w1[1];
+                    lds_words<1>(slot_s + (uint32_t)(b * p.row_bytes + 4 * k), w1);
+                    const uint32_t vk = k == 0 ? VAL[0] : k == 1 ? VAL[1] : k == 2 ? VAL[2] : VAL[3];
+                    const uint32_t nk = k == 0 ? NZ[0] : k == 1 ? NZ[1] : k == 2 ? NZ[2] : NZ[3];
+                    cz = ~w1[0] & vk;
+                    cn = ((own_mask >> k) & 1u) ? (nk & cz) : 0u;
+                    const uint32_t nn = nk & ~cz;
+                    NZ[0] = k == 0 ? nn : NZ[0];
+                    NZ[1] = k == 1 ? nn : NZ[1];
+                    NZ[2] = k == 2 ? nn : NZ[2];
+                    NZ[3] = k == 3 ? nn : NZ[3];
+                    cidx = i0 + k;
+                    crho = rho0 + b;
+                }
+                if (cz) {
+                    const int j = __ffs(cz) - 1;
+                    cz &= cz - 1;
+                    zwin[cidx * 32 + j] = (uint16_t)crho;
+                    if ((cn >> j) & 1u) p.e_out[sum_base + (size_t)(base_word + cidx) * 32 + j] = (uint16_t)(crho - 1);
+                }
+            }
+        }
+        // ---- last zero row per word, release the slot
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (zm[k]) ZW[k] = rho0 + ((31 - __clz(zm[k])) >> 2);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        // shared best side (ties): the CTA's every tile, the grid's every 8 tiles
+        int g = ld_volatile(&sh[1]);
+        if ((q & 7) == 7) g = max(g, ld_volatile(res_best(result)));
+        if (g > t) {
+            t = g;
+            if (t > STRIP_TMAX) aborted = true;
+            lmin = strip_lmin(t);
+        }
+    }
+    if (aborted && lane == 0) {
+        p.redo[band] = 1;
+        atomicExch(&sh[2], 1);
+    }
+
+    // ------------------------------------------------------------ band outputs (own words)
+    // word by word, lanes = columns: coalesced bottom runs, e = H for never-zeroed columns
+    if (!aborted) {
+        // 8 words per step: their last-zero rows are loaded (L2) before any is used
+        for (int i8 = STRIP_HALO; i8 < STRIP_WORDS; i8 += 8) {
+            int zr[8];
+            uint32_t nzw[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i8 + u;
+                const int kk = i & 3;
+                const uint32_t nzs = kk == 0 ? NZ[0] : kk == 1 ? NZ[1] : kk == 2 ? NZ[2] : NZ[3];
+                nzw[u] = __shfl_sync(0xFFFFFFFFu, nzs, i >> 2);
+                zr[u] = (base_word + i < p.W && !((nzw[u] >> lane) & 1u)) ? (int)zwin[i * 32 + lane] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int a = base_word + i8 + u;
+                if (a < p.W) {
+                    const size_t cb = sum_base + (size_t)a * 32;
+                    p.zb[cb + lane] = (uint16_t)(H - zr[u]);
+                    if ((nzw[u] >> lane) & 1u) p.e_out[cb + lane] = (uint16_t)H;
+                    if (lane == 0) p.ao_out[(size_t)band * p.W + a] = nzw[u];
+                }
+            }
+        }
+    }
+    if (lane == 0 && key && !aborted) atomicMax(skey, key);
+    asm volatile("bar.sync 1, %0;" ::"r"(p.nwarps * 32) : "memory");  // consumers only
+    if (tid == 0 && !ld_volatile(&sh[2])) {
+        const unsigned long long k = *skey;
+        p.band_keys[band] = k;
+        if (k) atomicMax(res_key1(result), k);
+    }
+}
+
+}  // namespace msq

@@ -338,3 +338,30 @@ def test_team_engine_invalid_cells(torch):
     cells[3, 10, 7] = 3
     with pytest.raises(ValueError):
         solve_batch(cells)
+
+
+@pytest.mark.parametrize("floor", [96, 120, 150])
+def test_strip_pass_bits(torch, monkeypatch, floor):
+    """Strip band pass (msq_strip.cuh): bit-packed, several bands, start threshold in its range.
+
+    MSQ_TEST_FLOOR presets the shared best side (a lower bound <= the answer, as
+    the seed provides on large inputs) so the strip pass runs on moderate sizes;
+    planted sides above 222 exercise its hand-back to pass1_kernel."""
+    monkeypatch.setenv("MSQ_TEST_FLOOR", str(floor))
+    rng = np.random.default_rng(40 + floor)
+    for it in range(14):
+        rows = int(rng.integers(300, 2500))
+        cols = int(rng.choice([8192, 9000, 16384, 40000, 65536]))
+        p = float(rng.choice([0.99, 0.997, 0.999, 0.9995]))
+        k = int(rng.integers(floor, 260 if it % 4 == 0 else 200))
+        a = _planted(rng, rows, cols, p, min(k, rows))
+        if it % 5 == 1:  # a second square of the same side further down-left: ties
+            kk = min(k, rows)
+            t0, l0 = int(rng.integers(0, rows - kk + 1)), int(rng.integers(0, cols - kk + 1))
+            a[t0:t0 + kk, l0:l0 + kk] = 1
+        want = oracle.freq(a)
+        if want.side < floor:
+            continue
+        w = torch.from_numpy(grid.pack_bits(a).view(np.int32)).cuda()
+        nb = int(rng.integers(2, min(rows // 8, 150) + 1))
+        _same(Solver(N.FMT_BITS, rows, cols, nbands=nb).solve(w)[0], want)

@@ -1,0 +1,28 @@
+"""Time the cfg4 solve (msq_launch) under env variants; print answer + ms."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2503_18974_b200 import _native as N, build, configs
+from paper_2503_18974_b200.squares import Solver
+build.build()
+cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
+src = configs.cfg4_device() if cfg == "cfg4" else configs.cfg5_device()
+fmt = N.FMT_BITS if cfg == "cfg4" else N.FMT_U8
+spec = configs.CONFIGS[cfg]
+for env in ({"MSQ_STRIP": "0"}, {}, {"MSQ_TEST_FLOOR": "100"}, {"MSQ_TEST_FLOOR": "120"}, {"MSQ_TEST_FLOOR": "133"}):
+    for k in ("MSQ_STRIP", "MSQ_TEST_FLOOR"):
+        os.environ.pop(k, None)
+    os.environ.update(env)
+    s = Solver(fmt, spec["rows"], spec["cols"])
+    for _ in range(3):
+        s.launch(src)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(20):
+        s.launch(src)
+    e1.record()
+    torch.cuda.synchronize()
+    r = s.result()[0]
+    host = s.res.cpu().numpy().view("int32")
+    print(env, round(e0.elapsed_time(e1) / 20, 4), "ms", (r.side, r.top, r.left), "best_side", host[5], flush=True)
