@@ -2032,7 +2032,7 @@ __global__ void __launch_bounds__(32 * CARRY_SEG) carry_scan_kernel(int rows, in
 // row.  Any square it finds is a real square of the matrix, so the bands may
 // start testing at the largest one (ties included) -- the same argument as the
 // shared best side (P2); rows whose local heights cannot reach it need no test.
-constexpr int SEED_ROWS = 128;  // strip height (squares found are <= this)
+constexpr int SEED_ROWS = 192;  // strip height (squares found are <= this)
 constexpr int SEED_BATCH = 16;  // rows loaded per batch (next batch in flight while one is processed)
 constexpr int SEED_STEP = 4;    // test every SEED_STEP rows at best + SEED_STEP (a lower bound needs no exactness)
 template <bool U8>
@@ -2057,7 +2057,7 @@ __global__ void __launch_bounds__(256) seed_climb_kernel(const uint8_t* src, lon
     const int nr = min(SEED_ROWS, rows - r0);
     const int w = chunk * 32 + lane;
     const uint32_t val = valid_mask(w, W, cols);
-    constexpr int P = 7;  // heights saturate at 127 (the strip is 128 rows)
+    constexpr int P = 8;  // heights saturate at 255 (the strip is 192 rows)
     uint32_t h[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) h[p] = 0u;

@@ -242,24 +242,26 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
                         }
                     }
                 }
-                // eligibility of column `lane` of window word i at row rho
-                auto elig = [&](int i) -> uint32_t {
-                    if (i < 0 || i >= STRIP_WORDS) return 0u;
-                    const int kk = i & 3;
+                // column `lane` of window word i at row rho: (last-zero row before the
+                // tile, never-zeroed, valid, zero in the tile up to this row)
+                auto col_state = [&](int i, int& zr, uint32_t& nzw, uint32_t& vlw, uint32_t& tz) {
+                    const int ic = min(max(i, 0), STRIP_WORDS - 1);
+                    const int kk = ic & 3;
                     const uint32_t nzs = kk == 0 ? NZ[0] : kk == 1 ? NZ[1] : kk == 2 ? NZ[2] : NZ[3];
                     const uint32_t vls = kk == 0 ? VAL[0] : kk == 1 ? VAL[1] : kk == 2 ? VAL[2] : VAL[3];
-                    const uint32_t nzw = __shfl_sync(0xFFFFFFFFu, nzs, i >> 2);
-                    const uint32_t vlw = __shfl_sync(0xFFFFFFFFu, vls, i >> 2);
-                    const int zr = zwin[i * 32 + lane];
-                    // a zero in the tile up to this row: never eligible (t > 8)
-                    const int aw = min(max(base_word + i, 0), p.W - 1);
+                    nzw = __shfl_sync(0xFFFFFFFFu, nzs, ic >> 2);
+                    vlw = (i == ic) ? __shfl_sync(0xFFFFFFFFu, vls, ic >> 2) : 0u;
+                    zr = zwin[ic * 32 + lane];
+                    const int aw = min(max(base_word + ic, 0), p.W - 1);
                     const uint32_t wsl = smem_addr(ring) + (uint32_t)(s * slot_bytes + aw * 4);
-                    uint32_t tz = 0u;
+                    tz = 0u;
                     for (int bb = 0; bb <= b; ++bb) {
                         uint32_t w1[1];
-                        lds_words<1>(wsl + (uint32_t)(bb * p.row_bytes), w1);
+                        lds_words<1>(wsl + (uint32_t)bb * rb_bytes, w1);
                         tz |= ~w1[0];
                     }
+                };
+                auto elig = [&](int zr, uint32_t nzw, uint32_t vlw, uint32_t tz) -> uint32_t {
                     const bool e = !((tz >> lane) & 1u) && (((nzw >> lane) & 1u) ? rho >= t : zr + t <= rho);
                     return __ballot_sync(0xFFFFFFFFu, e) & vlw;
                 };
@@ -273,7 +275,11 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
                         bal &= bal - 1;
                         const int c = __shfl_sync(0xFFFFFFFFu, mine, l);
                         const int a0 = c >> 8, L = c & 0xFF, a1 = a0 + L;
-                        const uint32_t el = elig(a0 - 1), er = elig(a1);
+                        int zl, zrr;
+                        uint32_t nl, nr_, vl, vr, tl, tr;
+                        col_state(a0 - 1, zl, nl, vl, tl);  // both boundary words' loads in flight
+                        col_state(a1, zrr, nr_, vr, tr);
+                        const uint32_t el = elig(zl, nl, vl, tl), er = elig(zrr, nr_, vr, tr);
                         const int suf = __clz(~el);
                         const int pre = er == 0xFFFFFFFFu ? 32 : __ffs(~er) - 1;
                         if (suf + 32 * L + pre >= t) {
