@@ -48,12 +48,15 @@ struct WsLayout {
 
 // ---- strip pass (msq_strip.cuh): bit-packed single matrices, several bands
 int strip_warps(const msq_plan* p) { return (int)ceil_div(p->words, msq::STRIP_STRIDE); }
+int strip_fixed_smem(const msq_plan* p) {  // barriers, flags, never-zeroed masks
+    return 2 * msq::STRIP_MAXSLOTS * 8 + 32 + strip_warps(p) * msq::STRIP_WORDS * 4;
+}
 int strip_slots(const msq_plan* p) {
     const long long slot = (long long)msq::STRIP_TR * p->row_stage_bytes;
-    return (int)std::min<long long>(msq::STRIP_MAXSLOTS, (kSmemMax - 256) / slot);
+    return (int)std::min<long long>(msq::STRIP_MAXSLOTS, (kSmemMax - 256 - strip_fixed_smem(p)) / slot);
 }
 int strip_smem(const msq_plan* p) {
-    return strip_slots(p) * msq::STRIP_TR * p->row_stage_bytes + 2 * msq::STRIP_MAXSLOTS * 8 + 64;
+    return strip_slots(p) * msq::STRIP_TR * p->row_stage_bytes + strip_fixed_smem(p);
 }
 bool strip_applies(const msq_plan* p) {
     if (const char* f = getenv("MSQ_STRIP"))  // experiments: MSQ_STRIP=0 disables

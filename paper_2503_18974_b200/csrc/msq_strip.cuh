@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
     uint64_t* empty = full + STRIP_MAXSLOTS;
     int* sh = (int*)(empty + STRIP_MAXSLOTS);  // [0] start threshold, [1] CTA best, [2] abort
     unsigned long long* skey = (unsigned long long*)(sh + 4);
+    uint32_t* nz_sm = (uint32_t*)(sh + 8);  // [nwarps][128] never-zeroed masks of the warps' windows
     unsigned char* result = p.results;
 
     if (tid == 0) {
@@ -125,14 +126,13 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
     // ------------------------------------------------------------ consumers
     const int base_word = STRIP_STRIDE * warp - STRIP_HALO;
     const int i0 = 4 * lane;  // first window index of this lane
-    uint32_t VAL[4], NZ[4];
+    uint32_t VAL[4];
     int ZW[4];
     uint32_t fullk = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int a = base_word + i0 + k;
         VAL[k] = (a >= 0 && a < p.W) ? valid_mask(a, p.W, p.cols) : 0u;
-        NZ[k] = VAL[k];
         ZW[k] = 0;
         fullk |= (VAL[k] == 0xFFFFFFFFu ? 1u : 0u) << k;
     }
@@ -143,6 +143,12 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
     const int a_ld = min(max(base_word + i0, 0), p.W - 4);
     const uint32_t ring_s = smem_addr(ring) + (uint32_t)(a_ld * 4);
     uint16_t* zwin = p.zw + ((size_t)band * p.nwarps + warp) * (STRIP_WORDS * 32);
+    uint32_t* nzw = nz_sm + warp * STRIP_WORDS;
+    *(uint4*)(nzw + i0) = make_uint4(VAL[0], VAL[1], VAL[2], VAL[3]);
+    // the only word of the matrix that can be partial is W-1
+    const int kpart = (p.cols & 31) ? (p.W - 1) - (base_word + i0) : -1;
+    const uint32_t valpart = (kpart >= 0 && kpart < 4) ? valid_mask(p.W - 1, p.W, p.cols) : 0xFFFFFFFFu;
+    __syncwarp();
     const size_t sum_base = (size_t)band * p.cols_pad;
 
     int t = t0;
@@ -244,13 +250,11 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
                 }
                 // column `lane` of window word i at row rho: (last-zero row before the
                 // tile, never-zeroed, valid, zero in the tile up to this row)
-                auto col_state = [&](int i, int& zr, uint32_t& nzw, uint32_t& vlw, uint32_t& tz) {
+                auto col_state = [&](int i, int& zr, uint32_t& nzv, uint32_t& vlw, uint32_t& tz) {
                     const int ic = min(max(i, 0), STRIP_WORDS - 1);
-                    const int kk = ic & 3;
-                    const uint32_t nzs = kk == 0 ? NZ[0] : kk == 1 ? NZ[1] : kk == 2 ? NZ[2] : NZ[3];
-                    const uint32_t vls = kk == 0 ? VAL[0] : kk == 1 ? VAL[1] : kk == 2 ? VAL[2] : VAL[3];
-                    nzw = __shfl_sync(0xFFFFFFFFu, nzs, ic >> 2);
-                    vlw = (i == ic) ? __shfl_sync(0xFFFFFFFFu, vls, ic >> 2) : 0u;
+                    const int ag = base_word + ic;
+                    nzv = nzw[ic];
+                    vlw = (i == ic && ag >= 0 && ag < p.W) ? valid_mask(ag, p.W, p.cols) : 0u;
                     zr = zwin[ic * 32 + lane];
                     const int aw = min(max(base_word + ic, 0), p.W - 1);
                     const uint32_t wsl = smem_addr(ring) + (uint32_t)(s * slot_bytes + aw * 4);
@@ -261,8 +265,8 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
                         tz |= ~w1[0];
                     }
                 };
-                auto elig = [&](int zr, uint32_t nzw, uint32_t vlw, uint32_t tz) -> uint32_t {
-                    const bool e = !((tz >> lane) & 1u) && (((nzw >> lane) & 1u) ? rho >= t : zr + t <= rho);
+                auto elig = [&](int zr, uint32_t nzv, uint32_t vlw, uint32_t tz) -> uint32_t {
+                    const bool e = !((tz >> lane) & 1u) && (((nzv >> lane) & 1u) ? rho >= t : zr + t <= rho);
                     return __ballot_sync(0xFFFFFFFFu, e) & vlw;
                 };
                 int beste = 0x7FFFFFFF;
@@ -307,31 +311,30 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
         {
             uint32_t EV = N;  // bit 4b + k: word k, row b (rows in order per word)
             uint32_t cz = 0u, cn = 0u;
-            int cidx = 0, crho = 0;
+            uint16_t* zp = zwin;
+            uint16_t* ep = p.e_out;
+            int crho = 0;
             while (__any_sync(0xFFFFFFFFu, (EV | cz) != 0u)) {
                 if (cz == 0u && EV != 0u) {
                     const int bit = __ffs(EV) - 1;
                     EV &= EV - 1;
                     const int k = bit & 3, b = bit >> 2;
                     uint32_t w1[1];
-                    lds_words<1>(slot_s + (uint32_t)(b * p.row_bytes + 4 * k), w1);
-                    const uint32_t vk = k == 0 ? VAL[0] : k == 1 ? VAL[1] : k == 2 ? VAL[2] : VAL[3];
-                    const uint32_t nk = k == 0 ? NZ[0] : k == 1 ? NZ[1] : k == 2 ? NZ[2] : NZ[3];
-                    cz = ~w1[0] & vk;
+                    lds_words<1>(slot_s + (uint32_t)b * rb_bytes + 4u * (uint32_t)k, w1);
+                    const int i = i0 + k;
+                    cz = ~w1[0] & (k == kpart ? valpart : 0xFFFFFFFFu);
+                    const uint32_t nk = nzw[i];
                     cn = ((own_mask >> k) & 1u) ? (nk & cz) : 0u;
-                    const uint32_t nn = nk & ~cz;
-                    NZ[0] = k == 0 ? nn : NZ[0];
-                    NZ[1] = k == 1 ? nn : NZ[1];
-                    NZ[2] = k == 2 ? nn : NZ[2];
-                    NZ[3] = k == 3 ? nn : NZ[3];
-                    cidx = i0 + k;
+                    nzw[i] = nk & ~cz;
+                    zp = zwin + i * 32;
+                    ep = p.e_out + sum_base + (size_t)(base_word + i) * 32;
                     crho = rho0 + b;
                 }
                 if (cz) {
                     const int j = __ffs(cz) - 1;
                     cz &= cz - 1;
-                    zwin[cidx * 32 + j] = (uint16_t)crho;
-                    if ((cn >> j) & 1u) p.e_out[sum_base + (size_t)(base_word + cidx) * 32 + j] = (uint16_t)(crho - 1);
+                    zp[j] = (uint16_t)crho;
+                    if ((cn >> j) & 1u) ep[j] = (uint16_t)(crho - 1);
                 }
             }
         }
@@ -361,14 +364,12 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
         // 8 words per step: their last-zero rows are loaded (L2) before any is used
         for (int i8 = STRIP_HALO; i8 < STRIP_WORDS; i8 += 8) {
             int zr[8];
-            uint32_t nzw[8];
+            uint32_t nzb[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int i = i8 + u;
-                const int kk = i & 3;
-                const uint32_t nzs = kk == 0 ? NZ[0] : kk == 1 ? NZ[1] : kk == 2 ? NZ[2] : NZ[3];
-                nzw[u] = __shfl_sync(0xFFFFFFFFu, nzs, i >> 2);
-                zr[u] = (base_word + i < p.W && !((nzw[u] >> lane) & 1u)) ? (int)zwin[i * 32 + lane] : 0;
+                nzb[u] = nzw[i];
+                zr[u] = (base_word + i < p.W && !((nzb[u] >> lane) & 1u)) ? (int)zwin[i * 32 + lane] : 0;
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -376,8 +377,8 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
                 if (a < p.W) {
                     const size_t cb = sum_base + (size_t)a * 32;
                     p.zb[cb + lane] = (uint16_t)(H - zr[u]);
-                    if ((nzw[u] >> lane) & 1u) p.e_out[cb + lane] = (uint16_t)H;
-                    if (lane == 0) p.ao_out[(size_t)band * p.W + a] = nzw[u];
+                    if ((nzb[u] >> lane) & 1u) p.e_out[cb + lane] = (uint16_t)H;
+                    if (lane == 0) p.ao_out[(size_t)band * p.W + a] = nzb[u];
                 }
             }
         }
