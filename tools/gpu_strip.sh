@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "strip or wide or cfg4" > gpurun_out/pytest_strip.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_strip.log
 timeout 300 python tools/time_cfg4.py > gpurun_out/time_cfg4.log 2>&1
-for c in cfg5 cfg3; do timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$c.json 2>gpurun_out/bench_$c.err; done

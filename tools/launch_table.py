@@ -12,7 +12,7 @@ for r in rows[1:]:
     v = float(r[vi].replace(",", ""))
     scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
     agg[r[ki]].append(v * scale)
-solve = {k: v for k, v in agg.items() if k.startswith("void msq::pass1") or k.startswith("msq::carry") or k.startswith("void msq::fixup")}
+solve = {k: v for k, v in agg.items() if k.startswith(("void msq::pass1", "msq::carry", "void msq::fixup", "msq::strip", "void msq::seed", "void msq::team"))}
 tot = sum(sum(v) for v in solve.values())
 print("# ncu launch list (cfg4 bench)\n")
 print(f"Command: `{sys.argv[2]}`\n(cold-cache, serialised per launch: compare shares, not absolutes)\n")
