@@ -2033,8 +2033,8 @@ __global__ void __launch_bounds__(32 * CARRY_SEG) carry_scan_kernel(int rows, in
 // start testing at the largest one (ties included) -- the same argument as the
 // shared best side (P2); rows whose local heights cannot reach it need no test.
 constexpr int SEED_ROWS = 192;  // strip height (squares found are <= this)
-constexpr int SEED_BATCH = 16;  // rows loaded per batch (next batch in flight while one is processed)
-constexpr int SEED_STEP = 4;    // test every SEED_STEP rows at best + SEED_STEP (a lower bound needs no exactness)
+constexpr int SEED_BATCH = 32;  // rows loaded per batch (next batch in flight while one is processed)
+constexpr int SEED_STEP = 8;    // test every SEED_STEP rows at best + SEED_STEP (a lower bound needs no exactness)
 template <bool U8>
 __device__ __forceinline__ uint32_t seed_word(const uint8_t* rp, int w, int W, int cols) {
     if (w >= W) return 0u;
@@ -2046,6 +2046,10 @@ __device__ __forceinline__ uint32_t seed_word(const uint8_t* rp, int w, int W, i
     for (int j = 0; j < 32 && c0 + j < cols; ++j) word |= (uint32_t)(rp[c0 + j] & 1u) << j;
     return word;
 }
+// Heights are kept as last-zero rows in 8 bit-planes (one LOP3 per plane and
+// row: rows count from 8 so inside a batch of 32 rows the low 3 plane bits are
+// compile-time constants), and a test every 8 rows is an 8-LOP3 comparison
+// plus one segmented warp scan.
 template <bool U8>
 __global__ void __launch_bounds__(256) seed_climb_kernel(const uint8_t* src, long long ld_bytes, int rows, int cols,
                                                          int W, int nstrips, int chunks, unsigned char* result) {
@@ -2057,10 +2061,10 @@ __global__ void __launch_bounds__(256) seed_climb_kernel(const uint8_t* src, lon
     const int nr = min(SEED_ROWS, rows - r0);
     const int w = chunk * 32 + lane;
     const uint32_t val = valid_mask(w, W, cols);
-    constexpr int P = 8;  // heights saturate at 255 (the strip is 192 rows)
-    uint32_t h[P];
+    constexpr int P = 8;  // stored rows r + 8 <= 199 < 256
+    uint32_t z[P];
 #pragma unroll
-    for (int p = 0; p < P; ++p) h[p] = 0u;
+    for (int q = 0; q < P; ++q) z[q] = (7u >> q) & 1u ? 0xFFFFFFFFu : 0u;  // 7 = no zero yet
     int best = 0;
     uint32_t nxt[SEED_BATCH];
 #pragma unroll
@@ -2076,21 +2080,34 @@ __global__ void __launch_bounds__(256) seed_climb_kernel(const uint8_t* src, lon
 #pragma unroll
         for (int q = 0; q < SEED_BATCH; ++q) {
             if (i0 + q >= nr) break;
-            planes_step<P>(h, rw[q] & val);
+            const uint32_t m = rw[q] & val;
+            const uint32_t rg = (uint32_t)(i0 + q + 8);  // stored row; low 3 bits = q & 7 (batches are multiples of 8)
+#pragma unroll
+            for (int p = 0; p < 3; ++p) z[p] = ((q >> p) & 1) ? (z[p] | ~m) : (z[p] & m);
+#pragma unroll
+            for (int p = 3; p < P; ++p) z[p] = (m & z[p]) | (~m & (0u - ((rg >> p) & 1u)));
             if ((q % SEED_STEP) != SEED_STEP - 1) continue;
-            const int T = min(best + SEED_STEP, (1 << P) - 1);
-            const uint32_t acc = planes_ge<P>(h, T) & val;
+            const int T = best + SEED_STEP;
+            // E = {z <= rg - T}: LSB-first comparison
+            const int cvs = (int)rg - T;
+            const uint32_t cv = (uint32_t)max(cvs, 0);
+            uint32_t le = 0xFFFFFFFFu;
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const uint32_t cb = 0u - ((cv >> p) & 1u);
+                le = (cb & (~z[p] | le)) | (~cb & ~z[p] & le);
+            }
+            const uint32_t acc = cvs >= 0 ? (le & val) : 0u;
             // run of eligible columns ending at the end of this lane's word (segmented warp scan)
             const bool full = acc == 0xFFFFFFFFu;
             int v = full ? 32 : __clz(~acc);
             int f = full ? 1 : 0;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const int v2 = __shfl_up_sync(0xFFFFFFFFu, v, o);
-                const int f2 = __shfl_up_sync(0xFFFFFFFFu, f, o);
+                const int v2 = __shfl_up_sync(0xFFFFFFFFu, v | (f << 16), o);
                 if (lane >= o) {
-                    if (f) v += v2;
-                    f &= f2;
+                    if (f) v += v2 & 0xFFFF;
+                    f &= v2 >> 16;
                 }
             }
             int rin = __shfl_up_sync(0xFFFFFFFFu, v, 1);
