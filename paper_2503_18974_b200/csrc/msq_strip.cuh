@@ -164,6 +164,8 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
         const int nrows = min(STRIP_TR, H - row0);
         const int rho0 = row0 + 1;
         const uint32_t slot_s = ring_s + (uint32_t)(s * slot_bytes);
+        // the grid's best side every 8 tiles, loaded here and used after the tile
+        const int gglob = (q & 7) == 7 ? ld_volatile(res_best(result)) : 0;
         mbar_wait(&full[s], par);
         if (aborted) {  // keep the ring moving; pass1_kernel redoes the band
             __syncwarp();
@@ -345,8 +347,7 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         // shared best side (ties): the CTA's every tile, the grid's every 8 tiles
-        int g = ld_volatile(&sh[1]);
-        if ((q & 7) == 7) g = max(g, ld_volatile(res_best(result)));
+        const int g = max(ld_volatile(&sh[1]), gglob);
         if (g > t) {
             t = g;
             if (t > STRIP_TMAX) aborted = true;
