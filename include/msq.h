@@ -111,6 +111,13 @@ int msq_solve_bits(const uint32_t* d_words, int64_t rows, int64_t cols, int64_t 
 int msq_solve_batch_u8(const uint8_t* d_cells, int64_t batch, int64_t rows, int64_t cols,
                        msq_result* out, void* stream);
 
+/* The three-way-min DP (dp_full, squares.py:142-171) over a batch of small
+ * matrices (cols <= 256), one thread per matrix: the independent second
+ * solver of the GPU verification campaigns (the reference's verify.py:32-37
+ * runs dp_full beside freq_square).  Same result convention. */
+int msq_dp_batch_u8(const uint8_t* d_cells, int64_t batch, int64_t rows, int64_t cols,
+                    msq_result* out, void* stream);
+
 /* Host-buffer entry points: copy H2D on `stream`, solve, copy the result
  * back (the path a CPU caller of freq_square takes). */
 int msq_solve_u8_host(const uint8_t* h_cells, int64_t rows, int64_t cols, int64_t ld,

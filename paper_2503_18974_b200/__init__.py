@@ -24,6 +24,7 @@ from .squares import (
     AllocationAudit,
     Solver,
     SquareResult,
+    dp_batch,
     freq_square,
     freq_square_bits,
     solve_batch,
@@ -36,5 +37,5 @@ __all__ = [
     "MatrixParseError", "RaggedRowsError", "generate_edge_case", "generate_matrix",
     "pack_bits", "parse_matrix", "serialize_matrix", "unpack_bits", "GPU_SOLVERS",
     "AllocationAudit", "Solver", "SquareResult", "freq_square", "freq_square_bits",
-    "solve_batch", "__version__",
+    "solve_batch", "dp_batch", "__version__",
 ]

@@ -15,6 +15,7 @@
 #include "msq_engine.cuh"
 #include "msq_team.cuh"
 #include "msq_strip.cuh"
+#include "msq_dp.cuh"
 
 namespace {
 
@@ -663,6 +664,48 @@ int msq_solve_u8(const uint8_t* d_cells, int64_t rows, int64_t cols, int64_t ld,
 int msq_solve_bits(const uint32_t* d_words, int64_t rows, int64_t cols, int64_t ld_words, msq_result* out,
                    void* stream) {
     return solve_sync(MSQ_FMT_BITS, 1, d_words, rows, cols, ld_words, out, stream);
+}
+
+int msq_dp_batch_u8(const uint8_t* d_cells, int64_t batch, int64_t rows, int64_t cols, msq_result* out,
+                    void* stream) {
+    if (!out || batch < 1 || rows < 0 || cols < 0 || cols > msq::DP_MAXCOLS || rows >= (1 << 20) ||
+        batch > (1 << 30))
+        return MSQ_EINVAL;
+    if (rows == 0 || cols == 0) {
+        for (int64_t k = 0; k < batch; ++k) out[k] = msq_result{0, 0, 0, -1, -1};
+        return MSQ_OK;
+    }
+    if (!d_cells) return MSQ_EINVAL;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return MSQ_ECUDA;
+    DevCache& C = g_cache[dev];
+    std::lock_guard<std::mutex> lk(C.mu);
+    int rc;
+    if ((rc = grow((void**)&C.res, &C.res_cap, sizeof(msq_devresult) * (size_t)batch))) return rc;
+    if (C.hres_cap < (size_t)batch) {
+        if (C.hres) cudaFreeHost(C.hres);
+        C.hres = nullptr;
+        C.hres_cap = 0;
+        if (cudaMallocHost((void**)&C.hres, sizeof(msq_devresult) * (size_t)batch) != cudaSuccess)
+            return MSQ_ENOMEM;
+        C.hres_cap = (size_t)batch;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemsetAsync(C.res, 0, sizeof(msq_devresult) * (size_t)batch, st) != cudaSuccess) return MSQ_ECUDA;
+    msq::dp_batch_kernel<<<(int)ceil_div(batch, 128), 128, 0, st>>>(d_cells, (int)batch, (int)rows, (int)cols,
+                                                                    (unsigned char*)C.res);
+    g_last_launches = 1;
+    if (cudaGetLastError() != cudaSuccess) return MSQ_ECUDA;
+    if (cudaMemcpyAsync(C.hres, C.res, sizeof(msq_devresult) * (size_t)batch, cudaMemcpyDeviceToHost, st) !=
+        cudaSuccess)
+        return MSQ_ECUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return MSQ_ECUDA;
+    int worst = MSQ_OK;
+    for (int64_t k = 0; k < batch; ++k) {
+        int r = msq_decode(&C.hres[k], rows, cols, &out[k]);
+        if (r) worst = r;
+    }
+    return worst;
 }
 
 int msq_solve_batch_u8(const uint8_t* d_cells, int64_t batch, int64_t rows, int64_t cols, msq_result* out,

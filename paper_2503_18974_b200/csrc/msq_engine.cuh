@@ -1960,7 +1960,7 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
 // the map c -> (all ones ? c + h_q : b_q); a segment composes its maps
 // (pass 1), then folds the maps of the segments above from base and writes
 // its carries (pass 2) -- 2 reads of the summaries, CARRY_SEG-way parallel.
-constexpr int CARRY_SEG = 8;
+constexpr int CARRY_SEG = 16;
 __global__ void __launch_bounds__(32 * CARRY_SEG) carry_scan_kernel(int rows, int cols, int W, int nbands,
                                                                     int cols_pad, const uint16_t* b_in,
                                                                     const uint32_t* ao_in, const uint32_t* base,
@@ -1989,8 +1989,10 @@ __global__ void __launch_bounds__(32 * CARRY_SEG) carry_scan_kernel(int rows, in
         }
         cmask |= ~full8 & 0xFFu;
     };
-    if (ok)
+    if (ok) {
+#pragma unroll 4
         for (int q = q0; q < q1; ++q) step(q, isc);
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) fval[sg][lane][i] = v[i];
     fconst[sg][lane] = (uint8_t)isc;
@@ -2018,6 +2020,7 @@ __global__ void __launch_bounds__(32 * CARRY_SEG) carry_scan_kernel(int rows, in
         *(uint4*)(carry_out + (size_t)row * cols_pad + j0) = make_uint4(o[0], o[1], o[2], o[3]);
     };
     if (sg == 0) emit(0);
+#pragma unroll 4
     for (int q = q0; q < q1; ++q) {
         uint32_t dummy = 0;
         step(q, dummy);

@@ -232,6 +232,26 @@ def solve_batch(cells) -> list[SquareResult]:
     return [_to_result(out[k]) for k in range(B)]
 
 
+def dp_batch(cells) -> list[SquareResult]:
+    """The three-way-min DP (dp_full, squares.py:142-171) over a stack of small
+    matrices on the GPU (uint8 [batch, rows, cols], cols <= 256): the
+    independent second solver of the GPU campaigns in ``verify``."""
+    torch = _torch()
+    t = cells if isinstance(cells, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(cells, dtype=np.uint8)))
+    if t.dim() != 3:
+        raise ValueError("expected [batch, rows, cols]")
+    B, R, C = (int(x) for x in t.shape)
+    if R == 0 or C == 0:
+        return [SquareResult(0, 0, 0) for _ in range(B)]
+    t = t.to(torch.uint8).cuda().contiguous()
+    out = (N.MsqResult * B)()
+    N.check(N.load().msq_dp_batch_u8(ctypes.c_void_p(t.data_ptr()), B, R, C,
+                                     ctypes.cast(out, ctypes.POINTER(N.MsqResult)),
+                                     _stream_handle()))
+    return [_to_result(out[k]) for k in range(B)]
+
+
 Solver_fn = Callable[[object], SquareResult]
 
 # plug-in registry in the shape of squarelab.verify.DEFAULT_SOLVERS (verify.py:32-37):
