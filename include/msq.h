@@ -111,6 +111,17 @@ int msq_solve_bits(const uint32_t* d_words, int64_t rows, int64_t cols, int64_t 
 int msq_solve_batch_u8(const uint8_t* d_cells, int64_t batch, int64_t rows, int64_t cols,
                        msq_result* out, void* stream);
 
+/* Text ingest (grid.py:172-206 parse_matrix format: one '0'/'1' line per
+ * row, '\n'-separated, trailing newline optional) on the device: d_text holds
+ * nbytes of text, rows x cols as the caller derived them from the first line
+ * (cols = its length, rows = lines).  Writes u8 cells (ld bytes per row) or
+ * LSB-first packed words (ld words per row) to d_out.  On a malformed text
+ * returns MSQ_EVALUE with *bad_line = the first (1-based) line that is ragged
+ * or holds a character outside {'0','1'}: where the reference's sequential
+ * parse raises RaggedRowsError / InvalidCharError. */
+int msq_parse_text(const char* d_text, int64_t nbytes, int64_t rows, int64_t cols, int32_t fmt,
+                   void* d_out, int64_t ld, int64_t* bad_line, void* stream);
+
 /* The three-way-min DP (dp_full, squares.py:142-171) over a batch of small
  * matrices (cols <= 256), one thread per matrix: the independent second
  * solver of the GPU verification campaigns (the reference's verify.py:32-37

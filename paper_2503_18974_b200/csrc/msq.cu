@@ -16,6 +16,7 @@
 #include "msq_team.cuh"
 #include "msq_strip.cuh"
 #include "msq_dp.cuh"
+#include "msq_ingest.cuh"
 
 namespace {
 
@@ -664,6 +665,42 @@ int msq_solve_u8(const uint8_t* d_cells, int64_t rows, int64_t cols, int64_t ld,
 int msq_solve_bits(const uint32_t* d_words, int64_t rows, int64_t cols, int64_t ld_words, msq_result* out,
                    void* stream) {
     return solve_sync(MSQ_FMT_BITS, 1, d_words, rows, cols, ld_words, out, stream);
+}
+
+int msq_parse_text(const char* d_text, int64_t nbytes, int64_t rows, int64_t cols, int32_t fmt, void* d_out,
+                   int64_t ld, int64_t* bad_line, void* stream) {
+    if (!bad_line || nbytes < 0 || rows < 1 || cols < 1 || rows > 65535 || cols > (1ll << 31) - 2 ||
+        (fmt != MSQ_FMT_U8 && fmt != MSQ_FMT_BITS))
+        return MSQ_EINVAL;
+    if (!d_text || !d_out) return MSQ_EINVAL;
+    if (fmt == MSQ_FMT_U8 ? ld < cols : ld < ceil_div(cols, 32)) return MSQ_EINVAL;
+    *bad_line = 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return MSQ_ECUDA;
+    DevCache& C = g_cache[dev];
+    std::lock_guard<std::mutex> lk(C.mu);
+    int rc;
+    if ((rc = grow(&C.ws, &C.ws_bytes, 256))) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long* d_bad = (unsigned long long*)C.ws;
+    if (cudaMemsetAsync(d_bad, 0xFF, 8, st) != cudaSuccess) return MSQ_ECUDA;
+    const dim3 grid((unsigned)ceil_div(cols, msq::INGEST_CHARS), (unsigned)rows);
+    if (fmt == MSQ_FMT_BITS)
+        msq::ingest_text_kernel<true><<<grid, 256, 0, st>>>((const uint8_t*)d_text, nbytes, (int)rows, (int)cols,
+                                                           (uint8_t*)d_out, ld * 4, d_bad);
+    else
+        msq::ingest_text_kernel<false><<<grid, 256, 0, st>>>((const uint8_t*)d_text, nbytes, (int)rows, (int)cols,
+                                                            (uint8_t*)d_out, ld, d_bad);
+    g_last_launches = 1;
+    if (cudaGetLastError() != cudaSuccess) return MSQ_ECUDA;
+    unsigned long long h = 0;
+    if (cudaMemcpyAsync(&h, d_bad, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess) return MSQ_ECUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return MSQ_ECUDA;
+    if (h != ~0ull) {
+        *bad_line = (int64_t)h;
+        return MSQ_EVALUE;
+    }
+    return MSQ_OK;
 }
 
 int msq_dp_batch_u8(const uint8_t* d_cells, int64_t batch, int64_t rows, int64_t cols, msq_result* out,
