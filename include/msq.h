@@ -122,6 +122,16 @@ int msq_solve_batch_u8(const uint8_t* d_cells, int64_t batch, int64_t rows, int6
 int msq_parse_text(const char* d_text, int64_t nbytes, int64_t rows, int64_t cols, int32_t fmt,
                    void* d_out, int64_t ld, int64_t* bad_line, void* stream);
 
+/* Cube extension (cubes.py:92-125): one probe of max_cube's binary search.
+ * d_vol: depth x rows x cols u8 voxels (depth-major, then row-major, the
+ * reference's BinaryVolume layout); d_scratch: depth*rows*cols bytes.
+ * *first_depth = the first depth d >= k-1 at which the depth-frequency matrix
+ * holds a k x k window of values >= k (exists_cube_at_depth, cubes.py:75-89),
+ * or -1.  The reference's probe reads (d+1)*rows*cols voxels when it finds one
+ * at d, all of them otherwise.  MSQ_EVALUE for a voxel outside {0,1}. */
+int msq_cube_probe(const uint8_t* d_vol, int64_t depth, int64_t rows, int64_t cols, int64_t k,
+                   uint8_t* d_scratch, int64_t* first_depth, void* stream);
+
 /* The three-way-min DP (dp_full, squares.py:142-171) over a batch of small
  * matrices (cols <= 256), one thread per matrix: the independent second
  * solver of the GPU verification campaigns (the reference's verify.py:32-37

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "msq.h"
 #include "msq_engine.cuh"
@@ -17,6 +18,7 @@
 #include "msq_strip.cuh"
 #include "msq_dp.cuh"
 #include "msq_ingest.cuh"
+#include "msq_cube.cuh"
 
 namespace {
 
@@ -340,6 +342,7 @@ struct DevCache {
     size_t res_cap = 0;
     msq_devresult* hres = nullptr;  // pinned
     size_t hres_cap = 0;
+    unsigned* flag = nullptr;  // 16 bytes of device flags (cube probe)
 };
 DevCache g_cache[64];
 
@@ -700,6 +703,44 @@ int msq_parse_text(const char* d_text, int64_t nbytes, int64_t rows, int64_t col
         *bad_line = (int64_t)h;
         return MSQ_EVALUE;
     }
+    return MSQ_OK;
+}
+
+int msq_cube_probe(const uint8_t* d_vol, int64_t depth, int64_t rows, int64_t cols, int64_t k, uint8_t* d_scratch,
+                   int64_t* first_depth, void* stream) {
+    if (!first_depth || !d_vol || !d_scratch || depth < 1 || rows < 1 || cols < 1 || k < 1 || depth > (1 << 20))
+        return MSQ_EINVAL;
+    *first_depth = -1;
+    if (k > depth || k > rows || k > cols) return MSQ_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long layer = rows * cols;
+    unsigned* d_bad = nullptr;
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return MSQ_ECUDA;
+        DevCache& C = g_cache[dev];
+        std::lock_guard<std::mutex> lk(C.mu);
+        if (!C.flag && cudaMalloc((void**)&C.flag, 16) != cudaSuccess) return MSQ_ENOMEM;
+        d_bad = C.flag;
+    }
+    if (cudaMemsetAsync(d_bad, 0, 4, st) != cudaSuccess) return MSQ_ECUDA;
+    msq::cube_threshold_kernel<<<(unsigned)ceil_div(layer, 256), 256, 0, st>>>(d_vol, (int)depth, layer, (int)k,
+                                                                              d_scratch, d_bad);
+    if (cudaGetLastError() != cudaSuccess) return MSQ_ECUDA;
+    unsigned hbad = 0;
+    if (cudaMemcpyAsync(&hbad, d_bad, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess) return MSQ_ECUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return MSQ_ECUDA;
+    if (hbad) return MSQ_EVALUE;
+    // layers below depth k-1 cannot hold a k-cube (their runs are < k): skip them
+    const int64_t d0 = k - 1, nd = depth - d0;
+    std::vector<msq_result> res((size_t)nd);
+    const int rc = solve_sync(MSQ_FMT_U8, nd, d_scratch + d0 * layer, rows, cols, cols, res.data(), stream);
+    if (rc) return rc;
+    for (int64_t d = 0; d < nd; ++d)
+        if (res[(size_t)d].side >= k) {
+            *first_depth = d0 + d;
+            break;
+        }
     return MSQ_OK;
 }
 
