@@ -132,6 +132,14 @@ int msq_parse_text(const char* d_text, int64_t nbytes, int64_t rows, int64_t col
 int msq_cube_probe(const uint8_t* d_vol, int64_t depth, int64_t rows, int64_t cols, int64_t k,
                    uint8_t* d_scratch, int64_t* first_depth, void* stream);
 
+/* Histogram maximal rectangle (histogram.py:60-70 maximal_rectangle): the
+ * largest all-ones rectangle of a u8 matrix as (area, height, width) of the
+ * first largest rectangle in the reference's sweep order.  d_scratch holds
+ * msq_max_rectangle_scratch_bytes(rows, cols) bytes; cols <= 65535. */
+int64_t msq_max_rectangle_scratch_bytes(int64_t rows, int64_t cols);
+int msq_max_rectangle_u8(const uint8_t* d_cells, int64_t rows, int64_t cols, int64_t ld, void* d_scratch,
+                         int64_t* area, int64_t* height, int64_t* width, void* stream);
+
 /* The three-way-min DP (dp_full, squares.py:142-171) over a batch of small
  * matrices (cols <= 256), one thread per matrix: the independent second
  * solver of the GPU verification campaigns (the reference's verify.py:32-37

@@ -77,6 +77,9 @@ def load():
         "msq_dp_batch_u8": ([P, I64, I64, I64, RP, P], ctypes.c_int),
         "msq_parse_text": ([P, I64, I64, I64, I32, P, I64, ctypes.POINTER(I64), P], ctypes.c_int),
         "msq_cube_probe": ([P, I64, I64, I64, I64, P, ctypes.POINTER(I64), P], ctypes.c_int),
+        "msq_max_rectangle_scratch_bytes": ([I64, I64], I64),
+        "msq_max_rectangle_u8": ([P, I64, I64, I64, P, ctypes.POINTER(I64), ctypes.POINTER(I64),
+                                  ctypes.POINTER(I64), P], ctypes.c_int),
         "msq_solve_u8_host": ([P, I64, I64, I64, RP, P], ctypes.c_int),
         "msq_solve_bits_host": ([P, I64, I64, I64, RP, P], ctypes.c_int),
         "msq_rank_pass1": ([PP, P, P, P, P], ctypes.c_int),

@@ -19,6 +19,7 @@
 #include "msq_dp.cuh"
 #include "msq_ingest.cuh"
 #include "msq_cube.cuh"
+#include "msq_hist.cuh"
 
 namespace {
 
@@ -742,6 +743,46 @@ int msq_cube_probe(const uint8_t* d_vol, int64_t depth, int64_t rows, int64_t co
             break;
         }
     return MSQ_OK;
+}
+
+int msq_max_rectangle_u8(const uint8_t* d_cells, int64_t rows, int64_t cols, int64_t ld, void* d_scratch,
+                         int64_t* area, int64_t* height, int64_t* width, void* stream) {
+    if (!area || !height || !width || rows < 0 || cols < 0 || rows >= (1 << 24) || cols > 65535 ||
+        (rows > 0 && cols > 0 && (!d_cells || !d_scratch || ld < cols)))
+        return MSQ_EINVAL;
+    *area = *height = *width = 0;
+    if (rows == 0 || cols == 0) return MSQ_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    // scratch: heights [rows][cols] u16, stacks [rows][cols] u16, row (h, w) [rows] u64, key u64, flag
+    uint8_t* w = (uint8_t*)d_scratch;
+    const size_t hb = (size_t)rows * cols * 2;
+    uint16_t* hh = (uint16_t*)w;
+    uint16_t* stk = (uint16_t*)(w + hb);
+    unsigned long long* rowhw = (unsigned long long*)(w + ((2 * hb + 15) & ~(size_t)15));
+    unsigned long long* key = rowhw + rows;
+    unsigned* bad = (unsigned*)(key + 1);
+    if (cudaMemsetAsync(key, 0, 16, st) != cudaSuccess) return MSQ_ECUDA;
+    msq::hist_heights_kernel<<<(unsigned)ceil_div(cols, 256), 256, 0, st>>>(d_cells, ld, (int)rows, (int)cols, hh,
+                                                                           bad);
+    msq::hist_rows_kernel<<<(unsigned)ceil_div(rows, 128), 128, 0, st>>>(hh, (int)rows, (int)cols, stk, key, rowhw);
+    g_last_launches = 2;
+    if (cudaGetLastError() != cudaSuccess) return MSQ_ECUDA;
+    unsigned long long hk[2] = {0, 0};
+    if (cudaMemcpyAsync(hk, key, 16, cudaMemcpyDeviceToHost, st) != cudaSuccess) return MSQ_ECUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return MSQ_ECUDA;
+    if ((unsigned)hk[1]) return MSQ_EVALUE;
+    if (hk[0] == 0) return MSQ_OK;
+    const long long row = 0xFFFFFF - (long long)(hk[0] & 0xFFFFFF);
+    unsigned long long hw = 0;
+    if (cudaMemcpy(&hw, rowhw + row, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return MSQ_ECUDA;
+    *area = (int64_t)(hk[0] >> 24);
+    *height = (int64_t)(hw >> 32);
+    *width = (int64_t)(hw & 0xFFFFFFFFu);
+    return MSQ_OK;
+}
+int64_t msq_max_rectangle_scratch_bytes(int64_t rows, int64_t cols) {
+    const size_t hb = (size_t)rows * cols * 2;
+    return (int64_t)(((2 * hb + 15) & ~(size_t)15) + (size_t)rows * 8 + 32);
 }
 
 int msq_dp_batch_u8(const uint8_t* d_cells, int64_t batch, int64_t rows, int64_t cols, msq_result* out,
