@@ -311,11 +311,15 @@ cudaError_t launch_carry(const msq_plan* pl, void* ws, const uint32_t* base, cud
 // Lower-bound seed before pass 1 (shared-threshold mode only): strips of
 // SEED_ROWS rows x 1024-column chunks, one warp each; about 2% of the input
 // bytes.  Skipped for small matrices, batches and deterministic plans.
+bool seed_disabled() {  // experiments: MSQ_NO_SEED=1
+    const char* f = getenv("MSQ_NO_SEED");
+    return f && f[0] == '1';
+}
 int seeds_launched(const msq_plan* pl) {
-    return (pl->deterministic || pl->batch != 1 || pl->rows < 8 * msq::SEED_ROWS || pl->cols < 256) ? 0 : 1;
+    return (seed_disabled() || pl->deterministic || pl->batch != 1 || pl->rows < 8 * msq::SEED_ROWS || pl->cols < 256) ? 0 : 1;
 }
 cudaError_t launch_seed(const msq_plan* pl, const void* d_src, msq_devresult* d_result, cudaStream_t st) {
-    if (pl->deterministic || pl->batch != 1 || pl->rows < 8 * msq::SEED_ROWS || pl->cols < 256) return cudaSuccess;
+    if (seed_disabled() || pl->deterministic || pl->batch != 1 || pl->rows < 8 * msq::SEED_ROWS || pl->cols < 256) return cudaSuccess;
     const int chunks = (int)ceil_div(pl->words, 32);
     const long long nstrips = std::max<long long>(1, std::min<long long>(pl->rows / 6400, std::max(1, 1024 / chunks)));
     const long long warps = nstrips * chunks;

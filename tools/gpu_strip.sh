@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "strip or wide or cfg4" > gpurun_out/pytest_strip.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_strip.log
-timeout 300 python tools/time_cfg4.py > gpurun_out/time_cfg4.log 2>&1
+MSQ_TEST_FLOOR=133 timeout 600 ncu --set full --clock-control none --import-source on -k regex:strip_kernel -s 1 -c 1 -o gpurun_out/ncu_strip133 -f python tools/prof_solve.py cfg4 > gpurun_out/ncu_strip133.log 2>&1

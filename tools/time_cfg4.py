@@ -9,8 +9,11 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
 src = configs.cfg4_device() if cfg == "cfg4" else configs.cfg5_device()
 fmt = N.FMT_BITS if cfg == "cfg4" else N.FMT_U8
 spec = configs.CONFIGS[cfg]
-for env in ({"MSQ_STRIP": "0"}, {}, {"MSQ_TEST_FLOOR": "100"}, {"MSQ_TEST_FLOOR": "120"}, {"MSQ_TEST_FLOOR": "133"}):
-    for k in ("MSQ_STRIP", "MSQ_TEST_FLOOR"):
+VARIANTS = ({"MSQ_STRIP": "0"}, {}, {"MSQ_TEST_FLOOR": "100"}, {"MSQ_TEST_FLOOR": "120"}, {"MSQ_TEST_FLOOR": "133"},
+            {"MSQ_TEST_FLOOR": "96", "MSQ_NO_SEED": "1"}, {"MSQ_TEST_FLOOR": "120", "MSQ_NO_SEED": "1"},
+            {"MSQ_TEST_FLOOR": "133", "MSQ_NO_SEED": "1"})
+for env in VARIANTS:
+    for k in ("MSQ_STRIP", "MSQ_TEST_FLOOR", "MSQ_NO_SEED"):
         os.environ.pop(k, None)
     os.environ.update(env)
     s = Solver(fmt, spec["rows"], spec["cols"])
