@@ -327,7 +327,12 @@ def main():
             e1 = torch.cuda.Event(enable_timing=True)
             be_ = band_solver.backend
             e0.record(stream)
-            be_.pass1(src)
+            if world > 1:  # as RowBandSolver.launch: pooled seed, then the band passes
+                be_.seed(src)
+                dist.all_reduce(be_.best_side(), op=dist.ReduceOp.MAX)
+                be_.band_pass(src)
+            else:
+                be_.pass1(src)
             e1.record(stream)
             p1_ev.append((e0, e1))
             # finish the solve exactly as RowBandSolver.launch does

@@ -168,6 +168,14 @@ int msq_solve_bits_host(const uint32_t* h_words, int64_t rows, int64_t cols, int
 int msq_rank_pass1(const msq_plan* plan, const void* d_src, void* d_ws,
                    msq_devresult* d_result, void* stream);
 int msq_rank_summary(const msq_plan* plan, const void* d_ws, uint32_t* d_summary, void* stream);
+/* msq_rank_pass1 in two halves, so the ranks can pool their lower bounds:
+ * msq_rank_seed resets d_result and runs the lower-bound seed over the local
+ * rows (best side in d_result->best_side); the caller all-reduces(max)
+ * best_side over the ranks in place; msq_rank_band_pass then runs the band
+ * passes from that shared lower bound. */
+int msq_rank_seed(const msq_plan* plan, const void* d_src, msq_devresult* d_result, void* stream);
+int msq_rank_band_pass(const msq_plan* plan, const void* d_src, void* d_ws, msq_devresult* d_result,
+                       void* stream);
 int msq_compose_carry(const uint32_t* d_summaries, const int64_t* h_rank_rows, int32_t nranks,
                       int32_t rank, int64_t cols, uint32_t* d_base_carry, void* stream);
 int msq_rank_fixup(const msq_plan* plan, void* d_ws, const uint32_t* d_base_carry,

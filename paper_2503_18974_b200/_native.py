@@ -83,6 +83,8 @@ def load():
         "msq_solve_u8_host": ([P, I64, I64, I64, RP, P], ctypes.c_int),
         "msq_solve_bits_host": ([P, I64, I64, I64, RP, P], ctypes.c_int),
         "msq_rank_pass1": ([PP, P, P, P, P], ctypes.c_int),
+        "msq_rank_seed": ([PP, P, P, P], ctypes.c_int),
+        "msq_rank_band_pass": ([PP, P, P, P, P], ctypes.c_int),
         "msq_rank_summary": ([PP, P, P, P], ctypes.c_int),
         "msq_compose_carry": ([P, P, I32, I32, I64, P, P], ctypes.c_int),
         "msq_rank_fixup": ([PP, P, P, P, P], ctypes.c_int),

@@ -887,6 +887,31 @@ int msq_rank_pass1(const msq_plan* pl, const void* d_src, void* d_ws, msq_devres
     return cuda_status(e);
 }
 
+int msq_rank_seed(const msq_plan* pl, const void* d_src, msq_devresult* d_result, void* stream) {
+    if (!pl || pl->batch != 1 || !d_src || !d_result) return MSQ_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemsetAsync(d_result, 0, sizeof(msq_devresult), st) != cudaSuccess) return MSQ_ECUDA;
+    cudaError_t e = apply_test_floor(pl, d_result, st);
+    if (e != cudaSuccess) return cuda_status(e);
+    e = launch_seed(pl, d_src, d_result, st);
+    g_last_launches = seeds_launched(pl);
+    return cuda_status(e);
+}
+
+int msq_rank_band_pass(const msq_plan* pl, const void* d_src, void* d_ws, msq_devresult* d_result, void* stream) {
+    if (!pl || pl->batch != 1 || !d_src || !d_ws || !d_result || pl->ws_bytes <= 0) return MSQ_EINVAL;
+    if (pl->nstage > 0 && ((uintptr_t)d_src % 16) != 0) {
+        msq_plan q = *pl;
+        q.nstage = 0;
+        return msq_rank_band_pass(&q, d_src, d_ws, d_result, stream);
+    }
+    msq::Pass1Params p1 = make_pass1(pl, d_src, d_ws, d_result, true);
+    int nl = 1;
+    const cudaError_t e = launch_band_pass(pl, p1, d_ws, d_src, (cudaStream_t)stream, &nl);
+    g_last_launches = nl;
+    return cuda_status(e);
+}
+
 int msq_rank_summary(const msq_plan* pl, const void* d_ws, uint32_t* d_summary, void* stream) {
     if (!pl || !d_ws || !d_summary || pl->batch != 1) return MSQ_EINVAL;
     WsLayout L = ws_layout(pl);

@@ -2,8 +2,9 @@
 
 Rank r owns rows [rows*r/N, rows*(r+1)/N).  Per solve:
 
-1. band passes over the local rows (libmsq: msq_rank_pass1) -> per-band column
-   summaries + a local key;
+1. lower-bound seed over the local rows, all-reduce(max) of the seeds' best
+   side (8 bytes), band passes from it (msq_rank_seed / msq_rank_band_pass;
+   one rank: msq_rank_pass1) -> per-band column summaries + a local key;
 2. per column, the bottom run of the local slice (msq_rank_summary, uint32,
    == local rows when the column is all ones);
 3. ONE all-gather of those summaries (NCCL over NVLink; cols*4 bytes/rank);
@@ -75,6 +76,22 @@ class GpuBackend:
                                         ctypes.c_void_p(self.res.data_ptr()), self._stream()))
         self.launches += int(self.lib.msq_last_launch_count())  # lower-bound seed + band pass
 
+    def seed(self, src):
+        """Lower-bound seed over the local rows (resets the result block)."""
+        N.check(self.lib.msq_rank_seed(ctypes.byref(self.plan), ctypes.c_void_p(src.data_ptr()),
+                                       ctypes.c_void_p(self.res.data_ptr()), self._stream()))
+        self.launches += int(self.lib.msq_last_launch_count())
+
+    def best_side(self):
+        """The device's shared best side (int32 view into the result block, in place)."""
+        return self.res.view(self.torch.int32)[5:6]
+
+    def band_pass(self, src):
+        N.check(self.lib.msq_rank_band_pass(ctypes.byref(self.plan), ctypes.c_void_p(src.data_ptr()),
+                                            ctypes.c_void_p(self.ws.data_ptr()),
+                                            ctypes.c_void_p(self.res.data_ptr()), self._stream()))
+        self.launches += int(self.lib.msq_last_launch_count())
+
     def rank_summary(self):
         N.check(self.lib.msq_rank_summary(ctypes.byref(self.plan),
                                           ctypes.c_void_p(self.ws.data_ptr()),
@@ -134,7 +151,13 @@ class RowBandSolver:
     def launch(self, src) -> None:
         import torch.distributed as dist
         be = self.backend
-        be.pass1(src)
+        if self.world > 1 and hasattr(be, "seed"):
+            # pool the ranks' lower bounds (8 bytes) before the band passes
+            be.seed(src)
+            dist.all_reduce(be.best_side(), op=dist.ReduceOp.MAX, group=self.group)
+            be.band_pass(src)
+        else:
+            be.pass1(src)
         base = None
         if self.world > 1:
             summary = be.rank_summary()

@@ -365,3 +365,41 @@ def test_strip_pass_bits(torch, monkeypatch, floor):
         w = torch.from_numpy(grid.pack_bits(a).view(np.int32)).cuda()
         nb = int(rng.integers(2, min(rows // 8, 150) + 1))
         _same(Solver(N.FMT_BITS, rows, cols, nbands=nb).solve(w)[0], want)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_row_band_ranks_pooled_seed(torch, world):
+    """RowBandSolver's multi-rank flow with the seeds pooled: msq_rank_seed on
+    every virtual rank, max of their best sides written back (the all-reduce),
+    msq_rank_band_pass (strip pass on bit-packed bands), summaries, carries,
+    fix-ups: same answer as the whole matrix, squares crossing rank bounds."""
+    from paper_2503_18974_b200.distributed import GpuBackend, decode_key, slice_rows
+    rng = np.random.default_rng(100 + world)
+    for it in range(3):
+        rows, cols = world * 2048, 8192 + 32 * int(rng.integers(0, 64))
+        a = (rng.random((rows, cols)) < 0.999).astype(np.uint8)
+        k = int(rng.integers(100, 200))
+        r0k = 2048 - k // 2  # crosses the first rank boundary
+        c0k = int(rng.integers(0, cols - k))
+        a[r0k:r0k + k, c0k:c0k + k] = 1
+        full = grid.pack_bits(a).view(np.int32)
+        rank_rows = [slice_rows(rows, world, q)[1] for q in range(world)]
+        bes, srcs = [], []
+        for q in range(world):
+            r0, n = slice_rows(rows, world, q)
+            srcs.append(torch.from_numpy(np.ascontiguousarray(full[r0:r0 + n])).cuda())
+            bes.append(GpuBackend(N.FMT_BITS, n, cols, r0))
+        for be, src in zip(bes, srcs):
+            be.seed(src)
+        best = torch.stack([be.best_side().clone() for be in bes]).max()
+        for be, src in zip(bes, srcs):
+            be.best_side().copy_(best.reshape(1))
+            be.band_pass(src)
+        gathered = torch.stack([be.rank_summary().clone() for be in bes])
+        keys = []
+        for q, be in enumerate(bes):
+            base = be.compose(gathered, rank_rows, q) if q > 0 else None
+            be.fixup(base)
+            keys.append(be.key_status())
+        ks = torch.stack(keys).max(dim=0).values.cpu().numpy()
+        _same(decode_key(int(ks[0]), int(ks[1]), rows, cols), oracle.freq(a))
