@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
     const uint32_t valpart = (kpart >= 0 && kpart < 4) ? valid_mask(p.W - 1, p.W, p.cols) : 0xFFFFFFFFu;
     __syncwarp();
     const size_t sum_base = (size_t)band * p.cols_pad;
+    uint16_t* ebase = p.e_out + sum_base + (ptrdiff_t)(base_word + i0) * 32;  // e of the lane's first word
 
     int t = t0;
     int lmin = strip_lmin(t);
@@ -313,11 +314,10 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
         {
             uint32_t EV = N;  // bit 4b + k: word k, row b (rows in order per word)
             uint32_t cz = 0u, cn = 0u;
-            uint16_t* zp = zwin;
-            uint16_t* ep = p.e_out;
-            int crho = 0;
-            while (__any_sync(0xFFFFFFFFu, (EV | cz) != 0u)) {
-                if (cz == 0u && EV != 0u) {
+            int zoff = 0, eoff = 0;
+            uint16_t crho = 0;
+            while (EV | cz) {  // one zero bit per step (an event's first bit in the step that opens it)
+                if (!cz) {
                     const int bit = __ffs(EV) - 1;
                     EV &= EV - 1;
                     const int k = bit & 3, b = bit >> 2;
@@ -328,16 +328,14 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
                     const uint32_t nk = nzw[i];
                     cn = ((own_mask >> k) & 1u) ? (nk & cz) : 0u;
                     nzw[i] = nk & ~cz;
-                    zp = zwin + i * 32;
-                    ep = p.e_out + sum_base + (size_t)(base_word + i) * 32;
-                    crho = rho0 + b;
+                    zoff = i * 32;
+                    eoff = k * 32;
+                    crho = (uint16_t)(rho0 + b);
                 }
-                if (cz) {
-                    const int j = __ffs(cz) - 1;
-                    cz &= cz - 1;
-                    zp[j] = (uint16_t)crho;
-                    if ((cn >> j) & 1u) ep[j] = (uint16_t)(crho - 1);
-                }
+                const int j = __ffs(cz) - 1;
+                cz &= cz - 1;
+                zwin[zoff + j] = crho;
+                if ((cn >> j) & 1u) ebase[eoff + j] = (uint16_t)(crho - 1);
             }
         }
         // ---- last zero row per word, release the slot

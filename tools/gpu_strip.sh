@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "ranks or cfg4 or strip" > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/bench_cfg4.json 2>gpurun_out/bench_cfg4.err
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "strip or wide or cfg4 or ranks" > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python tools/time_cfg4.py > gpurun_out/time_cfg4.log 2>&1
