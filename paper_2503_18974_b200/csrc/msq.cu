@@ -324,13 +324,14 @@ cudaError_t launch_seed(const msq_plan* pl, const void* d_src, msq_devresult* d_
     const long long nstrips = std::max<long long>(1, std::min<long long>(pl->rows / 6400, std::max(1, 1024 / chunks)));
     const long long warps = nstrips * chunks;
     const long long ld_bytes = pl->fmt == MSQ_FMT_U8 ? pl->ld : pl->ld * 4;
-    const int blocks = (int)ceil_div(warps * 32, 256);
+    // 2 warps per CTA: the strips spread over every SM (the seed is latency-bound)
+    const int blocks = (int)ceil_div(warps * 32, 64);
     if (pl->fmt == MSQ_FMT_U8)
-        msq::seed_climb_kernel<true><<<blocks, 256, 0, st>>>((const uint8_t*)d_src, ld_bytes, (int)pl->rows,
+        msq::seed_climb_kernel<true><<<blocks, 64, 0, st>>>((const uint8_t*)d_src, ld_bytes, (int)pl->rows,
                                                               (int)pl->cols, pl->words, (int)nstrips, chunks,
                                                               (unsigned char*)d_result);
     else
-        msq::seed_climb_kernel<false><<<blocks, 256, 0, st>>>((const uint8_t*)d_src, ld_bytes, (int)pl->rows,
+        msq::seed_climb_kernel<false><<<blocks, 64, 0, st>>>((const uint8_t*)d_src, ld_bytes, (int)pl->rows,
                                                                (int)pl->cols, pl->words, (int)nstrips, chunks,
                                                                (unsigned char*)d_result);
     return cudaGetLastError();
