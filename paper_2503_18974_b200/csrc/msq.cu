@@ -416,58 +416,81 @@ int plan_band(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld
 constexpr int kTeamThreads = 32;  // one warp per CTA: fine-grained spread over the SMs
 
 int team_planes(long long rows) { return rows <= 504 ? 9 : 11; }  // rows <= 2^PB - 8
+bool team_single() {  // experiments: MSQ_TEAM_SINGLE=1 keeps one team for a whole matrix
+    const char* f = getenv("MSQ_TEAM_SINGLE");
+    return f && f[0] == '1';
+}
 
 bool team_applies(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int32_t nbands) {
     if (const char* f = getenv("MSQ_ENGINE")) {  // experiments: force one engine where both apply
         if (f[0] == '0') return false;
     }
     const bool forced = getenv("MSQ_ENGINE") && getenv("MSQ_ENGINE")[0] == '1';
-    if (nbands > 0 || cols > 1024 || rows > 2040) return false;
+    if (nbands > 0 || cols > 1024) return false;
     (void)fmt;
-    // single matrices: one team is a serial row chain, faster than the band
-    // pipeline only while the matrix is short (measured: 512^2 123 vs 150 us,
-    // 1024^2 233 vs 207 us)
-    return batch > 1 || forced || rows <= 600;
+    // batches: one team per matrix (rows <= 2040).  Single matrices: one team
+    // per row band of the band plan (carry scan + fix-up behind), measured
+    // faster than the band engine for every width <= 1024 (512^2 44 vs 152 us,
+    // 1024^2 41 vs 158 us, 2000x1000 82 vs 485 us); the single-team chain only
+    // when the plan has one band.
+    if (batch > 1) return rows <= 2040;
+    return forced || rows <= 600 || rows <= 2040ll * std::min<long long>(num_sms(), std::max<long long>(1, rows / 64));
 }
 
-template <int TEAM, int PB>
-cudaError_t launch_team_t(const msq_plan* pl, const void* d_src, msq_devresult* d_result, cudaStream_t st) {
+template <int TEAM, int PB, bool BANDS>
+cudaError_t launch_team_t(const msq_plan* pl, const void* d_src, msq_devresult* d_result, cudaStream_t st,
+                          const msq::TeamBands& tb) {
     const int mpb = (kTeamThreads / 32) * (32 / TEAM);
-    const int blocks = (int)ceil_div(pl->batch, mpb);
+    const int units = BANDS ? tb.nbands : pl->batch;
+    const int blocks = (int)ceil_div(units, mpb);
     const bool u8 = pl->fmt == MSQ_FMT_U8;
     const long long ld_bytes = u8 ? pl->ld : pl->ld * 4;
-    const long long mstride = pl->rows * ld_bytes;
+    // band mode: the kernel takes the matrix's rows in mat_stride and the tallest band in rows
+    const long long mstride = BANDS ? pl->rows : pl->rows * ld_bytes;
     const bool vec = u8 && pl->cols % 32 == 0 && ld_bytes % 16 == 0 && ((uintptr_t)d_src % 16) == 0;
     const uint8_t* s = (const uint8_t*)d_src;
     unsigned char* r = (unsigned char*)d_result;
-    const int R = (int)pl->rows, C = (int)pl->cols, W = pl->words, B = pl->batch;
+    const int R = BANDS ? (int)ceil_div(pl->rows, tb.nbands) : (int)pl->rows;
+    const int C = (int)pl->cols, W = pl->words, B = units;
     if (!u8)
-        msq::team_kernel<TEAM, PB, false, false, 16><<<blocks, kTeamThreads, 0, st>>>(s, mstride, ld_bytes, R, C, W, B, r);
+        msq::team_kernel<TEAM, PB, false, false, 16, BANDS><<<blocks, kTeamThreads, 0, st>>>(s, mstride, ld_bytes, R, C, W, B, r, tb);
     else if (vec)
-        msq::team_kernel<TEAM, PB, true, true, 8><<<blocks, kTeamThreads, 0, st>>>(s, mstride, ld_bytes, R, C, W, B, r);
+        msq::team_kernel<TEAM, PB, true, true, 8, BANDS><<<blocks, kTeamThreads, 0, st>>>(s, mstride, ld_bytes, R, C, W, B, r, tb);
     else
-        msq::team_kernel<TEAM, PB, true, false, 8><<<blocks, kTeamThreads, 0, st>>>(s, mstride, ld_bytes, R, C, W, B, r);
+        msq::team_kernel<TEAM, PB, true, false, 8, BANDS><<<blocks, kTeamThreads, 0, st>>>(s, mstride, ld_bytes, R, C, W, B, r, tb);
     return cudaGetLastError();
 }
 
 template <int PB>
-cudaError_t launch_team_pb(const msq_plan* pl, const void* d_src, msq_devresult* d_result, cudaStream_t st) {
+cudaError_t launch_team_pb(const msq_plan* pl, const void* d_src, msq_devresult* d_result, cudaStream_t st,
+                           const msq::TeamBands* tb) {
     int ts = 1;
     while (ts < pl->words) ts *= 2;
+    const msq::TeamBands none{};
+    if (tb) {  // row-band mode: teams of 8..32 lanes
+        switch (ts) {
+            case 1: case 2: case 4: case 8: return launch_team_t<8, PB, true>(pl, d_src, d_result, st, *tb);
+            case 16: return launch_team_t<16, PB, true>(pl, d_src, d_result, st, *tb);
+            case 32: return launch_team_t<32, PB, true>(pl, d_src, d_result, st, *tb);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     switch (ts) {
-        case 1: return launch_team_t<1, PB>(pl, d_src, d_result, st);
-        case 2: return launch_team_t<2, PB>(pl, d_src, d_result, st);
-        case 4: return launch_team_t<4, PB>(pl, d_src, d_result, st);
-        case 8: return launch_team_t<8, PB>(pl, d_src, d_result, st);
-        case 16: return launch_team_t<16, PB>(pl, d_src, d_result, st);
-        case 32: return launch_team_t<32, PB>(pl, d_src, d_result, st);
+        case 1: return launch_team_t<1, PB, false>(pl, d_src, d_result, st, none);
+        case 2: return launch_team_t<2, PB, false>(pl, d_src, d_result, st, none);
+        case 4: return launch_team_t<4, PB, false>(pl, d_src, d_result, st, none);
+        case 8: return launch_team_t<8, PB, false>(pl, d_src, d_result, st, none);
+        case 16: return launch_team_t<16, PB, false>(pl, d_src, d_result, st, none);
+        case 32: return launch_team_t<32, PB, false>(pl, d_src, d_result, st, none);
         default: return cudaErrorInvalidValue;
     }
 }
 
-cudaError_t launch_team(const msq_plan* pl, const void* d_src, msq_devresult* d_result, cudaStream_t st) {
-    return team_planes(pl->rows) == 9 ? launch_team_pb<9>(pl, d_src, d_result, st)
-                                      : launch_team_pb<11>(pl, d_src, d_result, st);
+cudaError_t launch_team(const msq_plan* pl, const void* d_src, msq_devresult* d_result, cudaStream_t st,
+                        const msq::TeamBands* tb = nullptr) {
+    const long long h = tb ? ceil_div(pl->rows, tb->nbands) : pl->rows;  // rows one team walks
+    return team_planes(h) == 9 ? launch_team_pb<9>(pl, d_src, d_result, st, tb)
+                               : launch_team_pb<11>(pl, d_src, d_result, st, tb);
 }
 }  // namespace
 
@@ -616,6 +639,29 @@ int msq_launch(const msq_plan* pl, const void* d_src, void* d_ws, msq_devresult*
         g_last_launches = 0;
         if (cudaMemsetAsync(d_result, 0, sizeof(msq_devresult) * (size_t)pl->batch, st) != cudaSuccess)
             return MSQ_ECUDA;
+        if (pl->batch == 1 && pl->nbands > 1 && d_ws && pl->ws_bytes > 0 && !team_single() &&
+            ceil_div(pl->rows, pl->nbands) <= 2040) {
+            // one matrix on row bands: a team per band, then carry scan + fix-up
+            WsLayout L = ws_layout(pl);
+            uint8_t* w = (uint8_t*)d_ws;
+            msq::TeamBands tb{};
+            tb.nbands = pl->nbands;
+            tb.cols_pad = pl->words * 32;
+            tb.row_base = pl->row_base;
+            tb.e_out = (uint16_t*)(w + L.e);
+            tb.zb = (uint16_t*)(w + L.zb);
+            tb.ao_out = (uint32_t*)(w + L.ao);
+            tb.band_keys = (unsigned long long*)(w + L.band_keys);
+            cudaError_t e = launch_team(pl, d_src, d_result, st, &tb);
+            if (e != cudaSuccess) return cuda_status(e);
+            e = launch_carry(pl, d_ws, nullptr, st);
+            if (e != cudaSuccess) return cuda_status(e);
+            msq::FixParams f = make_fix(pl, d_ws, nullptr, d_result);
+            e = launch_fixup(pl, f, pl->nbands - 1, st);
+            if (e != cudaSuccess) return cuda_status(e);
+            g_last_launches = 3;
+            return MSQ_OK;
+        }
         cudaError_t e = launch_team(pl, d_src, d_result, st);
         if (e != cudaSuccess) return cuda_status(e);
         g_last_launches = 1;

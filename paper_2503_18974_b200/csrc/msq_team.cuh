@@ -110,15 +110,28 @@ __device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
 constexpr int LUT_SEL = 0xE2;  // (a=z, b=m, c=r): m ? z : r
 constexpr int LUT_LE = 0x8E;   // (a=z, b=le, c=cb): cb ? (~z | le) : (~z & le)
 
+// Row-band mode (one matrix, short but wide enough to want several teams):
+// team k runs Algorithm 1 on band k alone and writes the band outputs of
+// pass1_kernel (first-zero depth e, bottom run b, never-zeroed masks, band
+// key) for the carry scan and the data-free fix-up.
+struct TeamBands {
+    int nbands, cols_pad;
+    long long row_base;
+    uint16_t* e_out;
+    uint16_t* zb;
+    uint32_t* ao_out;
+    unsigned long long* band_keys;
+};
+
 // TEAM lanes per matrix (power of two >= words), PB bit planes, D rows in
 // flight per lane (a multiple of 8).  Rows are counted from 8 (z = r + 8 for
 // a zero in 0-based row r, 7 = no zero yet), so within a group of 8 rows the
 // low 3 bits of the row number are compile-time constants and the upper ones
 // are uniform: the last-zero update is one LOP3 per plane.  rows <= 2^PB - 8.
-template <int TEAM, int PB, bool U8, bool VEC, int D>
+template <int TEAM, int PB, bool U8, bool VEC, int D, bool BANDS>
 __global__ void __launch_bounds__(128) team_kernel(const uint8_t* __restrict__ src, long long mat_stride,
                                                    long long ld_bytes, int rows, int cols, int W, int batch,
-                                                   unsigned char* __restrict__ results) {
+                                                   unsigned char* __restrict__ results, const TeamBands tb) {
     static_assert(D % 8 == 0, "groups of 8 rows");
     constexpr int MPW = 32 / TEAM;  // matrices per warp
     constexpr unsigned FULL = 0xFFFFFFFFu;
@@ -133,7 +146,15 @@ __global__ void __launch_bounds__(128) team_kernel(const uint8_t* __restrict__ s
     const bool mat_ok = mat < batch;
     const bool on = mat_ok && tau < W;
     const uint32_t val = on ? valid_mask(tau, W, cols) : 0u;
-    const uint8_t* base = src + (size_t)(mat_ok ? mat : 0) * (size_t)mat_stride;
+    // band mode: "matrix" = band of the one matrix; rows = the largest band height
+    // (band mode passes the matrix's row count in mat_stride)
+    const int band_r0 = BANDS ? band_row0((int)mat_stride, tb.nbands, mat_ok ? mat : 0) : 0;
+    const int my_rows = BANDS ? (mat_ok ? band_row0((int)mat_stride, tb.nbands, mat + 1) - band_r0 : 0) : rows;
+    const uint8_t* base = BANDS ? src + (size_t)band_r0 * (size_t)ld_bytes
+                                : src + (size_t)(mat_ok ? mat : 0) * (size_t)mat_stride;
+    uint32_t fz[PB], nz = val;  // band mode: first-zero rows (bit-planes), never-zeroed columns
+#pragma unroll
+    for (int q = 0; q < PB; ++q) fz[q] = (7u >> q) & 1u ? FULL : 0u;
 
     uint32_t z[PB];
 #pragma unroll
@@ -148,7 +169,7 @@ __global__ void __launch_bounds__(128) team_kernel(const uint8_t* __restrict__ s
     TeamRow<U8, VEC> ring[D];
 #pragma unroll
     for (int d = 0; d < D; ++d)
-        if (d < rows) ring[d].load(base + (size_t)d * ld_bytes, tau, on, cols);
+        if (d < rows) ring[d].load(base + (size_t)d * ld_bytes, tau, on && d < my_rows, cols);
 
     for (int r0 = 0; r0 < rows; r0 += D) {
 #pragma unroll
@@ -162,8 +183,17 @@ __global__ void __launch_bounds__(128) team_kernel(const uint8_t* __restrict__ s
                 const int r = r0 + 8 * g + d;
                 if (r >= rows) break;  // warp-uniform
                 const TeamRow<U8, VEC> cur = ring[8 * g + d];
-                if (r + D < rows) ring[8 * g + d].load(base + (size_t)(r + D) * ld_bytes, tau, on, cols);
-                const uint32_t m = cur.bits(bad) & val;
+                if (r + D < rows) ring[8 * g + d].load(base + (size_t)(r + D) * ld_bytes, tau, on && r + D < my_rows, cols);
+                const bool live = !BANDS || r < my_rows;  // band mode: rows past this band's end
+                const uint32_t m = live ? (cur.bits(bad) & val) : FULL;
+                if (BANDS) {  // first zeros: fz = newly ? r + 8 : fz
+                    const uint32_t newly = nz & ~m;
+#pragma unroll
+                    for (int q = 0; q < 3 && q < PB; ++q) fz[q] = (d >> q) & 1 ? (fz[q] | newly) : (fz[q] & ~newly);
+#pragma unroll
+                    for (int q = 3; q < PB; ++q) fz[q] = lop3<LUT_SEL>(fz[q], ~newly, rb[q]);
+                    nz &= m;
+                }
                 // last-zero rows: z = m ? z : r + 8
 #pragma unroll
                 for (int q = 0; q < 3 && q < PB; ++q) z[q] = (d >> q) & 1 ? (z[q] | ~m) : (z[q] & m);
@@ -174,7 +204,7 @@ __global__ void __launch_bounds__(128) team_kernel(const uint8_t* __restrict__ s
                 uint32_t le = FULL;
 #pragma unroll
                 for (int q = 0; q < PB; ++q) le = lop3<LUT_LE>(z[q], le, 0u - ((cv >> q) & 1u));
-                const uint32_t E = le & val;
+                const uint32_t E = live ? (le & val) : 0u;
 
                 // ---- threshold test at t: leftmost window of t eligible columns
                 const uint32_t nE = ~E;
@@ -197,7 +227,7 @@ __global__ void __launch_bounds__(128) team_kernel(const uint8_t* __restrict__ s
                 const unsigned bal = __ballot_sync(FULL, endpos < 32) & tmask;
                 if (bal) {  // team-uniform: only the team's lanes take part
                     const int endcol = __shfl_sync(tmask, 32 * tau + endpos, __ffs(bal) - 1);
-                    key = pack_key(t, r, endcol);
+                    key = pack_key(t, BANDS ? tb.row_base + band_r0 + r : r, endcol);
                     ++t;
                     window_schedule(t, sh, inner);
                 }
@@ -205,6 +235,45 @@ __global__ void __launch_bounds__(128) team_kernel(const uint8_t* __restrict__ s
         }
     }
     const unsigned badbal = __ballot_sync(FULL, bad != 0u) & tmask;
+    if (BANDS) {
+        if (mat_ok && on) {  // this word's 32 columns: bottom runs and leading-ones depths
+            const int H = my_rows;
+            const size_t cb = (size_t)mat * tb.cols_pad + (size_t)tau * 32;
+            uint32_t bw[16], ew[16];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                int zl = 0, fl = 0;
+#pragma unroll
+                for (int q = 0; q < PB; ++q) {
+                    zl |= (int)((z[q] >> j) & 1u) << q;
+                    fl |= (int)((fz[q] >> j) & 1u) << q;
+                }
+                const uint32_t bj = (uint32_t)(H + 7 - zl);               // z = 7: never zeroed -> H
+                const uint32_t ej = ((nz >> j) & 1u) ? (uint32_t)H : (uint32_t)(fl - 8);
+                if (j & 1) {
+                    bw[j >> 1] |= bj << 16;
+                    ew[j >> 1] |= ej << 16;
+                } else {
+                    bw[j >> 1] = bj;
+                    ew[j >> 1] = ej;
+                }
+            }
+            uint4* bq = (uint4*)(tb.zb + cb);
+            uint4* eq = (uint4*)(tb.e_out + cb);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                bq[q] = make_uint4(bw[4 * q], bw[4 * q + 1], bw[4 * q + 2], bw[4 * q + 3]);
+                eq[q] = make_uint4(ew[4 * q], ew[4 * q + 1], ew[4 * q + 2], ew[4 * q + 3]);
+            }
+            tb.ao_out[(size_t)mat * W + tau] = nz;
+        }
+        if (mat_ok && tau == 0) {
+            tb.band_keys[mat] = key;
+            if (key) atomicMax(res_key1(results), key);
+            if (badbal) atomicOr(res_status(results), 1u);
+        }
+        return;
+    }
     if (mat_ok && tau == 0) {
         unsigned char* res = results + (size_t)mat * 32;
         if (key) *res_key1(res) = key;

@@ -403,3 +403,25 @@ def test_row_band_ranks_pooled_seed(torch, world):
             keys.append(be.key_status())
         ks = torch.stack(keys).max(dim=0).values.cpu().numpy()
         _same(decode_key(int(ks[0]), int(ks[1]), rows, cols), oracle.freq(a))
+
+
+def test_team_engine_row_bands(torch):
+    """Single matrices with cols <= 1024 on the team engine's row-band mode
+    (a team per band, carry scan + fix-up): tall shapes, squares crossing band
+    boundaries, strides, both formats."""
+    rng = np.random.default_rng(33)
+    for it in range(40):
+        rows = int(rng.integers(128, 6000))
+        cols = int(rng.integers(200, 1025))
+        p = float(rng.choice([0.5, 0.9, 0.99, 0.999, 1.0]))
+        k = int(rng.integers(0, min(rows, cols) + 1))
+        a = _planted(rng, rows, cols, p, k)
+        want = oracle.freq(a)
+        pad = int(rng.choice([0, 16]))
+        wide = np.zeros((rows, cols + pad), np.uint8)
+        wide[:, :cols] = a
+        s = Solver(N.FMT_U8, rows, cols, ld=cols + pad)
+        assert int(s.plan.engine) == 1 and s.nbands > 1
+        _same(s.solve(torch.from_numpy(wide).cuda())[0], want)
+        w = grid.pack_bits(a)
+        _same(Solver(N.FMT_BITS, rows, cols, ld=w.shape[1]).solve(torch.from_numpy(w.view(np.int32)).cuda())[0], want)
