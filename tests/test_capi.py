@@ -67,3 +67,29 @@ def test_decode_empty_key(lib):
     assert (out.side, out.area, out.cells_visited, out.top, out.left) == (0, 0, 12, -1, -1)
     r.status = 1
     assert lib.msq_decode(ctypes.byref(r), 3, 4, ctypes.byref(out)) == N.MSQ_EVALUE
+
+
+def test_engine_selection(lib):
+    """Which engine a plan picks: team engine for batches and
+    for single matrices up to 1024 columns (row bands when the plan has
+    several), band engine otherwise or when bands are requested explicitly."""
+    assert N.plan(N.FMT_U8, 4096, 256, 256, 256).engine == 1           # cfg2
+    p = N.plan(N.FMT_U8, 1, 512, 512, 512)                              # cfg1
+    assert p.engine == 1 and p.nbands > 1 and p.ws_bytes > 0
+    assert N.plan(N.FMT_U8, 1, 100, 64, 64).engine == 1                 # one band, one team
+    assert N.plan(N.FMT_BITS, 1, 65536, 65536, 2048).engine == 0        # cfg4: band engine (+ strip pass)
+    assert N.plan(N.FMT_U8, 1, 512, 512, 512, nbands=4).engine == 0     # explicit bands
+    assert N.plan(N.FMT_U8, 1, 512, 2048, 2048).engine == 0             # wider than 1024
+    assert N.plan(N.FMT_U8, 3, 4000, 64, 64).engine == 0                # batch rows > 2040
+
+
+def test_new_entry_points_reject_bad_arguments(lib):
+    out = N.MsqResult()
+    bad = ctypes.c_int64()
+    assert lib.msq_parse_text(None, 10, 1, 4, N.FMT_BITS, None, 1, ctypes.byref(bad), None) == N.MSQ_EINVAL
+    assert lib.msq_dp_batch_u8(None, 1, 4, 300, ctypes.byref(out), None) == N.MSQ_EINVAL  # cols > 256
+    first = ctypes.c_int64()
+    assert lib.msq_cube_probe(None, 2, 2, 2, 1, None, ctypes.byref(first), None) == N.MSQ_EINVAL
+    a, h, w = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    assert lib.msq_max_rectangle_u8(None, 0, 0, 0, None, ctypes.byref(a), ctypes.byref(h), ctypes.byref(w), None) == N.MSQ_OK
+    assert (a.value, h.value, w.value) == (0, 0, 0)
