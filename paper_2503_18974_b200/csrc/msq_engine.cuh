@@ -2069,19 +2069,43 @@ __global__ void __launch_bounds__(256) seed_climb_kernel(const uint8_t* src, lon
 #pragma unroll
     for (int q = 0; q < P; ++q) z[q] = (7u >> q) & 1u ? 0xFFFFFFFFu : 0u;  // 7 = no zero yet
     int best = 0;
-    uint32_t nxt[SEED_BATCH];
+    // rows in flight: raw 16-byte vectors for u8 (converted when used, so the
+    // loads of a whole batch are issued back to back), words for bits
+    constexpr int SB = U8 ? 16 : SEED_BATCH;
+    const bool fast = U8 && w < W && 32 * w + 32 <= cols && (ld_bytes & 15) == 0 && ((uintptr_t)src & 15) == 0;
+    struct Raw {
+        uint4 a, b;
+        uint32_t word;
+    };
+    auto fetch = [&](int i) -> Raw {
+        Raw r{make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), 0u};
+        if (i >= nr) return r;
+        const uint8_t* rp = src + (size_t)(r0 + i) * ld_bytes;
+        if (fast) {
+            r.a = *(const uint4*)(rp + 32 * w);
+            r.b = *(const uint4*)(rp + 32 * w + 16);
+        } else if (!U8) {
+            r.word = seed_word<U8>(rp, w, W, cols);
+        }
+        return r;
+    };
+    auto word_of = [&](const Raw& r, int i) -> uint32_t {
+        if (!U8) return r.word;
+        if (fast) return bits16(r.a) | (bits16(r.b) << 16);
+        return i < nr ? seed_word<U8>(src + (size_t)(r0 + i) * ld_bytes, w, W, cols) : 0u;  // partial / unaligned
+    };
+    Raw nxt[SB];
 #pragma unroll
-    for (int q = 0; q < SEED_BATCH; ++q) nxt[q] = q < nr ? seed_word<U8>(src + (size_t)(r0 + q) * ld_bytes, w, W, cols) : 0u;
-    for (int i0 = 0; i0 < nr; i0 += SEED_BATCH) {
-        uint32_t rw[SEED_BATCH];
+    for (int q = 0; q < SB; ++q) nxt[q] = fetch(q);
+    for (int i0 = 0; i0 < nr; i0 += SB) {
+        uint32_t rw[SB];
 #pragma unroll
-        for (int q = 0; q < SEED_BATCH; ++q) {
-            rw[q] = nxt[q];
-            const int i = i0 + SEED_BATCH + q;
-            nxt[q] = i < nr ? seed_word<U8>(src + (size_t)(r0 + i) * ld_bytes, w, W, cols) : 0u;
+        for (int q = 0; q < SB; ++q) {
+            rw[q] = word_of(nxt[q], i0 + q);
+            nxt[q] = fetch(i0 + SB + q);
         }
 #pragma unroll
-        for (int q = 0; q < SEED_BATCH; ++q) {
+        for (int q = 0; q < SB; ++q) {
             if (i0 + q >= nr) break;
             const uint32_t m = rw[q] & val;
             const uint32_t rg = (uint32_t)(i0 + q + 8);  // stored row; low 3 bits = q & 7 (batches are multiples of 8)
