@@ -148,7 +148,17 @@ cudaError_t launch_fixup_t(const msq_plan* pl, const msq::FixParams& prm, int nb
     static bool attr_set[64] = {false};
     cudaError_t e = set_smem_attr(kern, attr_set);
     if (e != cudaSuccess) return e;
-    kern<<<nblocks, pl->fix_threads, pl->smem_fixup, st>>>(prm);
+    cudaLaunchConfig_t cfg{};  // programmatic dependent of the carry scan
+    cfg.gridDim = dim3((unsigned)nblocks);
+    cfg.blockDim = dim3((unsigned)pl->fix_threads);
+    cfg.dynamicSmemBytes = (size_t)pl->smem_fixup;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, prm);
     return cudaGetLastError();
 }
 
@@ -302,10 +312,20 @@ int cuda_status(cudaError_t e) {
 cudaError_t launch_carry(const msq_plan* pl, void* ws, const uint32_t* base, cudaStream_t st) {
     WsLayout L = ws_layout(pl);
     uint8_t* w = (uint8_t*)ws;
-    msq::carry_scan_kernel<<<(int)ceil_div(pl->words * 32, 256), dim3(32, msq::CARRY_SEG), 0, st>>>(
-        (int)pl->rows, (int)pl->cols, pl->words, pl->nbands, pl->words * 32, (const uint16_t*)(w + L.zb),
-        (const uint32_t*)(w + L.ao), base, (uint16_t*)(w + L.carry));
-    return cudaGetLastError();
+    // programmatic dependent launch: the CTAs launch while the band pass drains
+    // and wait (griddepcontrol.wait) for its writes
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)ceil_div(pl->words * 32, 256));
+    cfg.blockDim = dim3(32, msq::CARRY_SEG);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, msq::carry_scan_kernel, (int)pl->rows, (int)pl->cols, pl->words, pl->nbands,
+                              pl->words * 32, (const uint16_t*)(w + L.zb), (const uint32_t*)(w + L.ao), base,
+                              (uint16_t*)(w + L.carry));
 }
 
 // Lower-bound seed before pass 1 (shared-threshold mode only): strips of

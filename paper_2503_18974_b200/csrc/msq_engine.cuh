@@ -1627,6 +1627,7 @@ struct FixExact {
 template <int WPT>
 __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the carry scan
     const int NT = blockDim.x;
     const int tau = threadIdx.x;
     const int lane = tau & 31;
@@ -1967,6 +1968,8 @@ __global__ void __launch_bounds__(32 * CARRY_SEG) carry_scan_kernel(int rows, in
                                                                     uint16_t* carry_out) {
     __shared__ uint32_t fval[CARRY_SEG][32][8];
     __shared__ uint8_t fconst[CARRY_SEG][32];
+    // launched as a programmatic dependent of the band pass: wait for its writes
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int lane = threadIdx.x, sg = threadIdx.y;
     const int j0 = (blockIdx.x * 32 + lane) * 8;  // 8 columns; cols_pad is a multiple of 32
     const int nq = nbands - 1;                     // transitions: carry of band q+1 from band q
