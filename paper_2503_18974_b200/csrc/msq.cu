@@ -129,8 +129,17 @@ cudaError_t launch_pass1_t(const msq_plan* pl, const msq::Pass1Params& prm, cuda
     static bool attr_set[64] = {false};
     cudaError_t e = set_smem_attr(kern, attr_set);
     if (e != cudaSuccess) return e;
-    kern<<<pl->grid, pl->threads, pl->smem_pass1, st>>>(prm);
-    cudaError_t e2 = cudaGetLastError();
+    cudaLaunchConfig_t cfg{};  // programmatic dependent of the seed / strip pass
+    cfg.gridDim = dim3((unsigned)pl->grid);
+    cfg.blockDim = dim3((unsigned)pl->threads);
+    cfg.dynamicSmemBytes = (size_t)pl->smem_pass1;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e2 = cudaLaunchKernelEx(&cfg, kern, prm);
     if (e2 != cudaSuccess) {
         cudaFuncAttributes fa{};
         cudaFuncGetAttributes(&fa, kern);
@@ -209,8 +218,17 @@ cudaError_t launch_band_pass(const msq_plan* pl, msq::Pass1Params prm, void* ws,
         static bool attr_set[64] = {false};
         cudaError_t e = set_smem_attr(msq::strip_kernel, attr_set);
         if (e != cudaSuccess) return e;
-        msq::strip_kernel<<<pl->nbands, (sp.nwarps + 1) * 32, strip_smem(pl), st>>>(sp);
-        e = cudaGetLastError();
+        cudaLaunchConfig_t cfg{};  // programmatic dependent of the seed
+        cfg.gridDim = dim3((unsigned)pl->nbands);
+        cfg.blockDim = dim3((unsigned)((sp.nwarps + 1) * 32));
+        cfg.dynamicSmemBytes = (size_t)strip_smem(pl);
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, msq::strip_kernel, sp);
         if (e != cudaSuccess) return e;
         prm.redo = sp.redo;
         *nlaunch = 2;

@@ -908,6 +908,7 @@ __device__ __forceinline__ uint32_t tile_zero_flags_bits(uint32_t ring_s, int rs
 template <int WPT, bool U8, bool TMA, bool SUB>
 __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
     extern __shared__ __align__(128) uint8_t smem[];
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the seed / strip pass
     if (!SUB && p.redo && ld_volatile(p.redo + blockIdx.x) == 0) return;  // done by strip_kernel
     const int NT = p.team;
     const int tid = threadIdx.x;

@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
     uint32_t* nz_sm = (uint32_t*)(sh + 8);  // [nwarps][128] never-zeroed masks of the warps' windows
     unsigned char* result = p.results;
 
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the seed
     if (tid == 0) {
         const int t0 = max(1, ld_volatile(res_best(result)));
         sh[0] = t0;
