@@ -20,7 +20,7 @@ template <bool BITS>
 __global__ void __launch_bounds__(256) ingest_text_kernel(const uint8_t* __restrict__ text, long long nbytes,
                                                           int rows, int cols, uint8_t* __restrict__ out,
                                                           long long ld_bytes, unsigned long long* bad_line) {
-    __shared__ __align__(16) uint8_t tile[INGEST_CHARS + 32];
+    __shared__ __align__(16) uint8_t tile[INGEST_CHARS + 48];
     const int row = blockIdx.y;
     const int c0 = blockIdx.x * INGEST_CHARS;
     const int n = min(INGEST_CHARS, cols - c0);
@@ -46,10 +46,27 @@ __global__ void __launch_bounds__(256) ingest_text_kernel(const uint8_t* __restr
     uint32_t word = 0;
     if (j0 < n && !bad) {
         const int m = min(32, n - j0);
-        for (int q = 0; q < m; ++q) {
-            const uint32_t ch = tile[off + j0 + q];
-            bad |= (ch & 0xFEu) != 0x30u;
-            word |= (ch & 1u) << q;
+        if (m == 32) {
+            // 32 characters as 8 words: aligned shared loads funnel-shifted to
+            // the line's byte offset; 4 characters validated and packed at once
+            const int o = off + j0;
+            const uint32_t* tw = (const uint32_t*)(tile + (o & ~3));
+            const uint32_t sh = 8u * (uint32_t)(o & 3);
+            uint32_t prev = tw[0];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t next = tw[q + 1];
+                const uint32_t c4 = __funnelshift_r(prev, next, sh);
+                prev = next;
+                bad |= ((c4 ^ 0x30303030u) & 0xFEFEFEFEu) != 0u;
+                word |= ((((c4 & 0x01010101u) * 0x01020408u) >> 24) & 0xFu) << (4 * q);
+            }
+        } else {
+            for (int q = 0; q < m; ++q) {
+                const uint32_t ch = tile[off + j0 + q];
+                bad |= (ch & 0xFEu) != 0x30u;
+                word |= (ch & 1u) << q;
+            }
         }
         if (BITS) {
             ((uint32_t*)(out + (long long)row * ld_bytes))[(c0 + j0) >> 5] = word;
