@@ -1969,8 +1969,10 @@ __global__ void __launch_bounds__(32 * CARRY_SEG) carry_scan_kernel(int rows, in
                                                                     uint16_t* carry_out) {
     __shared__ uint32_t fval[CARRY_SEG][32][8];
     __shared__ uint8_t fconst[CARRY_SEG][32];
-    // launched as a programmatic dependent of the band pass: wait for its writes
+    // launched as a programmatic dependent of the band pass: wait for its writes,
+    // then let the fix-up's CTAs launch (they wait for this grid in turn)
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int lane = threadIdx.x, sg = threadIdx.y;
     const int j0 = (blockIdx.x * 32 + lane) * 8;  // 8 columns; cols_pad is a multiple of 32
     const int nq = nbands - 1;                     // transitions: carry of band q+1 from band q
