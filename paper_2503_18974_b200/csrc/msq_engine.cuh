@@ -1846,12 +1846,21 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
         __syncthreads();
 
         // ---------------------------------------------- depths 2.. in tiles
+        // Climbing (every depth of the previous tile raised): first test only
+        // the tile's last depth at t + lastb.  A square of side t + lastb
+        // ending there contains one of side t + i ending at depth i (drop the
+        // bottom lastb - i rows and right columns), so success means every
+        // depth of the tile raises in turn and this test's window is the last
+        // raise -- one round instead of one per depth.  On failure the tile
+        // runs its normal rounds.
+        bool climbing = r != RES_INF;
         int tile = 0;
         for (int d0 = 2; d0 <= H && d0 < t; ++tile) {
             const bool modeL = t >= FIX_TL;
             const int nrows = min(modeL ? p.bl : p.bs, H - d0 + 1);
             if (dfilt && !dmarked(d0, nrows)) {  // no run of F words at these depths
                 d0 += nrows;
+                climbing = false;
                 continue;
             }
             uint32_t* fm = fmap + (tile & 1) * BMAX * fstride;
@@ -1885,7 +1894,8 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
             __syncthreads();
 
             const int lastb = nrows - 1;
-            int cur_t = t, start_b = 0;
+            bool spec = climbing && modeL && lastb > 0;
+            int cur_t = spec ? t + lastb : t, start_b = spec ? lastb : 0;
             ex.d0 = d0;
             for (;;) {
                 uint32_t best = RES_INF;
@@ -1932,6 +1942,14 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
                     }
                 }
                 const uint32_t rr = round_result(best);
+                if (spec) {
+                    spec = false;
+                    if (rr == RES_INF) {  // not a full climb: the tile's normal rounds
+                        cur_t = t;
+                        start_b = 0;
+                        continue;
+                    }
+                }
                 if (rr == RES_INF) break;
                 const int bs_ = (int)(rr >> 20), col = (int)(rr & 0xFFFFFu);
                 if (tau == 0) {
@@ -1942,6 +1960,7 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
                 start_b = bs_ + 1;
                 if (start_b > lastb) break;
             }
+            climbing = cur_t - t == nrows;  // every depth of this tile raised
             t = cur_t;
             if (p.share) t = max(t, misc->g);
             d0 += nrows;

@@ -425,3 +425,25 @@ def test_team_engine_row_bands(torch):
         _same(s.solve(torch.from_numpy(wide).cuda())[0], want)
         w = grid.pack_bits(a)
         _same(Solver(N.FMT_BITS, rows, cols, ld=w.shape[1]).solve(torch.from_numpy(w.view(np.int32)).cuda())[0], want)
+
+
+def test_fixup_climb_large_squares(torch):
+    """Squares far taller than a band: the fix-up climbs one side per depth;
+    the speculative last-depth test of a climbing tile must keep the exact
+    side and location (ties included), for every band count."""
+    rng = np.random.default_rng(44)
+    for it in range(16):
+        rows, cols = int(rng.integers(800, 3000)), int(rng.integers(800, 3000))
+        a = (rng.random((rows, cols)) < float(rng.choice([0.9, 0.97, 0.995]))).astype(np.uint8)
+        k = int(rng.integers(200, min(rows, cols)))
+        t0, l0 = int(rng.integers(0, rows - k + 1)), int(rng.integers(0, cols - k + 1))
+        a[t0:t0 + k, l0:l0 + k] = 1
+        if it % 3 == 0:  # an equal square elsewhere: the first one in row-major order wins
+            t1, l1 = int(rng.integers(0, rows - k + 1)), int(rng.integers(0, cols - k + 1))
+            a[t1:t1 + k, l1:l1 + k] = 1
+        want = oracle.freq(a)
+        nb = int(rng.integers(2, 60))
+        _same(Solver(N.FMT_U8, rows, cols, nbands=nb).solve(torch.from_numpy(a).cuda())[0], want)
+        w = torch.from_numpy(grid.pack_bits(a).view(np.int32)).cuda()
+        _same(Solver(N.FMT_BITS, rows, cols, nbands=nb).solve(w)[0], want)
+        _same(Solver(N.FMT_U8, rows, cols, nbands=nb, deterministic=True).solve(torch.from_numpy(a).cuda())[0], want)
