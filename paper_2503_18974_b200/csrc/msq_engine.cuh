@@ -1063,6 +1063,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
 
     int t = max(1, misc->g);
     bool full_next = false;
+    bool climbL = false;  // every row of the previous mode-L tile raised
     int climb_s = 0;
     unsigned long long bandkey = 0ull;
     int round_ctr = 0;
@@ -1339,7 +1340,13 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 }
             }
         } else {
-            int start_b = 0, full_from = full_next ? 0 : BMAX;
+            // climbing (the previous mode-L tile raised on every row): test the
+            // last row at t + lastb first -- success implies a raise on every
+            // row (a square of side t + lastb ending there contains one of side
+            // t + b ending at row b), and its window is the last raise
+            bool spec = modeL && climbL && lastb > 0;
+            int start_b = spec ? lastb : 0, full_from = full_next ? 0 : BMAX;
+            if (spec) cur_t = t + lastb;
             bool round_ctr_first = true;
             for (;;) {
                 uint32_t best = RES_INF;
@@ -1423,6 +1430,14 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
                 }
                 const uint32_t rr = misc->res[slot];
                 ++round_ctr;
+                if (spec) {
+                    spec = false;
+                    if (rr == RES_INF) {  // not a full climb: the tile's normal rounds
+                        cur_t = t;
+                        start_b = 0;
+                        continue;
+                    }
+                }
                 if (rr == RES_INF) break;
                 const int bs_ = (int)(rr >> 20), col = (int)(rr & 0xFFFFFu);
                 if (tau == 0) {
@@ -1445,6 +1460,7 @@ __global__ void __launch_bounds__(512, 1) pass1_kernel(const Pass1Params p) {
             ck = c1;
         }
         MSQ_TR(14)
+        climbL = modeL && !climb && cur_t - t == nrows;
         const bool raised = cur_t != t;
         t = cur_t;
         bool jumped = false;
