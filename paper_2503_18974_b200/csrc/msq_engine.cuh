@@ -792,16 +792,21 @@ __device__ __noinline__ uint32_t test_rows_s(const uint32_t* hist, int Wpad, int
 
 // band outputs: bottom run b_j = H - z_j from the last-zero planes
 __device__ __noinline__ void band_bottom_runs(const uint32_t* zp, int zbase, int Wpad, int P, int H, uint16_t* bo) {
-    uint32_t zb[MAXP];
+    // the 32 last-zero rows as packed uint16 pairs, plane by plane; 4 vector stores
+    uint32_t v[16];
 #pragma unroll
-    for (int q = 0; q < MAXP; ++q) zb[q] = q < P ? zp[zbase + q * Wpad] : 0u;
-#pragma unroll 1
-    for (int j = 0; j < 32; ++j) {
-        int z = 0;
+    for (int h = 0; h < 16; ++h) v[h] = 0u;
+    for (int q = 0; q < P; ++q) {
+        const uint32_t zq = zp[zbase + q * Wpad];
 #pragma unroll
-        for (int q = 0; q < MAXP; ++q) z |= (int)((zb[q] >> j) & 1u) << q;
-        bo[j] = (uint16_t)(H - z);
+        for (int j = 0; j < 32; ++j) v[j >> 1] |= ((zq >> j) & 1u) << (q + 16 * (j & 1));
     }
+    const uint32_t HH = (uint32_t)H | ((uint32_t)H << 16);
+#pragma unroll
+    for (int h = 0; h < 16; ++h) v[h] = HH - v[h];  // per half: H - z (z <= H, no borrow)
+    uint4* bq = (uint4*)bo;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bq[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
 }
 
 // Rows b < nrows of a tile (ring stages st0.., already waited for): loads of
