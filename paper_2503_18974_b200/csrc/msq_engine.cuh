@@ -221,8 +221,12 @@ __device__ __forceinline__ void tsync(unsigned mask) {
 // 4 bytes in {0,1} -> 4 bits (byte i -> bit i).  The partial products of
 // x * 0x01020408 land on distinct bit positions, so there are no carries.
 __device__ __forceinline__ uint32_t nib4(uint32_t x) { return ((x * 0x01020408u) >> 24) & 0xFu; }
+// 16 u8 cells (bytes 0/1) -> 16 bits: (x0 + 16 x1) * 0x01020408 has the 8
+// cells of x0, x1 in column order in its top byte; one byte permute joins two
 __device__ __forceinline__ uint32_t bits16(uint4 v) {
-    return nib4(v.x) | (nib4(v.y) << 4) | (nib4(v.z) << 8) | (nib4(v.w) << 12);
+    const uint32_t p0 = (v.x + (v.y << 4)) * 0x01020408u;
+    const uint32_t p1 = (v.z + (v.w << 4)) * 0x01020408u;
+    return __byte_perm(p0, p1, 0x0073) & 0xFFFFu;
 }
 
 // windows of length t (1..32) inside a word: bit p set iff bits p..p+t-1 set
