@@ -204,10 +204,12 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
         // runs of lmin F words ending in this lane's words: bytes = row masks of
         // the 8 words (left lane's 4, then ours); AND over lmin consecutive bytes
         const uint32_t PX = __shfl_up_sync(0xFFFFFFFFu, X, 1);
-        const unsigned long long S = (unsigned long long)(lane ? PX : 0u) | ((unsigned long long)X << 32);
-        unsigned long long A = S;
-        for (int i = 1; i < lmin; ++i) A &= S << (8 * i);
-        uint32_t cm = (uint32_t)(A >> 32);
+        // bytes of our 4 words ANDed with the lmin-1 bytes before each: funnel
+        // shifts of (left lane's 4, ours); lmin <= 5, unused steps are all-ones
+        const uint32_t PL = lane ? PX : 0u;
+        uint32_t cm = X;
+#pragma unroll
+        for (int i = 1; i < 5; ++i) cm &= i < lmin ? __funnelshift_l(PL, X, 8 * i) : 0xFFFFFFFFu;
         cm |= cm >> 16;
         cm |= cm >> 8;
         const uint32_t crows = __reduce_or_sync(0xFFFFFFFFu, cm & 0xFFu);
