@@ -228,6 +228,14 @@ __device__ __forceinline__ uint32_t bits16(uint4 v) {
     const uint32_t p1 = (v.z + (v.w << 4)) * 0x01020408u;
     return __byte_perm(p0, p1, 0x0073) & 0xFFFFu;
 }
+// 32 u8 cells -> 32 bits (two 16-byte vectors): three byte permutes join the four products
+__device__ __forceinline__ uint32_t bits32(uint4 a, uint4 b) {
+    const uint32_t p0 = (a.x + (a.y << 4)) * 0x01020408u;
+    const uint32_t p1 = (a.z + (a.w << 4)) * 0x01020408u;
+    const uint32_t p2 = (b.x + (b.y << 4)) * 0x01020408u;
+    const uint32_t p3 = (b.z + (b.w << 4)) * 0x01020408u;
+    return __byte_perm(__byte_perm(p0, p1, 0x0073), __byte_perm(p2, p3, 0x0073), 0x5410);
+}
 
 // windows of length t (1..32) inside a word: bit p set iff bits p..p+t-1 set
 __device__ __forceinline__ uint32_t windows_in_word(uint32_t x, int t) {
@@ -415,7 +423,7 @@ __device__ __forceinline__ void fetch_words(const uint8_t* stage_row, const uint
                     uint4 v1 = make_uint4(0, 0, 0, 0);
                     if (a * 32 + 16 < rs) v1 = *(const uint4*)(rp + 16);
                     bad_or |= v0.x | v0.y | v0.z | v0.w | v1.x | v1.y | v1.z | v1.w;
-                    word = bits16(v0) | (bits16(v1) << 16);
+                    word = bits32(v0, v1);
                 } else {
                     const int c0 = 32 * a;
                     const int n = min(32, cols - c0);
@@ -476,7 +484,7 @@ __device__ __forceinline__ uint32_t word_of_row(const uint8_t* stage_row, const 
             const uint4 v0 = *(const uint4*)rp;
             uint4 v1 = make_uint4(0, 0, 0, 0);
             if (a * 32 + 16 < rs) v1 = *(const uint4*)(rp + 16);
-            word = bits16(v0) | (bits16(v1) << 16);
+            word = bits32(v0, v1);
         } else {
             const int c0 = 32 * a;
             const int n = min(32, cols - c0);
@@ -2141,7 +2149,7 @@ __global__ void __launch_bounds__(256) seed_climb_kernel(const uint8_t* src, lon
     };
     auto word_of = [&](const Raw& r, int i) -> uint32_t {
         if (!U8) return r.word;
-        if (fast) return bits16(r.a) | (bits16(r.b) << 16);
+        if (fast) return bits32(r.a, r.b);
         return i < nr ? seed_word<U8>(src + (size_t)(r0 + i) * ld_bytes, w, W, cols) : 0u;  // partial / unaligned
     };
     Raw nxt[SB];
