@@ -404,7 +404,7 @@ def main():
                 "frac": round(achieved / peak, 4), "traffic": None,
                 "kernel": ("msq::team_kernel" if use_solver and int(solver.plan.engine) == 1 else
                            "band pass: msq::strip_kernel (+ pass1_kernel for bands it hands back), "
-                           "timed with the seed_climb_kernel before it" if fmt == N.FMT_BITS and os.environ.get("MSQ_STRIP") != "0" else
+                           "timed with the seed_climb_kernel before it" if fmt == N.FMT_BITS else
                            "msq::pass1_kernel (timed with the seed_climb_kernel before it)"),
                 "kernel_ms": round(p1_ms, 5),
                 "peak_kind": peak_kind,

@@ -83,8 +83,17 @@ typedef struct {
     int32_t grid;         /* pass-1 CTAs                                    */
     int32_t fix_threads;  /* fix-up CTA size                                */
     int32_t fix_wpt;      /* fix-up words per thread                        */
-    int32_t engine;       /* 0: band engine; 1: register team engine (small matrices, no workspace) */
+    int32_t engine;       /* 0: band engine; 1: register team engine (small matrices) */
+    int32_t flags;        /* MSQ_PLAN_* experiment switches; 0 from msq_plan_make */
+    int32_t test_floor;   /* TEST ONLY: > 0 presets the shared best side (the caller
+                             vouches that the answer is >= it); 0 from msq_plan_make */
 } msq_plan;
+
+/* msq_plan.flags: experiment switches a caller may set on its own plan
+ * (per call, no global state); production plans leave them 0. */
+#define MSQ_PLAN_NO_STRIP 1     /* bit-packed bands: skip the strip pass        */
+#define MSQ_PLAN_NO_SEED 2      /* skip the lower-bound seed                     */
+#define MSQ_PLAN_SINGLE_TEAM 4  /* team engine: one team per matrix (rows <= 2040) */
 
 /* Build a plan.  nbands <= 0 picks a default (one band per SM, bands of
  * >= 64 rows, <= 65535 rows each).  Returns MSQ_EINVAL for unsupported
@@ -92,8 +101,13 @@ typedef struct {
  * are handled by the direct-load path, not rejected). */
 int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld,
                   int32_t nbands, int32_t deterministic, msq_plan* plan);
+/* Same with an engine choice: -1 = automatic (msq_plan_make), 0 = band
+ * engine, 1 = register team engine (cols <= 1024; MSQ_EINVAL otherwise). */
+int msq_plan_make_ex(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld,
+                     int32_t nbands, int32_t deterministic, int32_t engine, msq_plan* plan);
 
-/* Enqueue a solve on `stream`.  d_ws: >= plan->ws_bytes of device memory;
+/* Enqueue a solve on `stream`.  d_ws: >= plan->ws_bytes of device memory
+ * (required for every plan with ws_bytes > 0, team-engine plans included);
  * d_result: plan->batch msq_devresult blocks (device memory).  Nothing is
  * synchronised; decode with msq_decode after the stream completes. */
 int msq_launch(const msq_plan* plan, const void* d_src, void* d_ws, msq_devresult* d_result,

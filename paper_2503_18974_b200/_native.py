@@ -16,6 +16,7 @@ HEADER = os.path.join(os.path.dirname(_PKG), "include", "msq.h")
 
 MSQ_OK, MSQ_EINVAL, MSQ_EVALUE, MSQ_ECUDA, MSQ_ENOMEM = 0, 1, 2, 3, 4
 FMT_U8, FMT_BITS = 0, 1
+PLAN_NO_STRIP, PLAN_NO_SEED, PLAN_SINGLE_TEAM = 1, 2, 4
 
 
 class MsqResult(ctypes.Structure):
@@ -41,7 +42,8 @@ class MsqPlan(ctypes.Structure):
                 ("ws_bytes", ctypes.c_int64), ("team", ctypes.c_int32),
                 ("teams_per_cta", ctypes.c_int32), ("tile_rows_l", ctypes.c_int32),
                 ("tl", ctypes.c_int32), ("grid", ctypes.c_int32), ("fix_threads", ctypes.c_int32),
-                ("fix_wpt", ctypes.c_int32), ("engine", ctypes.c_int32)]
+                ("fix_wpt", ctypes.c_int32), ("engine", ctypes.c_int32),
+                ("flags", ctypes.c_int32), ("test_floor", ctypes.c_int32)]
 
 
 _lib = None
@@ -69,6 +71,7 @@ def load():
     PP = ctypes.POINTER(MsqPlan)
     sig = {
         "msq_plan_make": ([I32, I32, I64, I64, I64, I32, I32, PP], ctypes.c_int),
+        "msq_plan_make_ex": ([I32, I32, I64, I64, I64, I32, I32, I32, PP], ctypes.c_int),
         "msq_launch": ([PP, P, P, P, P], ctypes.c_int),
         "msq_decode": ([ctypes.POINTER(MsqDevResult), I64, I64, RP], ctypes.c_int),
         "msq_solve_u8": ([P, I64, I64, I64, RP, P], ctypes.c_int),
@@ -120,8 +123,8 @@ def check(rc: int) -> None:
 
 
 def plan(fmt: int, batch: int, rows: int, cols: int, ld: int, nbands: int = 0,
-         deterministic: bool = False) -> MsqPlan:
+         deterministic: bool = False, engine: int = -1) -> MsqPlan:
     p = MsqPlan()
-    check(load().msq_plan_make(fmt, batch, rows, cols, ld, nbands, int(deterministic),
-                               ctypes.byref(p)))
+    check(load().msq_plan_make_ex(fmt, batch, rows, cols, ld, nbands, int(deterministic), engine,
+                                  ctypes.byref(p)))
     return p

@@ -64,8 +64,7 @@ int strip_smem(const msq_plan* p) {
     return strip_slots(p) * msq::STRIP_TR * p->row_stage_bytes + strip_fixed_smem(p);
 }
 bool strip_applies(const msq_plan* p) {
-    if (const char* f = getenv("MSQ_STRIP"))  // experiments: MSQ_STRIP=0 disables
-        if (f[0] == '0') return false;
+    if (p->flags & MSQ_PLAN_NO_STRIP) return false;  // experiments
     const long long ld_bytes = p->ld * 4;
     return p->fmt == MSQ_FMT_BITS && p->batch == 1 && p->nbands > 1 && !p->deterministic &&
            p->words >= 2 * msq::STRIP_WORDS && p->words % 4 == 0 && p->row_stage_bytes % 16 == 0 &&
@@ -236,14 +235,11 @@ cudaError_t launch_band_pass(const msq_plan* pl, msq::Pass1Params prm, void* ws,
     return launch_pass1(pl, prm, st);
 }
 
-// tests only: MSQ_TEST_FLOOR=k presets the shared best side to k (a lower
+// tests only: plan->test_floor = k presets the shared best side to k (a lower
 // bound the caller vouches for, k <= answer), as if the seed had found it
 cudaError_t apply_test_floor(const msq_plan* pl, msq_devresult* d_result, cudaStream_t st) {
-    const char* f = getenv("MSQ_TEST_FLOOR");
-    if (!f || pl->batch != 1) return cudaSuccess;
-    const int32_t v = atoi(f);
-    if (v <= 0) return cudaSuccess;
-    return cudaMemcpyAsync(&d_result->best_side, &v, sizeof(v), cudaMemcpyHostToDevice, st);
+    if (pl->test_floor <= 0 || pl->batch != 1) return cudaSuccess;
+    return cudaMemcpyAsync(&d_result->best_side, &pl->test_floor, sizeof(int32_t), cudaMemcpyHostToDevice, st);
 }
 
 cudaError_t launch_fixup(const msq_plan* pl, const msq::FixParams& prm, int nblocks, cudaStream_t st) {
@@ -349,15 +345,12 @@ cudaError_t launch_carry(const msq_plan* pl, void* ws, const uint32_t* base, cud
 // Lower-bound seed before pass 1 (shared-threshold mode only): strips of
 // SEED_ROWS rows x 1024-column chunks, one warp each; about 2% of the input
 // bytes.  Skipped for small matrices, batches and deterministic plans.
-bool seed_disabled() {  // experiments: MSQ_NO_SEED=1
-    const char* f = getenv("MSQ_NO_SEED");
-    return f && f[0] == '1';
-}
+bool seed_disabled(const msq_plan* pl) { return (pl->flags & MSQ_PLAN_NO_SEED) != 0; }  // experiments
 int seeds_launched(const msq_plan* pl) {
-    return (seed_disabled() || pl->deterministic || pl->batch != 1 || pl->rows < 8 * msq::SEED_ROWS || pl->cols < 256) ? 0 : 1;
+    return (seed_disabled(pl) || pl->deterministic || pl->batch != 1 || pl->rows < 8 * msq::SEED_ROWS || pl->cols < 256) ? 0 : 1;
 }
 cudaError_t launch_seed(const msq_plan* pl, const void* d_src, msq_devresult* d_result, cudaStream_t st) {
-    if (seed_disabled() || pl->deterministic || pl->batch != 1 || pl->rows < 8 * msq::SEED_ROWS || pl->cols < 256) return cudaSuccess;
+    if (seed_disabled(pl) || pl->deterministic || pl->batch != 1 || pl->rows < 8 * msq::SEED_ROWS || pl->cols < 256) return cudaSuccess;
     const int chunks = (int)ceil_div(pl->words, 32);
     const long long nstrips = std::max<long long>(1, std::min<long long>(pl->rows / 6400, std::max(1, 1024 / chunks)));
     const long long warps = nstrips * chunks;
@@ -403,21 +396,20 @@ int grow(void** p, size_t* cap, size_t need) {
     return MSQ_OK;
 }
 
-int solve_sync(int32_t fmt, int64_t batch, const void* d_src, int64_t rows, int64_t cols, int64_t ld,
-               msq_result* out, void* stream) {
-    if (!out) return MSQ_EINVAL;
-    if (rows == 0 || cols == 0) {
-        if (rows < 0 || cols < 0 || (rows == 0 && cols != 0)) return MSQ_EINVAL;
-        for (int64_t k = 0; k < std::max<int64_t>(batch, 1); ++k) out[k] = msq_result{0, 0, 0, -1, -1};
-        return MSQ_OK;
-    }
+// Solve with the per-device cache; the caller holds C.mu from its own staging
+// (if any) through the result copy, so no other thread's input or workspace
+// can land in between.
+// keys pack global rows and columns into KEY_DIM_BITS each (msq_engine.cuh)
+bool key_range_ok(const msq_plan* pl) {
+    return pl->row_base >= 0 && pl->row_base + pl->rows <= (1ll << msq::KEY_DIM_BITS) - 1 &&
+           pl->cols <= (1ll << msq::KEY_DIM_BITS) - 1;
+}
+
+int solve_locked(DevCache& C, int32_t fmt, int64_t batch, const void* d_src, int64_t rows, int64_t cols, int64_t ld,
+                 msq_result* out, void* stream) {
     msq_plan pl;
     int rc = msq_plan_make(fmt, (int32_t)batch, rows, cols, ld, 0, 0, &pl);
     if (rc) return rc;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return MSQ_ECUDA;
-    DevCache& C = g_cache[dev];
-    std::lock_guard<std::mutex> lk(C.mu);
     if ((rc = grow(&C.ws, &C.ws_bytes, (size_t)std::max<int64_t>(pl.ws_bytes, 256)))) return rc;
     if ((rc = grow((void**)&C.res, &C.res_cap, sizeof(msq_devresult) * (size_t)batch))) return rc;
     if (C.hres_cap < (size_t)batch) {
@@ -443,6 +435,29 @@ int solve_sync(int32_t fmt, int64_t batch, const void* d_src, int64_t rows, int6
     return worst;
 }
 
+bool empty_shape(int64_t batch, int64_t rows, int64_t cols, msq_result* out, int* rc) {
+    if (rows != 0 && cols != 0) return false;
+    if (rows < 0 || cols < 0 || (rows == 0 && cols != 0)) {
+        *rc = MSQ_EINVAL;
+        return true;
+    }
+    for (int64_t k = 0; k < std::max<int64_t>(batch, 1); ++k) out[k] = msq_result{0, 0, 0, -1, -1};
+    *rc = MSQ_OK;
+    return true;
+}
+
+int solve_sync(int32_t fmt, int64_t batch, const void* d_src, int64_t rows, int64_t cols, int64_t ld,
+               msq_result* out, void* stream) {
+    if (!out) return MSQ_EINVAL;
+    int rc;
+    if (empty_shape(batch, rows, cols, out, &rc)) return rc;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return MSQ_ECUDA;
+    DevCache& C = g_cache[dev];
+    std::lock_guard<std::mutex> lk(C.mu);
+    return solve_locked(C, fmt, batch, d_src, rows, cols, ld, out, stream);
+}
+
 }  // namespace
 
 
@@ -454,16 +469,12 @@ int plan_band(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld
 constexpr int kTeamThreads = 32;  // one warp per CTA: fine-grained spread over the SMs
 
 int team_planes(long long rows) { return rows <= 504 ? 9 : 11; }  // rows <= 2^PB - 8
-bool team_single() {  // experiments: MSQ_TEAM_SINGLE=1 keeps one team for a whole matrix
-    const char* f = getenv("MSQ_TEAM_SINGLE");
-    return f && f[0] == '1';
-}
+constexpr int kTeamMaxRows = 2040;  // one team walks <= 2^11 - 8 rows (11 last-zero planes)
 
-bool team_applies(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int32_t nbands) {
-    if (const char* f = getenv("MSQ_ENGINE")) {  // experiments: force one engine where both apply
-        if (f[0] == '0') return false;
-    }
-    const bool forced = getenv("MSQ_ENGINE") && getenv("MSQ_ENGINE")[0] == '1';
+// engine: -1 automatic, 0 band engine, 1 team engine (where it applies)
+bool team_applies(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int32_t nbands, int32_t engine) {
+    if (engine == 0) return false;
+    const bool forced = engine == 1;
     if (nbands > 0 || cols > 1024) return false;
     (void)fmt;
     // batches: one team per matrix (rows <= 2040).  Single matrices: one team
@@ -471,8 +482,8 @@ bool team_applies(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int32_
     // faster than the band engine for every width <= 1024 (512^2 44 vs 152 us,
     // 1024^2 41 vs 158 us, 2000x1000 82 vs 485 us); the single-team chain only
     // when the plan has one band.
-    if (batch > 1) return rows <= 2040;
-    return forced || rows <= 600 || rows <= 2040ll * std::min<long long>(num_sms(), std::max<long long>(1, rows / 64));
+    if (batch > 1) return rows <= kTeamMaxRows;
+    return forced || rows <= 600 || rows <= (long long)kTeamMaxRows * std::min<long long>(num_sms(), std::max<long long>(1, rows / 64));
 }
 
 template <int TEAM, int PB, bool BANDS>
@@ -534,12 +545,18 @@ cudaError_t launch_team(const msq_plan* pl, const void* d_src, msq_devresult* d_
 
 extern "C" int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld, int32_t nbands,
                              int32_t deterministic, msq_plan* plan) {
-    if (!plan) return MSQ_EINVAL;
+    return msq_plan_make_ex(fmt, batch, rows, cols, ld, nbands, deterministic, -1, plan);
+}
+
+extern "C" int msq_plan_make_ex(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld, int32_t nbands,
+                                int32_t deterministic, int32_t engine, msq_plan* plan) {
+    if (!plan || engine < -1 || engine > 1) return MSQ_EINVAL;
     msq_plan p{};
     int rc = plan_band(fmt, batch, rows, cols, ld, nbands, deterministic, &p);
     const bool shape_ok = (fmt == MSQ_FMT_U8 || fmt == MSQ_FMT_BITS) && batch >= 1 && rows >= 1 && cols >= 1 &&
                           (fmt == MSQ_FMT_U8 ? ld >= cols : ld >= (cols + 31) / 32);
-    if (shape_ok && team_applies(fmt, batch, rows, cols, nbands)) {
+    if (engine == 1 && !(shape_ok && team_applies(fmt, batch, rows, cols, nbands, engine))) return MSQ_EINVAL;
+    if (shape_ok && team_applies(fmt, batch, rows, cols, nbands, engine)) {
         if (rc != MSQ_OK) {  // the band plan does not fit: the team engine needs no workspace
             p = msq_plan{};
             p.fmt = fmt;
@@ -671,14 +688,17 @@ int plan_band(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld
 extern "C" {
 
 int msq_launch(const msq_plan* pl, const void* d_src, void* d_ws, msq_devresult* d_result, void* stream) {
+    if (!pl || !key_range_ok(pl)) return MSQ_EINVAL;
     if (pl && pl->engine == 1) {  // register team engine: one launch, no workspace
         if (!d_src || !d_result) return MSQ_EINVAL;
         cudaStream_t st = (cudaStream_t)stream;
         g_last_launches = 0;
         if (cudaMemsetAsync(d_result, 0, sizeof(msq_devresult) * (size_t)pl->batch, st) != cudaSuccess)
             return MSQ_ECUDA;
-        if (pl->batch == 1 && pl->nbands > 1 && d_ws && pl->ws_bytes > 0 && !team_single() &&
-            ceil_div(pl->rows, pl->nbands) <= 2040) {
+        const bool single = (pl->flags & MSQ_PLAN_SINGLE_TEAM) != 0;  // experiments
+        if (pl->batch == 1 && pl->nbands > 1 && !single) {
+            // one matrix on row bands (the plan keeps every band <= kTeamMaxRows)
+            if (!d_ws || pl->ws_bytes <= 0 || ceil_div(pl->rows, pl->nbands) > kTeamMaxRows) return MSQ_EINVAL;
             // one matrix on row bands: a team per band, then carry scan + fix-up
             WsLayout L = ws_layout(pl);
             uint8_t* w = (uint8_t*)d_ws;
@@ -700,6 +720,7 @@ int msq_launch(const msq_plan* pl, const void* d_src, void* d_ws, msq_devresult*
             g_last_launches = 3;
             return MSQ_OK;
         }
+        if (pl->rows > kTeamMaxRows) return MSQ_EINVAL;  // one team walks every row
         cudaError_t e = launch_team(pl, d_src, d_result, st);
         if (e != cudaSuccess) return cuda_status(e);
         g_last_launches = 1;
@@ -925,21 +946,18 @@ int msq_solve_batch_u8(const uint8_t* d_cells, int64_t batch, int64_t rows, int6
 static int solve_host(int32_t fmt, const void* h, int64_t rows, int64_t cols, int64_t ld, msq_result* out,
                       void* stream) {
     if (!out) return MSQ_EINVAL;
-    if (rows == 0 || cols == 0) return solve_sync(fmt, 1, h, rows, cols, ld, out, stream);
+    int rc;
+    if (empty_shape(1, rows, cols, out, &rc)) return rc;
+    if (!h) return MSQ_EINVAL;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return MSQ_ECUDA;
     const size_t bytes = (size_t)rows * (size_t)ld * (fmt == MSQ_FMT_U8 ? 1 : 4);
-    void* din;
-    {
-        DevCache& C = g_cache[dev];
-        std::lock_guard<std::mutex> lk(C.mu);
-        int rc = grow(&C.in, &C.in_bytes, bytes);
-        if (rc) return rc;
-        din = C.in;
-        if (cudaMemcpyAsync(din, h, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream) != cudaSuccess)
-            return MSQ_ECUDA;
-    }
-    return solve_sync(fmt, 1, din, rows, cols, ld, out, stream);
+    DevCache& C = g_cache[dev];
+    std::lock_guard<std::mutex> lk(C.mu);  // held through the solve: the staging buffer is shared
+    if ((rc = grow(&C.in, &C.in_bytes, bytes))) return rc;
+    if (cudaMemcpyAsync(C.in, h, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream) != cudaSuccess)
+        return MSQ_ECUDA;
+    return solve_locked(C, fmt, 1, C.in, rows, cols, ld, out, stream);
 }
 
 int msq_solve_u8_host(const uint8_t* h_cells, int64_t rows, int64_t cols, int64_t ld, msq_result* out,
@@ -953,6 +971,7 @@ int msq_solve_bits_host(const uint32_t* h_words, int64_t rows, int64_t cols, int
 }
 
 int msq_rank_pass1(const msq_plan* pl, const void* d_src, void* d_ws, msq_devresult* d_result, void* stream) {
+    if (pl && !key_range_ok(pl)) return MSQ_EINVAL;
     if (!pl || pl->batch != 1 || !d_src || !d_ws || !d_result || pl->ws_bytes <= 0) return MSQ_EINVAL;
     if (pl->nstage > 0 && ((uintptr_t)d_src % 16) != 0) {
         msq_plan q = *pl;
@@ -973,6 +992,7 @@ int msq_rank_pass1(const msq_plan* pl, const void* d_src, void* d_ws, msq_devres
 }
 
 int msq_rank_seed(const msq_plan* pl, const void* d_src, msq_devresult* d_result, void* stream) {
+    if (pl && !key_range_ok(pl)) return MSQ_EINVAL;
     if (!pl || pl->batch != 1 || !d_src || !d_result) return MSQ_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     if (cudaMemsetAsync(d_result, 0, sizeof(msq_devresult), st) != cudaSuccess) return MSQ_ECUDA;
@@ -984,6 +1004,7 @@ int msq_rank_seed(const msq_plan* pl, const void* d_src, msq_devresult* d_result
 }
 
 int msq_rank_band_pass(const msq_plan* pl, const void* d_src, void* d_ws, msq_devresult* d_result, void* stream) {
+    if (pl && !key_range_ok(pl)) return MSQ_EINVAL;
     if (!pl || pl->batch != 1 || !d_src || !d_ws || !d_result || pl->ws_bytes <= 0) return MSQ_EINVAL;
     if (pl->nstage > 0 && ((uintptr_t)d_src % 16) != 0) {
         msq_plan q = *pl;
@@ -1024,6 +1045,7 @@ int msq_compose_carry(const uint32_t* d_summaries, const int64_t* h_rank_rows, i
 
 int msq_rank_fixup(const msq_plan* pl, void* d_ws, const uint32_t* d_base_carry, msq_devresult* d_result,
                    void* stream) {
+    if (pl && !key_range_ok(pl)) return MSQ_EINVAL;
     if (!pl || !d_ws || !d_result || pl->batch != 1) return MSQ_EINVAL;
     cudaError_t e = launch_carry(pl, d_ws, d_base_carry, (cudaStream_t)stream);
     if (e != cudaSuccess) return MSQ_ECUDA;

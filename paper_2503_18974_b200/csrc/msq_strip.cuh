@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(640, 1) strip_kernel(const StripParams p) {
         const uint32_t PL = lane ? PX : 0u;
         uint32_t cm = X;
 #pragma unroll
-        for (int i = 1; i < 5; ++i) cm &= i < lmin ? __funnelshift_l(PL, X, 8 * i) : 0xFFFFFFFFu;
+        for (int i = 1; i < 5; ++i) cm &= i < lmin ? __funnelshift_lc(PL, X, 8 * i) : 0xFFFFFFFFu;
         cm |= cm >> 16;
         cm |= cm >> 8;
         const uint32_t crows = __reduce_or_sync(0xFFFFFFFFu, cm & 0xFFu);

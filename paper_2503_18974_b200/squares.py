@@ -89,12 +89,19 @@ class Solver:
     """
 
     def __init__(self, fmt: int, rows: int, cols: int, ld: int | None = None, batch: int = 1,
-                 nbands: int = 0, deterministic: bool = False, device=None):
+                 nbands: int = 0, deterministic: bool = False, device=None, engine: int = -1,
+                 flags: int = 0, test_floor: int = 0):
+        """``engine``: -1 automatic, 0 band engine, 1 register team engine.
+        ``flags`` (N.PLAN_*) and ``test_floor`` are experiment / test switches
+        (``test_floor`` presets the shared best side: the caller vouches that
+        the answer is at least that)."""
         torch = _torch()
         self.fmt, self.rows, self.cols, self.batch = fmt, rows, cols, batch
         words = (cols + 31) // 32
         self.ld = ld if ld is not None else (cols if fmt == N.FMT_U8 else words)
-        self.plan = N.plan(fmt, batch, rows, cols, self.ld, nbands, deterministic)
+        self.plan = N.plan(fmt, batch, rows, cols, self.ld, nbands, deterministic, engine)
+        self.plan.flags = flags
+        self.plan.test_floor = test_floor
         self.device = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
         self.ws = torch.empty(max(int(self.plan.ws_bytes), 256), dtype=torch.uint8,

@@ -285,14 +285,9 @@ def test_seed_lower_bound_keeps_ties_exact(torch, fmt):
         _same(got, want)
 
 
-@pytest.fixture
-def team_engine(monkeypatch):
-    """Force the register team engine (msq_team.cuh) for single matrices too."""
-    monkeypatch.setenv("MSQ_ENGINE", "1")
-
-
-def test_team_engine_single_matrices(torch, team_engine):
-    """Team engine on one matrix at a time: odd widths, strides, both formats."""
+def test_team_engine_single_matrices(torch):
+    """Team engine (forced by the plan's engine choice) on one matrix at a
+    time: odd widths, strides, both formats."""
     rng = np.random.default_rng(31)
     for it in range(400):
         rows = int(rng.integers(1, 1200))
@@ -303,12 +298,12 @@ def test_team_engine_single_matrices(torch, team_engine):
         pad = int(rng.choice([0, 0, 16, 5]))
         wide = np.zeros((rows, cols + pad), np.uint8)
         wide[:, :cols] = a
-        s = Solver(N.FMT_U8, rows, cols, ld=cols + pad)
+        s = Solver(N.FMT_U8, rows, cols, ld=cols + pad, engine=1)
         assert int(s.plan.engine) == 1
         _same(s.solve(torch.from_numpy(wide).cuda())[0], want)
         if it % 2 == 0:
             w = grid.pack_bits(a)
-            sb = Solver(N.FMT_BITS, rows, cols, ld=w.shape[1])
+            sb = Solver(N.FMT_BITS, rows, cols, ld=w.shape[1], engine=1)
             assert int(sb.plan.engine) == 1
             _same(sb.solve(torch.from_numpy(w.view(np.int32)).cuda())[0], want)
 
@@ -340,20 +335,20 @@ def test_team_engine_invalid_cells(torch):
         solve_batch(cells)
 
 
-@pytest.mark.parametrize("floor", [96, 120, 150])
-def test_strip_pass_bits(torch, monkeypatch, floor):
+@pytest.mark.parametrize("floor", [96, 120, 150, 200])
+def test_strip_pass_bits(torch, floor):
     """Strip band pass (msq_strip.cuh): bit-packed, several bands, start threshold in its range.
 
-    MSQ_TEST_FLOOR presets the shared best side (a lower bound <= the answer, as
-    the seed provides on large inputs) so the strip pass runs on moderate sizes;
-    planted sides above 222 exercise its hand-back to pass1_kernel."""
-    monkeypatch.setenv("MSQ_TEST_FLOOR", str(floor))
+    The plan's test_floor presets the shared best side (a lower bound <= the
+    answer, as the seed provides on large inputs) so the strip pass runs on
+    moderate sizes; planted sides above 222 exercise its hand-back to
+    pass1_kernel; floor 200 runs the 5-word run filter (t in 191..222)."""
     rng = np.random.default_rng(40 + floor)
     for it in range(14):
         rows = int(rng.integers(300, 2500))
         cols = int(rng.choice([8192, 9000, 16384, 40000, 65536]))
         p = float(rng.choice([0.99, 0.997, 0.999, 0.9995]))
-        k = int(rng.integers(floor, 260 if it % 4 == 0 else 200))
+        k = int(rng.integers(floor, 260 if it % 4 == 0 else max(200, floor + 20)))
         a = _planted(rng, rows, cols, p, min(k, rows))
         if it % 5 == 1:  # a second square of the same side further down-left: ties
             kk = min(k, rows)
@@ -364,7 +359,7 @@ def test_strip_pass_bits(torch, monkeypatch, floor):
             continue
         w = torch.from_numpy(grid.pack_bits(a).view(np.int32)).cuda()
         nb = int(rng.integers(2, min(rows // 8, 150) + 1))
-        _same(Solver(N.FMT_BITS, rows, cols, nbands=nb).solve(w)[0], want)
+        _same(Solver(N.FMT_BITS, rows, cols, nbands=nb, test_floor=floor).solve(w)[0], want)
 
 
 @pytest.mark.parametrize("world", [2, 4])

@@ -1,4 +1,4 @@
-"""Time the cfg4 solve (msq_launch) under env variants; print answer + ms."""
+"""Time the cfg4 solve (msq_launch) under plan variants (flags / test floor); print answer + ms."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -9,14 +9,11 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
 src = configs.cfg4_device() if cfg == "cfg4" else configs.cfg5_device()
 fmt = N.FMT_BITS if cfg == "cfg4" else N.FMT_U8
 spec = configs.CONFIGS[cfg]
-VARIANTS = ({"MSQ_STRIP": "0"}, {}, {"MSQ_TEST_FLOOR": "100"}, {"MSQ_TEST_FLOOR": "120"}, {"MSQ_TEST_FLOOR": "133"},
-            {"MSQ_TEST_FLOOR": "96", "MSQ_NO_SEED": "1"}, {"MSQ_TEST_FLOOR": "120", "MSQ_NO_SEED": "1"},
-            {"MSQ_TEST_FLOOR": "133", "MSQ_NO_SEED": "1"})
+VARIANTS = ({"flags": N.PLAN_NO_STRIP}, {}, {"test_floor": 100}, {"test_floor": 120}, {"test_floor": 133},
+            {"test_floor": 96, "flags": N.PLAN_NO_SEED}, {"test_floor": 120, "flags": N.PLAN_NO_SEED},
+            {"test_floor": 133, "flags": N.PLAN_NO_SEED})
 for env in VARIANTS:
-    for k in ("MSQ_STRIP", "MSQ_TEST_FLOOR", "MSQ_NO_SEED"):
-        os.environ.pop(k, None)
-    os.environ.update(env)
-    s = Solver(fmt, spec["rows"], spec["cols"])
+    s = Solver(fmt, spec["rows"], spec["cols"], **env)
     for _ in range(3):
         s.launch(src)
     torch.cuda.synchronize()
