@@ -464,8 +464,8 @@ def main():
             host_np = host_np.view(np.uint32)
         if not args.no_verify:
             if batch > 1:
-                want = oracle.freq_batch(host_np[:256])
-                got = answer[:256]
+                want = oracle.freq_batch(host_np)  # every matrix of the batch
+                got = answer
             elif fmt == N.FMT_BITS:
                 want = [oracle.freq_bits(host_np, cols)]
                 got = answer

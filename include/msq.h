@@ -161,6 +161,22 @@ int msq_max_rectangle_u8(const uint8_t* d_cells, int64_t rows, int64_t cols, int
 int msq_dp_batch_u8(const uint8_t* d_cells, int64_t batch, int64_t rows, int64_t cols,
                     msq_result* out, void* stream);
 
+/* The DP baselines on any shape (dp_full / dp_rows, squares.py:142-200) by the
+ * row-parallel form dp[i][j] = min(h, w, dp[i-1][j-1] + 1) (msq_rowdp.cuh),
+ * u8 or bit-packed input, rows * cols < 2^40.  Optional outputs for the traced
+ * mode (freq_square_traced, squares.py:129-139): d_heights = [rows][cols]
+ * uint32 column heights after each row (the reference's freq snapshots),
+ * d_rowmax = [rows] int32 largest square ending in each row (found_max_width
+ * after row i = max of rowmax[0..i]).  NULL skips them.  Synchronous. */
+int msq_dp_solve(int32_t fmt, const void* d_src, int64_t rows, int64_t cols, int64_t ld,
+                 uint32_t* d_heights, int32_t* d_rowmax, msq_result* out, void* stream);
+
+/* brute_force_square (squares.py:203-249): one thread per anchor; out->
+ * cells_visited = the reference's raw cell-read count.  rows*cols <= 2^24 (the
+ * Python wrapper applies the reference's cap first).  Synchronous. */
+int msq_brute_u8(const uint8_t* d_cells, int64_t rows, int64_t cols, int64_t ld, msq_result* out,
+                 void* stream);
+
 /* Host-buffer entry points: copy H2D on `stream`, solve, copy the result
  * back (the path a CPU caller of freq_square takes). */
 int msq_solve_u8_host(const uint8_t* h_cells, int64_t rows, int64_t cols, int64_t ld,

@@ -21,12 +21,19 @@ from .grid import (
 )
 from .squares import (
     GPU_SOLVERS,
+    ORACLE_CELL_CAP,
     AllocationAudit,
+    FreqState,
+    OracleCapExceededError,
     Solver,
     SquareResult,
+    brute_force_square,
     dp_batch,
+    dp_full,
+    dp_rows,
     freq_square,
     freq_square_bits,
+    freq_square_traced,
     solve_batch,
 )
 
@@ -37,5 +44,6 @@ __all__ = [
     "MatrixParseError", "RaggedRowsError", "generate_edge_case", "generate_matrix",
     "pack_bits", "parse_matrix", "serialize_matrix", "unpack_bits", "GPU_SOLVERS",
     "AllocationAudit", "Solver", "SquareResult", "freq_square", "freq_square_bits",
-    "solve_batch", "dp_batch", "__version__",
+    "solve_batch", "dp_batch", "dp_full", "dp_rows", "brute_force_square", "freq_square_traced",
+    "FreqState", "ORACLE_CELL_CAP", "OracleCapExceededError", "__version__",
 ]

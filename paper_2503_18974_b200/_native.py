@@ -78,6 +78,8 @@ def load():
         "msq_solve_bits": ([P, I64, I64, I64, RP, P], ctypes.c_int),
         "msq_solve_batch_u8": ([P, I64, I64, I64, RP, P], ctypes.c_int),
         "msq_dp_batch_u8": ([P, I64, I64, I64, RP, P], ctypes.c_int),
+        "msq_dp_solve": ([I32, P, I64, I64, I64, P, P, RP, P], ctypes.c_int),
+        "msq_brute_u8": ([P, I64, I64, I64, RP, P], ctypes.c_int),
         "msq_parse_text": ([P, I64, I64, I64, I32, P, I64, ctypes.POINTER(I64), P], ctypes.c_int),
         "msq_cube_probe": ([P, I64, I64, I64, I64, P, ctypes.POINTER(I64), P], ctypes.c_int),
         "msq_max_rectangle_scratch_bytes": ([I64, I64], I64),

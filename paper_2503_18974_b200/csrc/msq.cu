@@ -20,6 +20,7 @@
 #include "msq_ingest.cuh"
 #include "msq_cube.cuh"
 #include "msq_hist.cuh"
+#include "msq_rowdp.cuh"
 
 namespace {
 
@@ -380,6 +381,8 @@ struct DevCache {
     msq_devresult* hres = nullptr;  // pinned
     size_t hres_cap = 0;
     unsigned* flag = nullptr;  // 16 bytes of device flags (cube probe)
+    void* dpws = nullptr;      // row-DP / brute-force workspace
+    size_t dpws_bytes = 0;
 };
 DevCache g_cache[64];
 
@@ -1101,3 +1104,107 @@ const char* msq_version(void) { return "msq 0.1.0 sm_100a"; }
 const char* msq_last_cuda_error(void) { return g_last_err; }
 
 }  // extern "C"
+
+// ------------------------------------------------------ DP baselines, traced
+namespace {
+int64_t rowdp_strips(int32_t fmt, int64_t cols) { return ceil_div(cols, 32 * (fmt == MSQ_FMT_BITS ? 32 : 16)); }
+
+void decode_rowdp(unsigned long long key, int64_t rows, int64_t cols, bool key_is_anchor, msq_result* out) {
+    if (!key) {
+        *out = msq_result{0, 0, rows * cols, -1, -1};
+        return;
+    }
+    const int64_t side = (int64_t)(key >> msq::ROWDP_LIN_BITS);
+    const int64_t lin = (int64_t)(((1ull << msq::ROWDP_LIN_BITS) - 1ull) - (key & ((1ull << msq::ROWDP_LIN_BITS) - 1ull)));
+    const int64_t r = lin / cols, c = lin % cols;
+    if (key_is_anchor) *out = msq_result{side, side * side, rows * cols, r, c};
+    else *out = msq_result{side, side * side, rows * cols, r - side + 1, c - side + 1};
+}
+}  // namespace
+
+extern "C" int msq_dp_solve(int32_t fmt, const void* d_src, int64_t rows, int64_t cols, int64_t ld,
+                            uint32_t* d_heights, int32_t* d_rowmax, msq_result* out, void* stream) {
+    if (!out || (fmt != MSQ_FMT_U8 && fmt != MSQ_FMT_BITS)) return MSQ_EINVAL;
+    int rc;
+    if (empty_shape(1, rows, cols, out, &rc)) return rc;
+    const int64_t words = ceil_div(cols, 32);
+    if (!d_src || ld < (fmt == MSQ_FMT_U8 ? cols : words) || rows * cols >= (1ll << msq::ROWDP_LIN_BITS) ||
+        cols >= (1ll << 31) - 64)
+        return MSQ_EINVAL;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return MSQ_ECUDA;
+    DevCache& C = g_cache[dev];
+    std::lock_guard<std::mutex> lk(C.mu);
+    const int64_t nstrips = rowdp_strips(fmt, cols);
+    const size_t bnd_bytes = (size_t)std::max<int64_t>(nstrips - 1, 0) * (size_t)rows * 8;
+    const size_t need = 64 + bnd_bytes;
+    if ((rc = grow(&C.dpws, &C.dpws_bytes, need))) return rc;
+    if (C.hres_cap < 1) {
+        if (cudaMallocHost((void**)&C.hres, sizeof(msq_devresult)) != cudaSuccess) return MSQ_ENOMEM;
+        C.hres_cap = 1;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemsetAsync(C.dpws, 0, need, st) != cudaSuccess) return MSQ_ECUDA;
+    if (d_rowmax && cudaMemsetAsync(d_rowmax, 0, sizeof(int32_t) * (size_t)rows, st) != cudaSuccess)
+        return MSQ_ECUDA;
+    unsigned char* base = (unsigned char*)C.dpws;
+    msq::RowDpParams p;
+    p.src = (const uint8_t*)d_src;
+    p.ld = ld;
+    p.rows = rows;
+    p.cols = cols;
+    p.nstrips = (int)nstrips;
+    p.vec = (fmt == MSQ_FMT_U8 && ((uintptr_t)d_src % 16) == 0 && ld % 16 == 0 && cols % 16 == 0) ? 1 : 0;
+    p.key = (unsigned long long*)base;
+    p.status = (unsigned int*)(base + 16);
+    p.ticket = (unsigned int*)(base + 20);
+    p.bnd = (unsigned long long*)(base + 64);
+    p.heights = d_heights;
+    p.rowmax = d_rowmax;
+    const int grid = (int)ceil_div(nstrips, msq::ROWDP_WARPS);
+    if (fmt == MSQ_FMT_BITS) msq::rowdp_kernel<true><<<grid, 32 * msq::ROWDP_WARPS, 0, st>>>(p);
+    else msq::rowdp_kernel<false><<<grid, 32 * msq::ROWDP_WARPS, 0, st>>>(p);
+    g_last_launches = 1;
+    if (cudaGetLastError() != cudaSuccess) return MSQ_ECUDA;
+    if (cudaMemcpyAsync(C.hres, base, 32, cudaMemcpyDeviceToHost, st) != cudaSuccess) return MSQ_ECUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return MSQ_ECUDA;
+    const unsigned long long key = *(const unsigned long long*)C.hres;
+    const unsigned status = *(const unsigned*)((const unsigned char*)C.hres + 16);
+    decode_rowdp(key, rows, cols, false, out);
+    return (status & 1u) ? MSQ_EVALUE : MSQ_OK;
+}
+
+extern "C" int msq_brute_u8(const uint8_t* d_cells, int64_t rows, int64_t cols, int64_t ld, msq_result* out,
+                            void* stream) {
+    if (!out) return MSQ_EINVAL;
+    int rc;
+    if (empty_shape(1, rows, cols, out, &rc)) return rc;
+    if (!d_cells || ld < cols || rows * cols > (1ll << 24)) return MSQ_EINVAL;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return MSQ_ECUDA;
+    DevCache& C = g_cache[dev];
+    std::lock_guard<std::mutex> lk(C.mu);
+    if ((rc = grow(&C.dpws, &C.dpws_bytes, 64))) return rc;
+    if (C.hres_cap < 1) {
+        if (cudaMallocHost((void**)&C.hres, sizeof(msq_devresult)) != cudaSuccess) return MSQ_ENOMEM;
+        C.hres_cap = 1;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemsetAsync(C.dpws, 0, 64, st) != cudaSuccess) return MSQ_ECUDA;
+    unsigned char* base = (unsigned char*)C.dpws;
+    const int64_t n = rows * cols;
+    msq::brute_kernel<<<(int)ceil_div(n, 256), 256, 0, st>>>(d_cells, ld, (int)rows, (int)cols,
+                                                             (unsigned long long*)base,
+                                                             (unsigned long long*)(base + 8),
+                                                             (unsigned int*)(base + 16));
+    g_last_launches = 1;
+    if (cudaGetLastError() != cudaSuccess) return MSQ_ECUDA;
+    if (cudaMemcpyAsync(C.hres, base, 32, cudaMemcpyDeviceToHost, st) != cudaSuccess) return MSQ_ECUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return MSQ_ECUDA;
+    const unsigned long long key = *(const unsigned long long*)C.hres;
+    const unsigned long long visited = *(const unsigned long long*)((const unsigned char*)C.hres + 8);
+    const unsigned status = *(const unsigned*)((const unsigned char*)C.hres + 16);
+    decode_rowdp(key, rows, cols, true, out);
+    out->cells_visited = (int64_t)visited;
+    return (status & 1u) ? MSQ_EVALUE : MSQ_OK;
+}

@@ -14,6 +14,12 @@ Reference interface (/root/reference/pkg/src/squarelab/squares.py):
   2-D numpy uint8 array, or a 2-D torch uint8 tensor (host or CUDA).
 * ``ValueError`` for cells outside {0, 1} (grid.py:61-62); other library
   errors raise ``MsqError`` (a RuntimeError).
+* The other routes of the reference, same signatures and audit contracts, on
+  the GPU too: ``dp_full`` / ``dp_rows`` (:142-200, the row-parallel DP kernel
+  of csrc/msq_rowdp.cuh), ``brute_force_square`` (:203-249, one thread per
+  anchor, the reference's cap and cell-read count), and
+  ``freq_square_traced`` / ``FreqState`` (:33-45, :129-139: the result of
+  ``freq_square`` plus per-row height snapshots dumped by the DP kernel).
 
 Every call runs the sm_100a kernels in libmsq.so; there is no CPU path.
 """
@@ -26,6 +32,26 @@ from typing import Callable
 import numpy as np
 
 from . import _native as N
+
+
+ORACLE_CELL_CAP = 10_000  # squares.py:17
+
+
+class OracleCapExceededError(ValueError):
+    """Input too large for the brute-force oracle (squares.py:20-21)."""
+
+
+@dataclass(frozen=True, slots=True)
+class FreqState:
+    """Frequency-solver state after a row (squares.py:33-45): the column
+    heights, the best side so far, both thresholds (= best + 1) and the
+    counter (0 at every row end, squares.py:102-103)."""
+
+    freq: tuple[int, ...]
+    found_max_width: int
+    check_max_width: int
+    check_max_height: int
+    counter: int
 
 
 @dataclass(frozen=True, slots=True)
@@ -195,6 +221,110 @@ def freq_square(m, audit: AllocationAudit | None = None) -> SquareResult:
     N.check(N.load().msq_solve_u8_host(a.ctypes.data_as(ctypes.c_void_p), rows, cols, cols,
                                        ctypes.byref(out), _stream_handle()))
     return _to_result(out)
+
+
+def _device_u8(m):
+    """(rows, cols, CUDA uint8 tensor [rows, cols]) for a BinaryMatrix-like,
+    numpy array or torch tensor."""
+    torch = _torch()
+    if isinstance(m, torch.Tensor):
+        if m.dim() != 2:
+            raise ValueError("expected a 2-D binary matrix")
+        rows, cols = int(m.shape[0]), int(m.shape[1])
+        t = m if m.dtype == torch.uint8 else m.to(torch.uint8)
+        return rows, cols, (t if t.is_cuda else t.cuda()).contiguous()
+    rows, cols, a = _host_u8(m)
+    if rows < 0 or cols < 0 or (rows == 0 and cols != 0):
+        raise ValueError("empty matrix must be 0x0")
+    if rows == 0 or cols == 0:
+        return rows, cols, None
+    _stream_handle()  # raises without a device
+    a = np.ascontiguousarray(a)
+    return rows, cols, torch.from_numpy(a if a.flags.writeable else a.copy()).cuda()
+
+
+def _dp_solve(t, rows: int, cols: int, heights=None, rowmax=None) -> SquareResult:
+    out = N.MsqResult()
+    hp = ctypes.c_void_p(heights.data_ptr()) if heights is not None else None
+    rp = ctypes.c_void_p(rowmax.data_ptr()) if rowmax is not None else None
+    N.check(N.load().msq_dp_solve(N.FMT_U8, ctypes.c_void_p(t.data_ptr()), rows, cols, cols, hp, rp,
+                                  ctypes.byref(out), _stream_handle()))
+    return _to_result(out)
+
+
+def dp_full(m, audit: AllocationAudit | None = None) -> SquareResult:
+    """Full-table DP (squares.py:142-171) on the GPU: dp = min(up, left, diag) + 1
+    evaluated row-parallel as min(height, row run, diag + 1) (msq_rowdp.cuh).
+    Same result as the reference plus the location of the first strict
+    improvement; the audit records the reference's rows*cols table."""
+    rows, cols, t = _device_u8(m)
+    if rows == 0 or cols == 0:
+        return SquareResult(0, 0, 0)
+    if audit is not None:
+        audit.add(rows * cols)  # squares.py:152-153
+    return _dp_solve(t, rows, cols)
+
+
+def dp_rows(m, audit: AllocationAudit | None = None) -> SquareResult:
+    """Row-rolling DP (squares.py:174-200): same recurrence and kernel as
+    dp_full; the audit records the reference's two rolling rows (2*cols)."""
+    rows, cols, t = _device_u8(m)
+    if rows == 0 or cols == 0:
+        return SquareResult(0, 0, 0)
+    if audit is not None:
+        audit.add(2 * cols)  # squares.py:181-182
+    return _dp_solve(t, rows, cols)
+
+
+def brute_force_square(m, audit: AllocationAudit | None = None,
+                       cap: int = ORACLE_CELL_CAP) -> SquareResult:
+    """Direct oracle (squares.py:203-249): every anchor grows its square on the
+    GPU, one thread per anchor; cells_visited is the reference's raw read count
+    (which exceeds rows*cols).  Raises OracleCapExceededError past `cap`."""
+    if hasattr(m, "rows") and hasattr(m, "cols") and not hasattr(m, "dim"):
+        rows, cols = int(m.rows), int(m.cols)
+    else:
+        shp = getattr(m, "shape", None) or np.asarray(m).shape
+        rows, cols = (int(shp[0]), int(shp[1])) if len(shp) == 2 else (0, 0)
+    if rows * cols > cap:
+        raise OracleCapExceededError(
+            f"{rows}x{cols} = {rows * cols} cells exceeds oracle cap {cap}")
+    if audit is not None:
+        audit.add(0)  # no auxiliary storage (squares.py:219-220)
+    rows, cols, t = _device_u8(m)
+    if rows == 0 or cols == 0:
+        return SquareResult(0, 0, 0)
+    out = N.MsqResult()
+    N.check(N.load().msq_brute_u8(ctypes.c_void_p(t.data_ptr()), rows, cols, cols,
+                                  ctypes.byref(out), _stream_handle()))
+    return _to_result(out)
+
+
+def freq_square_traced(m, audit: AllocationAudit | None = None
+                       ) -> tuple[SquareResult, list[FreqState]]:
+    """freq_square plus a FreqState after each row (squares.py:129-139).
+
+    The result is freq_square's (the band kernels).  The snapshots come from
+    the row-DP kernel's per-row height dump: freq = the column heights after
+    row i, found_max_width = the largest square ending in rows 0..i (what
+    Algorithm 1 has found after row i), thresholds = found + 1,
+    counter = 0.  Memory is O(rows * cols), as in the reference.
+    """
+    torch = _torch()
+    rows, cols, t = _device_u8(m)
+    if rows == 0 or cols == 0:
+        return SquareResult(0, 0, 0), []
+    result = freq_square(t, audit)
+    heights = torch.empty((rows, cols), dtype=torch.int32, device=t.device)
+    rowmax = torch.empty(rows, dtype=torch.int32, device=t.device)
+    dp = _dp_solve(t, rows, cols, heights, rowmax)
+    found = torch.cummax(rowmax, 0).values.cpu().numpy()
+    h = heights.cpu().numpy()
+    if dp.side != result.side or int(found[-1]) != result.side:
+        raise N.MsqError("traced snapshots disagree with freq_square")
+    snaps = [FreqState(tuple(h[i].tolist()), int(found[i]), int(found[i]) + 1,
+                       int(found[i]) + 1, 0) for i in range(rows)]
+    return result, snaps
 
 
 def freq_square_bits(words, cols: int) -> SquareResult:

@@ -1,0 +1,134 @@
+"""GPU parity at the shapes the round-1 suite left out.
+
+* cfg3 / cfg4 answers pinned to the REFERENCE implementation itself on the
+  same bytes (tests/golden/large.json, made by make_large_golden.py from
+  squarelab._freq_core, squares.py:68-114), checked through sha256 of the
+  device-generated input;
+* matrices with more than 65,535 rows (carry heights clamp at 65535, many
+  bands, rank row bases);
+* packed 65536^2 all-ones / all-zeros (side 65536, area 2^32);
+* bit-packed inputs >= 8192^2 whose answers lie below and above the strip
+  pass's threshold window [96, 222] (hand-off to pass1_kernel), through the
+  automatic path (no test floor).
+Every answer is compared on (side, area, cells_visited, top, left).
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2503_18974_b200 import configs, grid
+from paper_2503_18974_b200.squares import freq_square, freq_square_bits
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    from paper_2503_18974_b200 import build
+    build.build()
+    return t
+
+
+def _same(res, want):
+    assert (res.side, res.area, res.cells_visited, res.top, res.left) == (
+        want.side, want.area, want.cells_visited, want.top, want.left)
+
+
+def _pin(res, rec):
+    assert (res.side, res.area, res.cells_visited, res.top, res.left) == (
+        rec["side"], rec["area"], rec["cells_visited"], rec["top"], rec["left"])
+
+
+def _large():
+    with open(os.path.join(GOLDEN, "large.json")) as f:
+        return json.load(f)
+
+
+def test_cfg3_reference_pin(torch):
+    g = _large()
+    m = configs.cfg3_device()
+    assert hashlib.sha256(m.cpu().numpy().tobytes()).hexdigest() == g["cfg3"]["sha256_u8"]
+    _pin(freq_square(m), g["cfg3"])
+    z = torch.zeros((16384, 16384), dtype=torch.uint8, device="cuda")
+    _pin(freq_square(z), g["cfg3_all_zeros"])
+    z.fill_(1)
+    _pin(freq_square(z), g["cfg3_all_ones"])
+
+
+@pytest.mark.slow
+def test_cfg4_reference_pin(torch):
+    g = _large()
+    if "cfg4" not in g:
+        pytest.skip("cfg4 reference pin not generated")
+    w = configs.cfg4_device()
+    assert hashlib.sha256(w.cpu().numpy().tobytes()).hexdigest() == g["cfg4"]["sha256_bits"]
+    _pin(freq_square_bits(w, 65536), g["cfg4"])
+
+
+@pytest.mark.slow
+def test_packed_65536_all_ones_and_zeros(torch):
+    n = 65536
+    w = torch.zeros((n, n // 32), dtype=torch.int32, device="cuda")
+    r = freq_square_bits(w, n)
+    assert (r.side, r.area, r.cells_visited, r.top, r.left) == (0, 0, n * n, -1, -1)
+    w.fill_(-1)
+    r = freq_square_bits(w, n)
+    assert (r.side, r.area, r.cells_visited, r.top, r.left) == (n, n * n, n * n, 0, 0)
+    # one zero cell at the centre (k, k):
+    w[n // 2, (n // 2) // 32] = ~np.int32(1)
+    r = freq_square_bits(w, n)
+    # every (k+1)-window of rows (and of columns) contains row (column) k, so the
+    # answer is the side-k square at (0, 0)
+    k = n // 2
+    assert (r.side, r.top, r.left) == (k, 0, 0)
+
+
+@pytest.mark.parametrize("fmt", ["u8", "bits"])
+def test_tall_matrices_over_65535_rows(torch, fmt):
+    """rows >= 2^17, cols <= 64: column heights > 65535 (carry clamp), many bands."""
+    rng = np.random.default_rng(170 if fmt == "u8" else 171)
+    for rows, cols, p in [(140000, 48, 0.995), (200000, 64, 0.999), (131072, 17, 1.0),
+                          (150001, 33, 0.9999)]:
+        a = (rng.random((rows, cols)) < p).astype(np.uint8)
+        if p < 1.0:
+            # a long all-ones column band (heights pass 65535), then a square at its bottom
+            a[10:90000, 3:9] = 1
+            k = min(cols - 2, 40)
+            a[120000 - k:120000, 1:1 + k] = 1
+        want = oracle.freq(a)
+        if fmt == "u8":
+            got = freq_square(torch.from_numpy(a).cuda())
+        else:
+            got = freq_square_bits(torch.from_numpy(grid.pack_bits(a).view(np.int32)).cuda(), cols)
+        _same(got, want)
+
+
+@pytest.mark.parametrize("case", ["small_side", "planted_300", "planted_1000"])
+def test_bits_answers_outside_strip_window(torch, case):
+    """>= 8192^2 bit-packed through the automatic path: answers < 96 (no strip
+    pass) and > 222 (the strip pass hands its bands back to pass1_kernel)."""
+    n = 8192
+    seed = {"small_side": 11, "planted_300": 12, "planted_1000": 13}[case]
+    p = 0.99 if case == "small_side" else 0.999
+    w = configs.device_hash("bits", seed, p, n, n)
+    host = w.cpu().numpy().view(np.uint32).copy()
+    if case != "small_side":
+        k = 300 if case == "planted_300" else 1000
+        rng = np.random.default_rng(seed)
+        top, left = int(rng.integers(0, n - k)), int(rng.integers(0, n - k))
+        a = grid.unpack_bits(host, n)
+        a[top:top + k, left:left + k] = 1
+        host = grid.pack_bits(a)
+        w = torch.from_numpy(host.view(np.int32)).cuda()
+    want = oracle.freq_bits(host, n)
+    if case == "small_side":
+        assert want.side < 96
+    else:
+        assert want.side > 222
+    _same(freq_square_bits(w, n), want)

@@ -188,7 +188,7 @@ def test_cfg1(torch):
 
 
 def test_cfg2_batch_vs_oracle(torch):
-    cells = configs.cfg2_array(count=512)
+    cells = configs.cfg2_array()  # all 4096 matrices of the config
     got = solve_batch(cells)
     want = oracle.freq_batch(cells)
     for g_, w_ in zip(got, want):
