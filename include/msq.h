@@ -117,7 +117,10 @@ int msq_launch(const msq_plan* plan, const void* d_src, void* d_ws, msq_devresul
  * status flags an invalid cell. */
 int msq_decode(const msq_devresult* r, int64_t rows, int64_t cols, msq_result* out);
 
-/* Synchronous convenience calls (internal per-device workspace). */
+/* Synchronous convenience calls (internal per-device workspace).  Single
+ * matrices past the band engine's ranges (cols > 65536 or rows >= 2^21 - 1)
+ * are solved by the row-parallel DP kernel (msq_dp_solve): same result, any
+ * shape with rows * cols < 2^40. */
 int msq_solve_u8(const uint8_t* d_cells, int64_t rows, int64_t cols, int64_t ld,
                  msq_result* out, void* stream);
 int msq_solve_bits(const uint32_t* d_words, int64_t rows, int64_t cols, int64_t ld_words,

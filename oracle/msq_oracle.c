@@ -62,7 +62,7 @@ static inline void fetch_row(const void* src, int fmt, int64_t ld, int64_t i, in
  */
 static uint64_t freq_core(const void* src, int fmt, int64_t ld, int64_t r0, int64_t r1,
                           int64_t cols, int64_t found0, int64_t* freq, uint8_t* buf,
-                          int64_t* found_out) {
+                          int64_t* found_out, int64_t* last_ij) {
     int64_t found = found0;
     int64_t check_w = found0 + 1, check_h = found0 + 1;
     int64_t counter = 0;
@@ -81,6 +81,7 @@ static uint64_t freq_core(const void* src, int fmt, int64_t ld, int64_t r0, int6
                         check_h += 1;
                         counter = 0;
                         key = orc_pack_key(found, i, j);
+                        if (last_ij) { last_ij[0] = i; last_ij[1] = j; }
                     }
                     continue; /* a satisfied column skips the trailing reset */
                 }
@@ -106,10 +107,16 @@ static int solve_freq(const void* src, int fmt, int64_t ld, int64_t rows, int64_
     int64_t* freq = (int64_t*)calloc((size_t)cols, sizeof(int64_t));
     uint8_t* buf = (uint8_t*)malloc((size_t)cols);
     if (!freq || !buf) { free(freq); free(buf); return 2; }
-    uint64_t key = freq_core(src, fmt, ld, 0, rows, cols, 0, freq, buf, NULL);
+    /* the location is kept unpacked: any shape (the key packs 21-bit rows) */
+    int64_t found = 0, ij[2] = {-1, -1};
+    freq_core(src, fmt, ld, 0, rows, cols, 0, freq, buf, &found, ij);
     free(freq);
     free(buf);
-    result_from_key(key, rows, cols, out);
+    out->side = found;
+    out->area = found * found;
+    out->cells_visited = rows * cols;
+    out->top = found ? ij[0] - found + 1 : -1;
+    out->left = found ? ij[1] - found + 1 : -1;
     return 0;
 }
 
@@ -147,8 +154,7 @@ int orc_dp_u8(const uint8_t* cells, int64_t rows, int64_t cols, int64_t ld, orc_
     int64_t* prev = (int64_t*)calloc((size_t)cols, sizeof(int64_t));
     int64_t* cur = (int64_t*)calloc((size_t)cols, sizeof(int64_t));
     if (!prev || !cur) { free(prev); free(cur); return 2; }
-    int64_t best = 0;
-    uint64_t key = 0;
+    int64_t best = 0, bi = -1, bj = -1;
     for (int64_t i = 0; i < rows; ++i) {
         const uint8_t* row = cells + i * ld;
         for (int64_t j = 0; j < cols; ++j) {
@@ -163,7 +169,7 @@ int orc_dp_u8(const uint8_t* cells, int64_t rows, int64_t cols, int64_t ld, orc_
                     v = m + 1;
                 }
                 cur[j] = v;
-                if (v > best) { best = v; key = orc_pack_key(v, i, j); }
+                if (v > best) { best = v; bi = i; bj = j; }
             } else {
                 cur[j] = 0;
             }
@@ -172,7 +178,11 @@ int orc_dp_u8(const uint8_t* cells, int64_t rows, int64_t cols, int64_t ld, orc_
     }
     free(prev);
     free(cur);
-    result_from_key(key, rows, cols, out);
+    out->side = best;
+    out->area = best * best;
+    out->cells_visited = rows * cols;
+    out->top = best ? bi - best + 1 : -1;
+    out->left = best ? bj - best + 1 : -1;
     return 0;
 }
 
@@ -191,7 +201,7 @@ int orc_band_pass(const void* src, int fmt, int64_t ld, int64_t r0, int64_t r1, 
     if (!freq || !buf || !first0) { free(freq); free(buf); free(first0); return 2; }
     for (int64_t j = 0; j < cols; ++j) first0[j] = H;
     /* leading-ones depth needs a second look at the rows; do it alongside */
-    *key = freq_core(src, fmt, ld, r0, r1, cols, t0 - 1, freq, buf, NULL);
+    *key = freq_core(src, fmt, ld, r0, r1, cols, t0 - 1, freq, buf, NULL, NULL);
     for (int64_t i = r0; i < r1; ++i) {
         fetch_row(src, fmt, ld, i, cols, buf);
         for (int64_t j = 0; j < cols; ++j)

@@ -408,8 +408,21 @@ bool key_range_ok(const msq_plan* pl) {
            pl->cols <= (1ll << msq::KEY_DIM_BITS) - 1;
 }
 
+int dp_solve_locked(DevCache& C, int32_t fmt, const void* d_src, int64_t rows, int64_t cols, int64_t ld,
+                    uint32_t* d_heights, int32_t* d_rowmax, msq_result* out, void* stream);
+bool dp_shape_ok(int32_t fmt, int64_t rows, int64_t cols, int64_t ld);
+
+// shapes past the band engine's key and carry ranges (cols > 65536 or
+// rows >= 2^21 - 1): solved by the row-parallel DP kernel (msq_rowdp.cuh),
+// whose 40-bit linear-index key covers any matrix that fits in memory
+bool beyond_band_engine(int64_t rows, int64_t cols) {
+    return cols > (int64_t)kMaxWords * 32 || rows >= (1ll << msq::KEY_DIM_BITS) - 1;
+}
+
 int solve_locked(DevCache& C, int32_t fmt, int64_t batch, const void* d_src, int64_t rows, int64_t cols, int64_t ld,
                  msq_result* out, void* stream) {
+    if (batch == 1 && beyond_band_engine(rows, cols) && dp_shape_ok(fmt, rows, cols, ld))
+        return dp_solve_locked(C, fmt, d_src, rows, cols, ld, nullptr, nullptr, out, stream);
     msq_plan pl;
     int rc = msq_plan_make(fmt, (int32_t)batch, rows, cols, ld, 0, 0, &pl);
     if (rc) return rc;
@@ -1122,19 +1135,11 @@ void decode_rowdp(unsigned long long key, int64_t rows, int64_t cols, bool key_i
 }
 }  // namespace
 
-extern "C" int msq_dp_solve(int32_t fmt, const void* d_src, int64_t rows, int64_t cols, int64_t ld,
-                            uint32_t* d_heights, int32_t* d_rowmax, msq_result* out, void* stream) {
-    if (!out || (fmt != MSQ_FMT_U8 && fmt != MSQ_FMT_BITS)) return MSQ_EINVAL;
+namespace {
+// caller holds C.mu
+int dp_solve_locked(DevCache& C, int32_t fmt, const void* d_src, int64_t rows, int64_t cols, int64_t ld,
+                    uint32_t* d_heights, int32_t* d_rowmax, msq_result* out, void* stream) {
     int rc;
-    if (empty_shape(1, rows, cols, out, &rc)) return rc;
-    const int64_t words = ceil_div(cols, 32);
-    if (!d_src || ld < (fmt == MSQ_FMT_U8 ? cols : words) || rows * cols >= (1ll << msq::ROWDP_LIN_BITS) ||
-        cols >= (1ll << 31) - 64)
-        return MSQ_EINVAL;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return MSQ_ECUDA;
-    DevCache& C = g_cache[dev];
-    std::lock_guard<std::mutex> lk(C.mu);
     const int64_t nstrips = rowdp_strips(fmt, cols);
     const size_t bnd_bytes = (size_t)std::max<int64_t>(nstrips - 1, 0) * (size_t)rows * 8;
     const size_t need = 64 + bnd_bytes;
@@ -1172,6 +1177,26 @@ extern "C" int msq_dp_solve(int32_t fmt, const void* d_src, int64_t rows, int64_
     const unsigned status = *(const unsigned*)((const unsigned char*)C.hres + 16);
     decode_rowdp(key, rows, cols, false, out);
     return (status & 1u) ? MSQ_EVALUE : MSQ_OK;
+}
+
+bool dp_shape_ok(int32_t fmt, int64_t rows, int64_t cols, int64_t ld) {
+    const int64_t words = ceil_div(cols, 32);
+    return ld >= (fmt == MSQ_FMT_U8 ? cols : words) && rows * cols < (1ll << msq::ROWDP_LIN_BITS) &&
+           cols < (1ll << 31) - 64;
+}
+}  // namespace
+
+extern "C" int msq_dp_solve(int32_t fmt, const void* d_src, int64_t rows, int64_t cols, int64_t ld,
+                            uint32_t* d_heights, int32_t* d_rowmax, msq_result* out, void* stream) {
+    if (!out || (fmt != MSQ_FMT_U8 && fmt != MSQ_FMT_BITS)) return MSQ_EINVAL;
+    int rc;
+    if (empty_shape(1, rows, cols, out, &rc)) return rc;
+    if (!d_src || !dp_shape_ok(fmt, rows, cols, ld)) return MSQ_EINVAL;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return MSQ_ECUDA;
+    DevCache& C = g_cache[dev];
+    std::lock_guard<std::mutex> lk(C.mu);
+    return dp_solve_locked(C, fmt, d_src, rows, cols, ld, d_heights, d_rowmax, out, stream);
 }
 
 extern "C" int msq_brute_u8(const uint8_t* d_cells, int64_t rows, int64_t cols, int64_t ld, msq_result* out,

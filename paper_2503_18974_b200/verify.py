@@ -159,3 +159,39 @@ def random_campaign(count: int, max_dim: int, densities: set[float], seed: int,
         _check(report, f"random#{index}", stack[index, :rows, :cols], f, d, cpu_solvers)
     report.elapsed = time.perf_counter() - start
     return report
+
+
+def edge_case_suite() -> VerifyReport:
+    """The edge cases of verify.py:218-251 -- constant matrices and the empty
+    matrix -- on the GPU: the frequency solver (freq_square) against the DP
+    kernel (dp_full), both against the analytically known area, and the
+    implied location ((0, 0) for a square, none for side 0)."""
+    from .grid import EMPTY_MATRIX, EdgeKind, generate_edge_case
+    from .squares import dp_full, freq_square
+    cases = [
+        ("all_zeros_100", generate_edge_case(EdgeKind.ALL_ZEROS, 100), 0),
+        ("all_ones_100", generate_edge_case(EdgeKind.ALL_ONES, 100), 10_000),
+        ("single_row_1000", generate_edge_case(EdgeKind.SINGLE_ROW, 1000), 1),
+        ("single_col_1000", generate_edge_case(EdgeKind.SINGLE_COL, 1000), 1),
+        ("empty", EMPTY_MATRIX, 0),
+    ]
+    report = VerifyReport()
+    start = time.perf_counter()
+    for case_id, matrix, expected_area in cases:
+        a, b = freq_square(matrix), dp_full(matrix)
+        report.launches += 2
+        locs = (("gpu_freq", a.top, a.left), ("gpu_dp", b.top, b.left))
+        if a.side != b.side or locs[0][1:] != locs[1][1:]:
+            report.mismatches.append(
+                Mismatch(case_id, matrix, (("gpu_freq", a.side), ("gpu_dp", b.side)), locs))
+        for name, result in (("gpu_freq", a), ("gpu_dp", b)):
+            if result.area != expected_area:
+                report.invariant_failures.append(InvariantFailure(
+                    case_id, -1, f"{name} area {result.area}, expected {expected_area}"))
+            want_loc = (0, 0) if expected_area else (-1, -1)
+            if (result.top, result.left) != want_loc:
+                report.invariant_failures.append(InvariantFailure(
+                    case_id, -1, f"{name} location {(result.top, result.left)}, expected {want_loc}"))
+        report.cases_run += 1
+    report.elapsed = time.perf_counter() - start
+    return report

@@ -110,3 +110,19 @@ def test_dp_cfg3_equals_freq(torch):
     m = configs.cfg3_device()
     a, b = dp_full(m), freq_square(m)
     assert (a.side, a.top, a.left) == (b.side, b.top, b.left) == (2048, 3898, 9709)
+
+
+@pytest.mark.parametrize("shape", [(300, 70000), (2 ** 21 + 5, 3)])
+def test_freq_square_beyond_band_engine(torch, shape):
+    """cols > 65536 / rows >= 2^21: the drop-in freq_square still answers (the
+    library routes such shapes to the DP kernel); host and device inputs."""
+    from paper_2503_18974_b200 import freq_square_bits
+    from paper_2503_18974_b200.grid import pack_bits
+    rows, cols = shape
+    rng = np.random.default_rng(rows + cols)
+    a = (rng.random((rows, cols)) < 0.97).astype(np.uint8)
+    want = oracle.freq(a)
+    for got in (freq_square(a), freq_square(torch.from_numpy(a).cuda()),
+                freq_square_bits(pack_bits(a), cols)):
+        assert (got.side, got.area, got.cells_visited, got.top, got.left) == (
+            want.side, want.area, want.cells_visited, want.top, want.left)
