@@ -10,13 +10,18 @@ Bernoulli(0.999)), the matrix BASELINE.json's scaling target names; it is row-
 band sharded across the N ranks (strong scaling: the matrix is fixed).
 
 Rank 0 prints ONE JSON line.  Extra keys: roofline (dominant kernel = band
-pass, algorithmic bytes = input bytes per launch), cpu_baseline (the oracle
-port on the host, bounded sample), e2e (host buffers through the C ABI with the
-H2D copy inside the timed region), clocks (NVML sampled during the timed
-region), gpu_launches.
+pass, algorithmic bytes = input bytes per launch), cpu_baseline (the
+reference's own Python freq_square and dp_full from baseline/_ref, single
+threaded as its contract says, reference bench semantics, bounded sample), e2e
+(the public API -- freq_square_bits / freq_square / solve_batch -- on a
+pageable numpy array, H2D copy and result read-back inside the timed region),
+clocks (NVML sampled during the timed region), gpu_launches.  Inputs smaller
+than L2 get a 256 MiB flush before every step, outside the step's events.
 
---impl reference times the reference algorithm's CPU implementation (the C
-restatement in oracle/, the reference being pure Python) on the host cores.
+--impl reference solves the WHOLE configured matrix every step with the
+reference algorithm's CPU implementation (the C restatement in oracle/ -- the
+reference being pure Python -- per row band on all host threads plus the band
+combine), on the same bytes for cfg1-cfg4.
 """
 from __future__ import annotations
 
@@ -140,62 +145,151 @@ def build_input(cfg: str, torch, rank: int, world: int):
     return full[r0:r1].contiguous(), fmt, spec
 
 
-def cpu_baseline_sample(cfg: str, host_full, spec, budget_s: float = 12.0, threads: int = 1):
-    """Time the oracle port (Algorithm 1 restated in C) on a bounded sample."""
-    import oracle
-    if spec["batch"] > 1:
-        unit_cells = spec["rows"] * spec["cols"]
-        t0 = time.perf_counter()
-        oracle.freq_batch(host_full[:4])
-        per = (time.perf_counter() - t0) / 4
-        n = max(1, min(len(host_full), int(budget_s / max(per, 1e-9))))
-        t0 = time.perf_counter()
-        oracle.freq_batch(host_full[:n])
-        dt = time.perf_counter() - t0
-        return n * unit_cells / dt / 1e9, f"first {n} of {spec['batch']} matrices", 1
+def _trimmed_mean(xs, trim=0.1):
+    """bench.py:98-147 of the reference: drop floor(n * trim) runs per tail."""
+    xs = sorted(xs)
+    k = int(len(xs) * trim)
+    xs = xs[k:len(xs) - k] if len(xs) > 2 * k else xs
+    return sum(xs) / len(xs)
+
+
+def _squarelab():
+    """The reference package (pip-installed into baseline/_ref), or None."""
+    for cand in (os.environ.get("SQUARELAB_REF"), os.path.join(ROOT, "baseline", "_ref")):
+        if cand and os.path.isdir(os.path.join(cand, "squarelab")):
+            if cand not in sys.path:
+                sys.path.insert(0, cand)
+            import squarelab.squares
+            import squarelab.grid
+            return squarelab
+    return None
+
+
+def _sample_rows(host_full, spec, cells_budget):
+    """First rows of the workload (all columns) up to ~cells_budget cells, as u8."""
     cols = spec["cols"]
-    fmt_bits = spec["fmt"] == "bits"
+    rows = int(max(1, min(spec["rows"], cells_budget // cols)))
+    sub = host_full[:rows]
+    if spec["fmt"] == "bits":
+        from paper_2503_18974_b200.grid import unpack_bits
+        sub = unpack_bits(sub, cols)
+    return np.ascontiguousarray(sub, dtype=np.uint8), rows
 
-    def run(rows):
-        sub = host_full[:rows]
-        t0 = time.perf_counter()
-        if fmt_bits:
-            oracle.freq_bits(sub, cols)
-        else:
-            oracle.freq(sub)
-        return time.perf_counter() - t0
 
-    probe = min(spec["rows"], 64)
-    per_row = run(probe) / probe
-    rows = int(max(probe, min(spec["rows"], budget_s / max(per_row, 1e-12))))
-    if threads <= 1:
-        dt = run(rows)
-        return rows * cols / dt / 1e9, f"first {rows} rows x {cols} cols (1 solve)", 1
-    # independent solves of distinct row slices, one per thread (ctypes drops the GIL)
-    rows_t = max(1, min(rows, len(host_full) // threads))
-    ts = []
+def cpu_baseline_reference(cfg: str, host_full, spec):
+    """The reference's own CPU path, single-threaded as its contract states
+    (SPEC.md:469), timed with its bench semantics (bench.py:98-147: warmup 1,
+    trimmed mean, one instance reused, generation excluded): squarelab's
+    freq_square and its default DP baseline dp_full (bench.py:61), on a bounded
+    sample of this workload.  Falls back to the oracle C port if the reference
+    package is not installed."""
+    cores = len(os.sched_getaffinity(0))
+    sl = _squarelab()
+    runs = 30 if cfg == "cfg1" else 3
+    if spec["batch"] > 1:
+        n = 16
+        mats = [np.ascontiguousarray(host_full[k]) for k in range(n)]
+        unit = f"first {n} of {spec['batch']} matrices ({spec['rows']}x{spec['cols']})"
+        cells = n * spec["rows"] * spec["cols"]
+        dp_mats, dp_unit, dp_cells = mats[:4], f"first 4 of {spec['batch']} matrices", 4 * spec["rows"] * spec["cols"]
+    else:
+        a, r = _sample_rows(host_full, spec, 8_000_000)
+        mats, unit, cells = [a], f"first {r} rows x {spec['cols']} cols", a.size
+        d, rd = _sample_rows(host_full, spec, 2_000_000)
+        dp_mats, dp_unit, dp_cells = [d], f"first {rd} rows x {spec['cols']} cols", d.size
+    if sl is None:
+        import oracle
+        ts = []
+        for _ in range(runs + 1):
+            t0 = time.perf_counter()
+            for m in mats:
+                oracle.freq(m)
+            ts.append(time.perf_counter() - t0)
+        v = cells / _trimmed_mean(ts[1:]) / 1e9
+        return {"value": v, "unit": UNIT, "cores": 1, "host_cores": cores, "kind": "port",
+                "sample": unit + " (reference package not installed: oracle C port, 1 thread)"}
+    BM = sl.grid.BinaryMatrix
+    objs = [BM(m.shape[0], m.shape[1], m.tobytes()) for m in mats]  # construction excluded
+    dobjs = [BM(m.shape[0], m.shape[1], m.tobytes()) for m in dp_mats]
 
-    def worker(k):
-        sub = host_full[k * rows_t:(k + 1) * rows_t]
-        if fmt_bits:
-            oracle.freq_bits(sub, cols)
-        else:
-            oracle.freq(sub)
+    def timed(fn, ob, n):
+        ts = []
+        for it in range(n + 1):  # warmup 1
+            t0 = time.perf_counter()
+            for o in ob:
+                fn(o)
+            ts.append(time.perf_counter() - t0)
+        return _trimmed_mean(ts[1:])
 
-    t0 = time.perf_counter()
-    for k in range(threads):
-        th = threading.Thread(target=worker, args=(k,))
-        th.start()
-        ts.append(th)
-    for th in ts:
-        th.join()
-    dt = time.perf_counter() - t0
-    return (threads * rows_t * cols / dt / 1e9,
-            f"{threads} concurrent solves of {rows_t} x {cols} row slices", threads)
+    fv = cells / timed(sl.squares.freq_square, objs, runs) / 1e9
+    dv = dp_cells / timed(sl.squares.dp_full, dobjs, 3 if runs > 3 else 1) / 1e9
+    return {"value": fv, "unit": UNIT, "cores": 1, "host_cores": cores, "kind": "reference",
+            "impl": "squarelab.freq_square (the reference's Python, 1 of %d host cores)" % cores,
+            "sample": unit + f"; warmup 1, trimmed mean of {runs} (reference bench.py:98-147)",
+            "dp_full": {"value": dv, "unit": UNIT, "sample": dp_unit,
+                        "impl": "squarelab.dp_full (the reference's default DP baseline, bench.py:61)"}}
+
+
+def host_workload(cfg: str, spec):
+    """The configured matrix on the host, generated on the CPU: the same bytes as
+    the GPU arm for cfg1-4 (MT19937 mirror, counter hash); cfg5 is the same recipe
+    (N(0,1) noise, periodic Gaussian blur sigma 64, 40th percentile) drawn from
+    numpy's generator, so a different instance of the same distribution."""
+    from paper_2503_18974_b200 import configs
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    if cfg == "cfg1":
+        return configs.cfg1_array(), "same bytes as the GPU arm"
+    if cfg == "cfg2":
+        return configs.cfg2_array(), "same bytes as the GPU arm"
+    if cfg in ("cfg3", "cfg4"):
+        n, thr = spec["rows"], configs.thr53(spec["p"])
+        words = (spec["cols"] + 31) // 32
+        out = (np.empty((n, spec["cols"]), np.uint8) if cfg == "cfg3" else np.empty((n, words), np.uint32))
+        step = -(-n // cores)
+
+        def gen(k):
+            r0, r1 = k * step, min(n, (k + 1) * step)
+            if r0 < r1:
+                fn = oracle.gen_hash_u8 if cfg == "cfg3" else oracle.gen_hash_bits
+                out[r0:r1] = fn(spec["seed"], thr, r0, r1 - r0, spec["cols"])
+
+        ths = [threading.Thread(target=gen, args=(k,)) for k in range(cores)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        if cfg == "cfg3":
+            k = spec["square"]
+            top, left = configs.cfg3_square_pos(spec["seed"], n, k)
+            out[top:top + k, left:left + k] = 1
+        return out, "same bytes as the GPU arm"
+    import scipy.fft as sfft
+    n, sigma, q = spec["rows"], spec["sigma"], spec["q"]
+    rng = np.random.default_rng(spec["seed"])
+    x = rng.standard_normal((n, n), dtype=np.float32)
+    X = sfft.rfft2(x, workers=-1)
+    del x
+    fy = np.fft.fftfreq(n).astype(np.float32)
+    fx = np.fft.rfftfreq(n).astype(np.float32)
+    c = np.float32(-2.0 * np.pi ** 2 * sigma * sigma)
+    X *= np.exp(c * fy * fy)[:, None]
+    X *= np.exp(c * fx * fx)[None, :]
+    y = sfft.irfft2(X, s=(n, n), workers=-1)
+    del X
+    k = int(q * n * n)
+    thr = np.partition(y.ravel(), k)[k]
+    return (y > thr).astype(np.uint8), "same recipe as the GPU arm, numpy noise (another instance)"
 
 
 # ------------------------------------------------------------------ reference arm
 def run_reference(args, rank, world):
+    """The reference algorithm's CPU implementation on the WHOLE configured
+    matrix, every step: the oracle's C restatement of Algorithm 1
+    (squares.py:84-103; the reference itself is pure Python) run per row band
+    on all host threads plus the band combine (carry fold, data-free fix-up),
+    so each step returns the exact whole-matrix answer.  Batches: the
+    matrices split over the threads."""
     if rank != 0:
         return 0
     from paper_2503_18974_b200 import configs
@@ -203,34 +297,50 @@ def run_reference(args, rank, world):
     oracle.lib()
     spec = configs.CONFIGS[args.config]
     cores = len(os.sched_getaffinity(0))
-    # host copy of the workload (generated with the oracle's own generator on CPU)
-    if args.config == "cfg4":
-        rows = min(spec["rows"], 4096 * cores)
-        host = oracle.gen_hash_bits(spec["seed"], configs.thr53(spec["p"]), 0, rows, spec["cols"])
-    elif args.config == "cfg3":
-        rows = min(spec["rows"], 2048 * cores)
-        host = oracle.gen_hash_u8(spec["seed"], configs.thr53(spec["p"]), 0, rows, spec["cols"])
-    elif args.config == "cfg1":
-        host = configs.cfg1_array()
-    elif args.config == "cfg2":
-        host = configs.cfg2_array(count=256)
-    else:  # cfg5: blob mask recipe on CPU at reduced size (same statistics per row)
-        host = configs.blob_mask_numpy(4096, spec["sigma"], spec["q"], spec["seed"])
-        spec = dict(spec, rows=4096, cols=4096)
-    vals = []
-    sample = ""
-    for it in range(args.warmup + args.steps):
-        v, sample, used = cpu_baseline_sample(args.config, host, spec, budget_s=args.ref_budget,
-                                              threads=cores)
-        if it >= args.warmup:
-            vals.append(v)
-    value = statistics.median(vals)
+    host, same = host_workload(args.config, spec)
+    fmt_bits = spec["fmt"] == "bits"
+    cells = spec["batch"] * spec["rows"] * spec["cols"]
+
+    def solve():
+        if spec["batch"] > 1:
+            res = [None] * cores
+            step = -(-len(host) // cores)
+
+            def part(k):
+                res[k] = oracle.freq_batch(host[k * step:(k + 1) * step]) if k * step < len(host) else []
+
+            ths = [threading.Thread(target=part, args=(k,)) for k in range(cores)]
+            for t in ths:
+                t.start()
+            for t in ths:
+                t.join()
+            return [r for p in res for r in p][0]
+        return oracle.solve_banded_mt(host, 1 if fmt_bits else 0, spec["cols"], cores)
+
+    for _ in range(args.warmup):
+        ans = solve()
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ans = solve()
+        ts.append(time.perf_counter() - t0)
+    total = sum(ts)
+    value = cells * args.steps / total / 1e9
+    sample = (f"whole matrix every step ({spec['rows']}x{spec['cols']}"
+              f"{' x %d' % spec['batch'] if spec['batch'] > 1 else ''}, {same})")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic", "config": {"workload": spec["workload"], "impl": "oracle C port"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "port",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u32" if fmt_bits else "u8", "data": "synthetic",
+        "config": {"workload": spec["workload"], "rows": spec["rows"], "cols": spec["cols"],
+                   "batch": spec["batch"], "format": spec["fmt"],
+                   "impl": ("oracle C port of Algorithm 1 (squares.py:84-103) per row band on "
+                            f"{cores} host threads + band combine (carry fold, fix-up)"
+                            if spec["batch"] == 1 else
+                            f"oracle C port of Algorithm 1, matrices split over {cores} host threads"),
+                   "answer": {"side": ans.side, "top": ans.top, "left": ans.left}},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -242,13 +352,11 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
-    ap.add_argument("--ref-budget", type=float, default=6.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
     args = ap.parse_args()
@@ -310,7 +418,7 @@ def main():
     p1_ev = []
 
     def step(instrument=False):
-        if flush is not None:
+        if flush is not None and instrument:
             flush.fill_(1)
         if use_solver:
             if instrument:
@@ -369,17 +477,26 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     launches_before = be.launches if not use_solver else 0
-    start = torch.cuda.Event(enable_timing=True)
-    end = torch.cuda.Event(enable_timing=True)
+    # inputs < L2 are flushed before every step, OUTSIDE the step's events:
+    # the step time is the sum of the K per-step event intervals
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps if flush is not None else 1)]
     with ClockSampler(local) as clk:
-        start.record(stream)
-        for _ in range(args.steps):
-            step()
-        end.record(stream)
+        if flush is None:
+            evs[0][0].record(stream)
+            for _ in range(args.steps):
+                step()
+            evs[0][1].record(stream)
+        else:
+            for e0, e1 in evs:
+                flush.fill_(1)
+                e0.record(stream)
+                step()
+                e1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms_total = start.elapsed_time(end)
+    ms_total = sum(e0.elapsed_time(e1) for e0, e1 in evs)
     t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -417,42 +534,33 @@ def main():
         except Exception:
             pass
 
-    # ---- e2e: host buffers through the C ABI, H2D inside the timed region
+    # ---- e2e: the public API on a pageable numpy array (what a caller of
+    # freq_square / freq_square_bits / solve_batch passes); the library's H2D
+    # copy and the result read-back are inside the timed region
     e2e = None
-    if world == 1 and batch == 1:
-        host = src.cpu().pin_memory()
-        out = N.MsqResult()
-        hptr = ctypes.c_void_p(host.data_ptr())
-        sh = ctypes.c_void_p(stream.cuda_stream)
-        ld = src.shape[1]
-        fn = lib.msq_solve_bits_host if fmt == N.FMT_BITS else lib.msq_solve_u8_host
-        N.check(fn(hptr, rows, cols, ld, ctypes.byref(out), sh))  # warm
+    if world == 1:
+        from paper_2503_18974_b200.squares import freq_square, freq_square_bits, solve_batch
+        host = src.cpu().numpy()
+        if fmt == N.FMT_BITS:
+            host = host.view(np.uint32)
+        host = np.array(host, copy=True)  # plain pageable memory
+        if batch > 1:
+            call, path = (lambda: solve_batch(host)), "solve_batch(numpy) -> msq_solve_batch_u8_host"
+        elif fmt == N.FMT_BITS:
+            call, path = (lambda: [freq_square_bits(host, cols)]), "freq_square_bits(numpy) -> msq_solve_bits_host"
+        else:
+            call, path = (lambda: [freq_square(host)]), "freq_square(numpy) -> msq_solve_u8_host"
+        got = call()  # warm
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            N.check(fn(hptr, rows, cols, ld, ctypes.byref(out), sh))
-        torch.cuda.synchronize()
-        dt = (time.perf_counter() - t0) / args.e2e_steps
-        e2e = {"value": cells_total / dt / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": int(in_bytes), "d2h_bytes_per_step": 32,
-               "ms_per_step": dt * 1e3, "path": fn.__name__}
-        assert (out.side, out.top, out.left) == (answer[0].side, answer[0].top, answer[0].left)
-    elif world == 1:
-        host = src.cpu().pin_memory()
-        dev = host.to("cuda", non_blocking=True)  # warm: device buffer, pinned path
-        solver.launch(dev)
-        solver.res.cpu()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            dev = host.to("cuda", non_blocking=True)
-            solver.launch(dev)
-            solver.res.cpu()
+            got = call()
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / args.e2e_steps
         e2e = {"value": cells_total / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(in_bytes),
-               "d2h_bytes_per_step": int(32 * src.shape[0]), "ms_per_step": dt * 1e3,
-               "path": "Solver.launch (msq_launch)"}
+               "d2h_bytes_per_step": int(32 * batch), "ms_per_step": dt * 1e3, "path": path,
+               "host_memory": "pageable"}
+        assert [(g.side, g.top, g.left) for g in got] == [(a.side, a.top, a.left) for a in answer]
 
     # ---- parity of this run's answer against the oracle (rank 0, cheap configs / sample)
     parity = None
@@ -475,9 +583,7 @@ def main():
             parity = all((g.side, g.top, g.left) == (w.side, w.top, w.left)
                          for g, w in zip(got, want))
         if not args.no_cpu_baseline:
-            v, sample, used = cpu_baseline_sample(args.config, host_np, spec,
-                                                  budget_s=args.cpu_budget)
-            cpu = {"value": v, "unit": UNIT, "cores": used, "kind": "port", "sample": sample}
+            cpu = cpu_baseline_reference(args.config, host_np, spec)
 
     if rank == 0:
         a0 = answer[0]

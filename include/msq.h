@@ -186,6 +186,10 @@ int msq_solve_u8_host(const uint8_t* h_cells, int64_t rows, int64_t cols, int64_
                       msq_result* out, void* stream);
 int msq_solve_bits_host(const uint32_t* h_words, int64_t rows, int64_t cols, int64_t ld_words,
                         msq_result* out, void* stream);
+int msq_solve_batch_u8_host(const uint8_t* h_cells, int64_t batch, int64_t rows, int64_t cols,
+                            msq_result* out, void* stream);
+/* (Pageable host buffers are staged through pinned chunks by worker threads,
+ * host copies overlapping the PCIe transfers; pinned ones are copied directly.) */
 
 /* ---- row-band sharding across GPUs (one process per GPU) ----------------
  * A rank owns rows [row_base, row_base + plan->rows) of the global matrix.

@@ -7,6 +7,7 @@
  */
 #include "msq_oracle.h"
 
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -334,6 +335,99 @@ int orc_solve_banded(const void* src, int fmt, int64_t ld, int64_t rows, int64_t
     result_from_key(best, rows, cols, out);
 done:
     free(hts); free(r0s); free(e); free(b); free(ao); free(c); free(keys);
+    return rc;
+}
+
+/*
+ * All-core variant for the benchmark's CPU arm: the same band algebra as
+ * orc_solve_banded (Algorithm 1 per row band, P5 carry fold, P6 fix-up), the
+ * band passes and the fix-ups spread over `nthreads` POSIX threads, the carry
+ * fold sequential (O(nbands * cols)).  Whole-matrix exact.
+ */
+typedef struct {
+    const void* src; int fmt; int64_t ld, cols, words, nbands, nthreads, tid;
+    const int64_t* r0s; const int64_t* hts;
+    uint16_t* e; uint16_t* b; uint32_t* ao; uint32_t* carry; uint64_t* keys; uint64_t* fkeys;
+    int64_t g; int phase; int rc;
+} mt_job;
+
+static void* mt_worker(void* arg) {
+    mt_job* j = (mt_job*)arg;
+    for (int64_t k = j->tid; k < j->nbands; k += j->nthreads) {
+        if (j->phase == 0) {
+            int rc = orc_band_pass(j->src, j->fmt, j->ld, j->r0s[k], j->r0s[k] + j->hts[k], j->cols, 1,
+                                   j->e + k * j->cols, j->b + k * j->cols, j->ao + k * j->words, &j->keys[k]);
+            if (rc) j->rc = rc;
+        } else if (k > 0) {
+            int rc = orc_fixup(j->carry + k * j->cols, j->e + k * j->cols, j->cols, j->hts[k], j->r0s[k],
+                               j->g > 0 ? j->g : 1, &j->fkeys[k]);
+            if (rc) j->rc = rc;
+        }
+    }
+    return NULL;
+}
+
+int orc_solve_banded_mt(const void* src, int fmt, int64_t ld, int64_t rows, int64_t cols,
+                        int64_t nbands, int64_t nthreads, orc_result* out) {
+    if (rows == 0 || cols == 0) return solve_freq(src, fmt, ld, rows, cols, out);
+    if (nbands < 1 || nthreads < 1) return 1;
+    if (nbands > rows) nbands = rows;
+    if (nthreads > nbands) nthreads = nbands;
+    const int64_t words = (cols + 31) / 32;
+    int64_t* hts = (int64_t*)malloc((size_t)nbands * sizeof(int64_t));
+    int64_t* r0s = (int64_t*)malloc((size_t)nbands * sizeof(int64_t));
+    uint16_t* e = (uint16_t*)malloc((size_t)(nbands * cols) * sizeof(uint16_t));
+    uint16_t* b = (uint16_t*)malloc((size_t)(nbands * cols) * sizeof(uint16_t));
+    uint32_t* ao = (uint32_t*)malloc((size_t)(nbands * words) * sizeof(uint32_t));
+    uint32_t* carry = (uint32_t*)calloc((size_t)(nbands * cols), sizeof(uint32_t));
+    uint64_t* keys = (uint64_t*)calloc((size_t)nbands, sizeof(uint64_t));
+    uint64_t* fkeys = (uint64_t*)calloc((size_t)nbands, sizeof(uint64_t));
+    mt_job* jobs = (mt_job*)calloc((size_t)nthreads, sizeof(mt_job));
+    pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+    int rc = 0;
+    if (!hts || !r0s || !e || !b || !ao || !carry || !keys || !fkeys || !jobs || !th) { rc = 2; goto done; }
+    for (int64_t k = 0; k < nbands; ++k) {
+        r0s[k] = rows * k / nbands;
+        hts[k] = rows * (k + 1) / nbands - r0s[k];
+    }
+    for (int phase = 0; phase < 2; ++phase) {
+        uint64_t best = 0;
+        if (phase == 1) {
+            for (int64_t k = 0; k < nbands; ++k) if (keys[k] > best) best = keys[k];
+            /* P5 fold: carry_k = f_{k-1} ? carry_{k-1} + H_{k-1} : b_{k-1} */
+            for (int64_t k = 1; k < nbands; ++k)
+                for (int64_t jj = 0; jj < cols; ++jj) {
+                    const int full = (ao[(k - 1) * words + (jj >> 5)] >> (jj & 31)) & 1u;
+                    const uint64_t h = full ? (uint64_t)carry[(k - 1) * cols + jj] + (uint64_t)hts[k - 1]
+                                            : (uint64_t)b[(k - 1) * cols + jj];
+                    carry[k * cols + jj] = h > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)h;
+                }
+        }
+        for (int64_t t = 0; t < nthreads; ++t) {
+            mt_job* j = &jobs[t];
+            j->src = src; j->fmt = fmt; j->ld = ld; j->cols = cols; j->words = words;
+            j->nbands = nbands; j->nthreads = nthreads; j->tid = t; j->r0s = r0s; j->hts = hts;
+            j->e = e; j->b = b; j->ao = ao; j->carry = carry; j->keys = keys; j->fkeys = fkeys;
+            j->g = (int64_t)(best >> (2 * KEY_DIM_BITS)); j->phase = phase;
+            if (pthread_create(&th[t], NULL, mt_worker, j)) { rc = 3; goto done; }
+        }
+        for (int64_t t = 0; t < nthreads; ++t) {
+            pthread_join(th[t], NULL);
+            if (jobs[t].rc) rc = jobs[t].rc;
+        }
+        if (rc) goto done;
+    }
+    {
+        uint64_t best = 0;
+        for (int64_t k = 0; k < nbands; ++k) {
+            if (keys[k] > best) best = keys[k];
+            if (fkeys[k] > best) best = fkeys[k];
+        }
+        result_from_key(best, rows, cols, out);
+    }
+done:
+    free(hts); free(r0s); free(e); free(b); free(ao); free(carry); free(keys); free(fkeys);
+    free(jobs); free(th);
     return rc;
 }
 

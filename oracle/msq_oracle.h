@@ -71,6 +71,8 @@ int orc_fixup(const uint32_t* c, const uint16_t* e, int64_t cols, int64_t H, int
               int64_t t0, uint64_t* key);
 
 /* Whole-matrix solve through the band decomposition (nbands >= 1). */
+int orc_solve_banded_mt(const void* src, int fmt, int64_t ld, int64_t rows, int64_t cols,
+                        int64_t nbands, int64_t nthreads, orc_result* out);
 int orc_solve_banded(const void* src, int fmt, int64_t ld, int64_t rows, int64_t cols,
                      int64_t nbands, orc_result* out);
 

@@ -87,6 +87,7 @@ def load():
                                   ctypes.POINTER(I64), P], ctypes.c_int),
         "msq_solve_u8_host": ([P, I64, I64, I64, RP, P], ctypes.c_int),
         "msq_solve_bits_host": ([P, I64, I64, I64, RP, P], ctypes.c_int),
+        "msq_solve_batch_u8_host": ([P, I64, I64, I64, RP, P], ctypes.c_int),
         "msq_rank_pass1": ([PP, P, P, P, P], ctypes.c_int),
         "msq_rank_seed": ([PP, P, P, P], ctypes.c_int),
         "msq_rank_band_pass": ([PP, P, P, P, P], ctypes.c_int),

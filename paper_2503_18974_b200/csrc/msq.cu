@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "msq.h"
@@ -383,6 +384,14 @@ struct DevCache {
     unsigned* flag = nullptr;  // 16 bytes of device flags (cube probe)
     void* dpws = nullptr;      // row-DP / brute-force workspace
     size_t dpws_bytes = 0;
+    // pageable host -> device staging (host-buffer calls): per worker thread two
+    // pinned chunks, their events and a copy stream
+    static constexpr int kStageWorkers = 8;
+    void* stage[kStageWorkers][2] = {};
+    cudaEvent_t stage_ev[kStageWorkers][2] = {};
+    cudaEvent_t stage_done[kStageWorkers] = {};
+    cudaStream_t stage_st[kStageWorkers] = {};
+    int stage_ready = 0;
 };
 DevCache g_cache[64];
 
@@ -959,6 +968,73 @@ int msq_solve_batch_u8(const uint8_t* d_cells, int64_t batch, int64_t rows, int6
     return solve_sync(MSQ_FMT_U8, batch, d_cells, rows, cols, cols, out, stream);
 }
 
+namespace {
+constexpr size_t kStageChunk = 8u << 20;
+
+// Host -> device copy of a caller's buffer, ordered before later work on `st`.
+// Pinned buffers go straight to cudaMemcpyAsync.  Pageable ones are staged by
+// worker threads: each memcpy's its chunks (c = w, w + T, ...) into one of its
+// two pinned buffers while the other one's DMA runs on its own stream, so the
+// host copies and PCIe transfers of all workers overlap; `st` then waits on
+// every worker stream.  Caller holds C.mu.
+int h2d_copy(DevCache& C, int dev, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    cudaPointerAttributes at;
+    const bool pinned = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    if (pinned || bytes < 2 * kStageChunk)
+        return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st) == cudaSuccess ? MSQ_OK : MSQ_ECUDA;
+    const int T = std::max(1, std::min<int>(DevCache::kStageWorkers,
+                                            (int)std::thread::hardware_concurrency() / 2));
+    if (!C.stage_ready) {
+        for (int w = 0; w < DevCache::kStageWorkers; ++w) {
+            for (int b = 0; b < 2; ++b) {
+                if (cudaMallocHost(&C.stage[w][b], kStageChunk) != cudaSuccess) return MSQ_ENOMEM;
+                if (cudaEventCreateWithFlags(&C.stage_ev[w][b], cudaEventDisableTiming) != cudaSuccess)
+                    return MSQ_ECUDA;
+            }
+            if (cudaEventCreateWithFlags(&C.stage_done[w], cudaEventDisableTiming) != cudaSuccess ||
+                cudaStreamCreateWithFlags(&C.stage_st[w], cudaStreamNonBlocking) != cudaSuccess)
+                return MSQ_ECUDA;
+        }
+        C.stage_ready = 1;
+    }
+    // the destination may still be read by earlier work on `st`
+    cudaEvent_t ready;
+    if (cudaEventCreateWithFlags(&ready, cudaEventDisableTiming) != cudaSuccess) return MSQ_ECUDA;
+    cudaEventRecord(ready, st);
+    const size_t nchunks = (bytes + kStageChunk - 1) / kStageChunk;
+    std::vector<int> rcs(T, MSQ_OK);
+    std::vector<std::thread> pool;
+    for (int w = 0; w < T; ++w) {
+        pool.emplace_back([&, w]() {
+            cudaSetDevice(dev);
+            cudaStreamWaitEvent(C.stage_st[w], ready, 0);
+            int it = 0;
+            for (size_t c = (size_t)w; c < nchunks; c += (size_t)T, ++it) {
+                const int b = it & 1;
+                const size_t off = c * kStageChunk, n = std::min(kStageChunk, bytes - off);
+                if (cudaEventSynchronize(C.stage_ev[w][b]) != cudaSuccess) { rcs[w] = MSQ_ECUDA; return; }
+                std::memcpy(C.stage[w][b], (const char*)src + off, n);
+                if (cudaMemcpyAsync((char*)dst + off, C.stage[w][b], n, cudaMemcpyHostToDevice, C.stage_st[w]) !=
+                        cudaSuccess ||
+                    cudaEventRecord(C.stage_ev[w][b], C.stage_st[w]) != cudaSuccess) {
+                    rcs[w] = MSQ_ECUDA;
+                    return;
+                }
+            }
+            if (cudaEventRecord(C.stage_done[w], C.stage_st[w]) != cudaSuccess) rcs[w] = MSQ_ECUDA;
+        });
+    }
+    for (auto& t : pool) t.join();
+    cudaEventDestroy(ready);
+    for (int w = 0; w < T; ++w) {
+        if (rcs[w]) return rcs[w];
+        if (cudaStreamWaitEvent(st, C.stage_done[w], 0) != cudaSuccess) return MSQ_ECUDA;
+    }
+    return MSQ_OK;
+}
+}  // namespace
+
 static int solve_host(int32_t fmt, const void* h, int64_t rows, int64_t cols, int64_t ld, msq_result* out,
                       void* stream) {
     if (!out) return MSQ_EINVAL;
@@ -971,9 +1047,24 @@ static int solve_host(int32_t fmt, const void* h, int64_t rows, int64_t cols, in
     DevCache& C = g_cache[dev];
     std::lock_guard<std::mutex> lk(C.mu);  // held through the solve: the staging buffer is shared
     if ((rc = grow(&C.in, &C.in_bytes, bytes))) return rc;
-    if (cudaMemcpyAsync(C.in, h, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream) != cudaSuccess)
-        return MSQ_ECUDA;
+    if ((rc = h2d_copy(C, dev, C.in, h, bytes, (cudaStream_t)stream))) return rc;
     return solve_locked(C, fmt, 1, C.in, rows, cols, ld, out, stream);
+}
+
+int msq_solve_batch_u8_host(const uint8_t* h_cells, int64_t batch, int64_t rows, int64_t cols,
+                            msq_result* out, void* stream) {
+    if (!out || batch < 1) return MSQ_EINVAL;
+    int rc;
+    if (empty_shape(batch, rows, cols, out, &rc)) return rc;
+    if (!h_cells) return MSQ_EINVAL;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return MSQ_ECUDA;
+    const size_t bytes = (size_t)batch * (size_t)rows * (size_t)cols;
+    DevCache& C = g_cache[dev];
+    std::lock_guard<std::mutex> lk(C.mu);
+    if ((rc = grow(&C.in, &C.in_bytes, bytes))) return rc;
+    if ((rc = h2d_copy(C, dev, C.in, h_cells, bytes, (cudaStream_t)stream))) return rc;
+    return solve_locked(C, MSQ_FMT_U8, batch, C.in, rows, cols, cols, out, stream);
 }
 
 int msq_solve_u8_host(const uint8_t* h_cells, int64_t rows, int64_t cols, int64_t ld, msq_result* out,

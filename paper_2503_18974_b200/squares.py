@@ -352,10 +352,22 @@ def freq_square_bits(words, cols: int) -> SquareResult:
 
 
 def solve_batch(cells) -> list[SquareResult]:
-    """One launch over a stack of equal-shape matrices (uint8 [batch, rows, cols])."""
+    """One launch over a stack of equal-shape matrices (uint8 [batch, rows, cols]);
+    host arrays go through msq_solve_batch_u8_host (staged H2D inside the call)."""
     torch = _torch()
-    t = cells if isinstance(cells, torch.Tensor) else torch.from_numpy(
-        np.ascontiguousarray(np.asarray(cells, dtype=np.uint8)))
+    if not isinstance(cells, torch.Tensor):
+        a = np.ascontiguousarray(np.asarray(cells, dtype=np.uint8))
+        if a.ndim != 3:
+            raise ValueError("expected [batch, rows, cols]")
+        B, R, C = (int(x) for x in a.shape)
+        if R == 0 or C == 0:
+            return [SquareResult(0, 0, 0) for _ in range(B)]
+        out = (N.MsqResult * B)()
+        N.check(N.load().msq_solve_batch_u8_host(a.ctypes.data_as(ctypes.c_void_p), B, R, C,
+                                                 ctypes.cast(out, ctypes.POINTER(N.MsqResult)),
+                                                 _stream_handle()))
+        return [_to_result(out[k]) for k in range(B)]
+    t = cells
     if t.dim() != 3:
         raise ValueError("expected [batch, rows, cols]")
     B, R, C = (int(x) for x in t.shape)
