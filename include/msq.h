@@ -94,6 +94,8 @@ typedef struct {
 #define MSQ_PLAN_NO_STRIP 1     /* bit-packed bands: skip the strip pass        */
 #define MSQ_PLAN_NO_SEED 2      /* skip the lower-bound seed                     */
 #define MSQ_PLAN_SINGLE_TEAM 4  /* team engine: one team per matrix (rows <= 2040) */
+#define MSQ_PLAN_CLIMB_FIXUP 8  /* band-boundary fix-up by the per-depth climb (fixup_kernel)
+                                   instead of the window search (fixup2_kernel) */
 
 /* Build a plan.  nbands <= 0 picks a default (one band per SM, bands of
  * >= 64 rows, <= 65535 rows each).  Returns MSQ_EINVAL for unsupported

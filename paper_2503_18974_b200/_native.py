@@ -16,7 +16,7 @@ HEADER = os.path.join(os.path.dirname(_PKG), "include", "msq.h")
 
 MSQ_OK, MSQ_EINVAL, MSQ_EVALUE, MSQ_ECUDA, MSQ_ENOMEM = 0, 1, 2, 3, 4
 FMT_U8, FMT_BITS = 0, 1
-PLAN_NO_STRIP, PLAN_NO_SEED, PLAN_SINGLE_TEAM = 1, 2, 4
+PLAN_NO_STRIP, PLAN_NO_SEED, PLAN_SINGLE_TEAM, PLAN_CLIMB_FIXUP = 1, 2, 4, 8
 
 
 class MsqResult(ctypes.Structure):

@@ -17,6 +17,8 @@
 #include "msq_engine.cuh"
 #include "msq_team.cuh"
 #include "msq_strip.cuh"
+#include "msq_ustrip.cuh"
+#include "msq_fixup2.cuh"
 #include "msq_dp.cuh"
 #include "msq_ingest.cuh"
 #include "msq_cube.cuh"
@@ -72,6 +74,33 @@ bool strip_applies(const msq_plan* p) {
            p->words >= 2 * msq::STRIP_WORDS && p->words % 4 == 0 && p->row_stage_bytes % 16 == 0 &&
            ld_bytes % 16 == 0 && (strip_warps(p) + 1) * 32 <= 640 && strip_slots(p) >= 2 &&
            ceil_div(p->rows, p->nbands) <= 65535;
+}
+
+// ---- u8 strip pass (msq_ustrip.cuh): u8 single matrices, several bands
+int ustrip_warps(const msq_plan* p) { return (int)ceil_div(p->words, msq::USTRIP_STRIDE); }
+int ustrip_fixed_smem() { return 2 * msq::USTRIP_MAXSLOTS * 8 + 64; }
+// rows per ring slot: the largest of 8/4/2/1 that leaves >= 3 slots
+int ustrip_rows_per_slot(const msq_plan* p) {
+    const long long avail = kSmemMax - 256 - ustrip_fixed_smem();
+    for (int R = 8; R >= 1; R /= 2)
+        if (avail / ((long long)R * p->row_stage_bytes) >= 3) return R;
+    return 0;
+}
+int ustrip_slots(const msq_plan* p) {
+    const int R = ustrip_rows_per_slot(p);
+    if (!R) return 0;
+    const long long avail = kSmemMax - 256 - ustrip_fixed_smem();
+    return (int)std::min<long long>(msq::USTRIP_MAXSLOTS, avail / ((long long)R * p->row_stage_bytes));
+}
+int ustrip_smem(const msq_plan* p) {
+    return ustrip_slots(p) * ustrip_rows_per_slot(p) * p->row_stage_bytes + ustrip_fixed_smem();
+}
+bool ustrip_applies(const msq_plan* p) {
+    if (p->flags & MSQ_PLAN_NO_STRIP) return false;  // experiments
+    const int R = ustrip_rows_per_slot(p);
+    return p->fmt == MSQ_FMT_U8 && p->batch == 1 && p->nbands > 1 && R > 0 && p->cols % 32 == 0 &&
+           p->ld % 16 == 0 && p->row_stage_bytes == p->cols && ustrip_warps(p) <= msq::USTRIP_MAXWARPS &&
+           p->words >= msq::USTRIP_WORDS && ceil_div(p->rows, p->nbands) <= msq::ustrip_maxh(R);
 }
 
 WsLayout ws_layout(const msq_plan* p) {
@@ -191,9 +220,53 @@ cudaError_t launch_pass1(const msq_plan* pl, const msq::Pass1Params& prm, cudaSt
 }
 
 // band passes: the strip pass (when it applies) and pass1_kernel for the bands it left
+template <int R>
+cudaError_t launch_ustrip_t(const msq_plan* pl, const msq::UStripParams& up, cudaStream_t st) {
+    static bool attr_set[64] = {false};
+    cudaError_t e = set_smem_attr(msq::ustrip_kernel<R>, attr_set);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};  // programmatic dependent of the seed
+    cfg.gridDim = dim3((unsigned)pl->nbands);
+    cfg.blockDim = dim3((unsigned)((up.nwarps + 1) * 32));
+    cfg.dynamicSmemBytes = (size_t)ustrip_smem(pl);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, msq::ustrip_kernel<R>, up);
+}
+
 cudaError_t launch_band_pass(const msq_plan* pl, msq::Pass1Params prm, void* ws, const void* src, cudaStream_t st,
                              int* nlaunch) {
     *nlaunch = 1;
+    if (prm.write_summaries && ustrip_applies(pl) && ((uintptr_t)src % 16) == 0) {
+        msq::UStripParams up{};
+        up.src = (const uint8_t*)src;
+        up.ld = pl->ld;
+        up.rows = (int)pl->rows;
+        up.cols = (int)pl->cols;
+        up.W = pl->words;
+        up.nbands = pl->nbands;
+        up.cols_pad = pl->words * 32;
+        up.row_base = pl->row_base;
+        up.nslots = ustrip_slots(pl);
+        up.row_bytes = pl->row_stage_bytes;
+        up.nwarps = ustrip_warps(pl);
+        up.share = pl->deterministic ? 0 : 1;
+        up.zb = prm.zb;
+        up.e_out = prm.e_out;
+        up.ao_out = prm.ao_out;
+        up.band_keys = prm.band_keys;
+        up.results = prm.results;
+        switch (ustrip_rows_per_slot(pl)) {
+            case 8: return launch_ustrip_t<8>(pl, up, st);
+            case 4: return launch_ustrip_t<4>(pl, up, st);
+            case 2: return launch_ustrip_t<2>(pl, up, st);
+            default: return launch_ustrip_t<1>(pl, up, st);
+        }
+    }
     if (prm.write_summaries && strip_applies(pl) && ((uintptr_t)src % 16) == 0) {
         WsLayout L = ws_layout(pl);
         uint8_t* w = (uint8_t*)ws;
@@ -246,6 +319,23 @@ cudaError_t apply_test_floor(const msq_plan* pl, msq_devresult* d_result, cudaSt
 
 cudaError_t launch_fixup(const msq_plan* pl, const msq::FixParams& prm, int nblocks, cudaStream_t st) {
     if (nblocks <= 0) return cudaSuccess;
+    if (!(pl->flags & MSQ_PLAN_CLIMB_FIXUP)) {  // window-search fix-up (msq_fixup2.cuh)
+        static bool attr_set[64] = {false};
+        cudaError_t e = set_smem_attr(msq::fixup2_kernel, attr_set);
+        if (e != cudaSuccess) return e;
+        cudaLaunchConfig_t cfg{};  // programmatic dependent of the carry scan
+        cfg.gridDim = dim3((unsigned)nblocks);
+        cfg.blockDim = dim3((unsigned)msq::FIX2_THREADS);
+        cfg.dynamicSmemBytes = (size_t)msq::fix2_layout(pl->words).total;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, msq::fixup2_kernel, prm);
+        return cudaGetLastError();
+    }
     switch (pl->fix_wpt) {
         case 1: return launch_fixup_t<1>(pl, prm, nblocks, st);
         case 2: return launch_fixup_t<2>(pl, prm, nblocks, st);

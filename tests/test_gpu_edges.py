@@ -132,3 +132,32 @@ def test_bits_answers_outside_strip_window(torch, case):
     else:
         assert want.side > 222
     _same(freq_square_bits(w, n), want)
+
+
+@pytest.mark.parametrize("fmt", ["u8", "bits"])
+def test_fixup_window_search_vs_climb(torch, fmt):
+    """The window-search fix-up (msq_fixup2.cuh) and the per-depth climb
+    (MSQ_PLAN_CLIMB_FIXUP) on tall squares crossing many band tops, ties, and
+    dense backgrounds: both equal the oracle."""
+    from paper_2503_18974_b200 import _native as Nn
+    from paper_2503_18974_b200.squares import Solver
+    rng = np.random.default_rng(300 if fmt == "u8" else 301)
+    for it in range(40):
+        rows = int(rng.integers(200, 3000))
+        cols = int(rng.choice([256, 512, 2048, 4096, 8192]))
+        p = float(rng.choice([0.8, 0.97, 0.995, 0.999, 1.0]))
+        a = (rng.random((rows, cols)) < p).astype(np.uint8)
+        for _ in range(int(rng.integers(1, 4))):
+            k = int(rng.integers(20, min(rows, cols, 900)))
+            t0, l0 = int(rng.integers(0, rows - k + 1)), int(rng.integers(0, cols - k + 1))
+            a[t0:t0 + k, l0:l0 + k] = 1
+        want = oracle.freq(a)
+        nb = int(rng.integers(2, min(rows // 2, 148) + 1))
+        if fmt == "u8":
+            src, f = torch.from_numpy(a).cuda(), Nn.FMT_U8
+        else:
+            src, f = torch.from_numpy(grid.pack_bits(a).view(np.int32)).cuda(), Nn.FMT_BITS
+        for flags in (0, Nn.PLAN_CLIMB_FIXUP):
+            for det in (False, True):
+                got = Solver(f, rows, cols, nbands=nb, flags=flags, deterministic=det).solve(src)[0]
+                _same(got, want)
