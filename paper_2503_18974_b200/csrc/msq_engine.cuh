@@ -2114,6 +2114,8 @@ __device__ __forceinline__ uint32_t seed_word(const uint8_t* rp, int w, int W, i
 template <bool U8>
 __global__ void __launch_bounds__(256) seed_climb_kernel(const uint8_t* src, long long ld_bytes, int rows, int cols,
                                                          int W, int nstrips, int chunks, unsigned char* result) {
+    // the band pass may launch now (its CTAs wait in griddepcontrol.wait)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (gw >= nstrips * chunks) return;
@@ -2156,6 +2158,9 @@ __global__ void __launch_bounds__(256) seed_climb_kernel(const uint8_t* src, lon
 #pragma unroll
     for (int q = 0; q < SB; ++q) nxt[q] = fetch(q);
     for (int i0 = 0; i0 < nr; i0 += SB) {
+        // a strip whose squares grow slower than one side per 4 rows holds no
+        // large square; stop early (the bound only has to be a real square)
+        if (i0 >= 64 && 4 * best < i0) break;
         uint32_t rw[SB];
 #pragma unroll
         for (int q = 0; q < SB; ++q) {

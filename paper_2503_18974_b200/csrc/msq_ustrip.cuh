@@ -28,10 +28,12 @@
 //     plane (rows are counted from R, so inside a slot the low log2(R) plane bits
 //     are compile-time constants; a never-zeroed column reads as a zero in row -1);
 //   * the first-zero row as 8 more planes while the warp has never-zeroed columns;
-//   * from the row where the band-local height can reach t on: eligibility
-//     E = {z <= q - t} (8 LOP3), the run entering each word (one shuffle for
-//     t <= 33, a segmented warp scan above), and the leftmost window end in the
-//     warp's own words -> raise.
+//   * from the row where the band-local height can reach t on: for t >= 63 a
+//     filter first (a t-run holds ceil((t-62)/32) consecutive whole words with no
+//     zero in their last t rows: the word's last zero row, two ballots, shifted
+//     ANDs); then eligibility E = {z <= q - t} (8 LOP3), the run entering each
+//     word (one shuffle for t <= 33, a segmented warp scan above), and the
+//     leftmost window end in the warp's own words -> raise.
 #pragma once
 
 namespace msq {
@@ -158,6 +160,7 @@ __global__ void __launch_bounds__(640, 1) ustrip_kernel(const UStripParams p) {
         F0[q] = F1[q] = 0u;
     }
     uint32_t NZ0 = VAL0, NZ1 = VAL1;  // never-zeroed columns
+    int ZW0 = R - 1, ZW1 = R - 1;      // last row (stored form) with a zero in the word
     bool any_nz = true;
     uint32_t bad = 0u;
 
@@ -170,7 +173,7 @@ __global__ void __launch_bounds__(640, 1) ustrip_kernel(const UStripParams p) {
         const int row0 = q * R;
         const int nrows = min(R, H - row0);
         const uint32_t slot_s = ring_s + (uint32_t)(s * slot_bytes);
-        const int gglob = (p.share && (q & 7) == 7) ? ld_volatile(res_best(result)) : 0;
+        const int gglob = (p.share && (q & 3) == 3) ? ld_volatile(res_best(result)) : 0;
         // high plane masks of this slot's stored rows (row0 + R is a multiple of R)
         const uint32_t qbase = (uint32_t)(row0 + R);
         uint32_t hm[USTRIP_P];
@@ -195,6 +198,9 @@ __global__ void __launch_bounds__(640, 1) ustrip_kernel(const UStripParams p) {
             const uint32_t w0 = __byte_perm(us_half(v0a), us_half(v0b), sel);
             const uint32_t w1 = __byte_perm(us_half(v1a), us_half(v1b), sel);
             const uint32_t zm0 = ~w0 & VAL0, zm1 = ~w1 & VAL1;
+            const int qrow = row0 + R + b;
+            ZW0 = zm0 ? qrow : ZW0;
+            ZW1 = zm1 ? qrow : ZW1;
             // last zero := this row (q = qbase + b: low LR bits are b)
 #pragma unroll
             for (int pl = 0; pl < USTRIP_P; ++pl) {
@@ -215,7 +221,21 @@ __global__ void __launch_bounds__(640, 1) ustrip_kernel(const UStripParams p) {
                 any_nz = __any_sync(0xFFFFFFFFu, (NZ0 | NZ1) != 0u);
             }
             const int row = row0 + b;  // band-local row (0-based)
-            if (row + 1 >= t) {        // warp-uniform: band-local heights can reach t
+            bool test = row + 1 >= t;  // warp-uniform: band-local heights can reach t
+            if (test && t >= 63) {
+                // mode L: a t-run of eligible columns holds Lmin = ceil((t - 62) / 32) >= 1
+                // consecutive whole "F" words (no zero in their last t rows); the exact
+                // test runs only on rows whose window map has such a run
+                const int cq = row + R - t;
+                const unsigned f0 = __ballot_sync(0xFFFFFFFFu, VAL0 == 0xFFFFFFFFu && ZW0 <= cq);
+                const unsigned f1 = __ballot_sync(0xFFFFFFFFu, VAL1 == 0xFFFFFFFFu && ZW1 <= cq);
+                const unsigned long long M = (unsigned long long)f0 | ((unsigned long long)f1 << 32);
+                unsigned long long X = M;
+                const int lmin = (t - 62 + 31) / 32;
+                for (int i = 1; i < lmin && X; ++i) X &= M >> i;
+                test = X != 0ull;
+            }
+            if (test) {
                 const uint32_t c = (uint32_t)(row + R - t);  // eligible: z <= q - t
                 const uint32_t E0 = us_le(Z0, c) & VAL0, E1 = us_le(Z1, c) & VAL1;
                 const uint32_t full0 = E0 == 0xFFFFFFFFu, full1 = E1 == 0xFFFFFFFFu;
