@@ -122,6 +122,9 @@ def build_input(cfg: str, torch, rank: int, world: int):
     if cfg == "cfg4":
         full = configs.cfg4_device()
         fmt = N.FMT_BITS
+    elif cfg in ("cfg4_p99", "cfg4_planted"):
+        full = configs.cfg4_variant_device(cfg)
+        fmt = N.FMT_BITS
     elif cfg == "cfg5":
         full = configs.cfg5_device()
         fmt = N.FMT_U8
@@ -242,7 +245,7 @@ def host_workload(cfg: str, spec):
         return configs.cfg1_array(), "same bytes as the GPU arm"
     if cfg == "cfg2":
         return configs.cfg2_array(), "same bytes as the GPU arm"
-    if cfg in ("cfg3", "cfg4"):
+    if cfg in ("cfg3", "cfg4", "cfg4_p99", "cfg4_planted"):
         n, thr = spec["rows"], configs.thr53(spec["p"])
         words = (spec["cols"] + 31) // 32
         out = (np.empty((n, spec["cols"]), np.uint8) if cfg == "cfg3" else np.empty((n, words), np.uint32))
@@ -263,6 +266,11 @@ def host_workload(cfg: str, spec):
             k = spec["square"]
             top, left = configs.cfg3_square_pos(spec["seed"], n, k)
             out[top:top + k, left:left + k] = 1
+        elif "square" in spec:  # bit-packed planted square
+            k = spec["square"]
+            top, left = configs.planted_pos(spec["seed"], n, k)
+            for c in range(left, left + k):
+                out[top:top + k, c >> 5] |= np.uint32(1 << (c & 31))
         return out, "same bytes as the GPU arm"
     import scipy.fft as sfft
     n, sigma, q = spec["rows"], spec["sigma"], spec["q"]
@@ -354,7 +362,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--config", default="cfg4",
+                    choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "cfg4_p99", "cfg4_planted"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")

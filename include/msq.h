@@ -96,6 +96,8 @@ typedef struct {
 #define MSQ_PLAN_SINGLE_TEAM 4  /* team engine: one team per matrix (rows <= 2040) */
 #define MSQ_PLAN_CLIMB_FIXUP 8  /* band-boundary fix-up by the per-depth climb (fixup_kernel)
                                    instead of the window search (fixup2_kernel) */
+#define MSQ_PLAN_PASS1 16       /* bit-packed bands the strip pass leaves (or all of them):
+                                   pass1_kernel instead of ubits_kernel */
 
 /* Build a plan.  nbands <= 0 picks a default (one band per SM, bands of
  * >= 64 rows, <= 65535 rows each).  Returns MSQ_EINVAL for unsupported
@@ -219,6 +221,9 @@ int msq_compose_carry(const uint32_t* d_summaries, const int64_t* h_rank_rows, i
                       int32_t rank, int64_t cols, uint32_t* d_base_carry, void* stream);
 int msq_rank_fixup(const msq_plan* plan, void* d_ws, const uint32_t* d_base_carry,
                    msq_devresult* d_result, void* stream);
+/* d_out[0] = max(key_pass1, key_fix), d_out[1] = status & 1: the two int64
+ * the ranks all-reduce(max) in step 6 (one tiny kernel on `stream`). */
+int msq_rank_key_status(const msq_devresult* d_result, int64_t* d_out, void* stream);
 
 /* Intermediate outputs (tests): per band leading-ones depth e, bottom run b
  * (uint16 [nbands][words*32]) and all-ones masks (uint32 [nbands][words]),

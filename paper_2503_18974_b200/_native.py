@@ -16,7 +16,7 @@ HEADER = os.path.join(os.path.dirname(_PKG), "include", "msq.h")
 
 MSQ_OK, MSQ_EINVAL, MSQ_EVALUE, MSQ_ECUDA, MSQ_ENOMEM = 0, 1, 2, 3, 4
 FMT_U8, FMT_BITS = 0, 1
-PLAN_NO_STRIP, PLAN_NO_SEED, PLAN_SINGLE_TEAM, PLAN_CLIMB_FIXUP = 1, 2, 4, 8
+PLAN_NO_STRIP, PLAN_NO_SEED, PLAN_SINGLE_TEAM, PLAN_CLIMB_FIXUP, PLAN_PASS1 = 1, 2, 4, 8, 16
 
 
 class MsqResult(ctypes.Structure):
@@ -94,6 +94,7 @@ def load():
         "msq_rank_summary": ([PP, P, P, P], ctypes.c_int),
         "msq_compose_carry": ([P, P, I32, I32, I64, P, P], ctypes.c_int),
         "msq_rank_fixup": ([PP, P, P, P, P], ctypes.c_int),
+        "msq_rank_key_status": ([P, P, P], ctypes.c_int),
         "msq_ws_views": ([PP, P, P, P, P, P], ctypes.c_int),
         "msq_gen_hash": ([I32, U64, U64, I64, I64, I64, I64, P, P], ctypes.c_int),
         "msq_last_launch_count": ([], I32),

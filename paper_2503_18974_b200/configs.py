@@ -39,6 +39,13 @@ CONFIGS = {
              "cols": 16384, "fmt": "u8", "batch": 1, "seed": 3, "p": 0.95, "square": 2048},
     "cfg4": {"workload": "cfg4: 65536^2 bit-packed u32 Bernoulli(0.999)", "rows": 65536,
              "cols": 65536, "fmt": "bits", "batch": 1, "seed": 4, "p": 0.999},
+    # extra bit-packed workloads (not BASELINE configs): answers outside the strip
+    # pass's window -- a sparser background, and a planted square far above it
+    "cfg4_p99": {"workload": "extra: 65536^2 bit-packed u32 Bernoulli(0.99)", "rows": 65536,
+                 "cols": 65536, "fmt": "bits", "batch": 1, "seed": 41, "p": 0.99},
+    "cfg4_planted": {"workload": "extra: 65536^2 bit-packed u32 Bernoulli(0.999) + planted 4096^2",
+                     "rows": 65536, "cols": 65536, "fmt": "bits", "batch": 1, "seed": 42, "p": 0.999,
+                     "square": 4096},
     "cfg5": {"workload": "cfg5: 32768^2 u8 Gaussian-blob mask (sigma 64, 60% ones)",
              "rows": 32768, "cols": 32768, "fmt": "u8", "batch": 1, "seed": 5,
              "sigma": 64.0, "q": 0.4},
@@ -125,6 +132,26 @@ def cfg3_device(seed: int = 3, n: int = 16384, k: int = 2048, p: float = 0.95, d
 
 def cfg4_device(seed: int = 4, n: int = 65536, p: float = 0.999, device="cuda"):
     return device_hash("bits", seed, p, n, n, device)
+
+
+def planted_pos(seed: int, n: int, k: int) -> tuple[int, int]:
+    r = random.Random(seed)
+    return r.randint(0, n - k), r.randint(0, n - k)
+
+
+def cfg4_variant_device(name: str, device="cuda"):
+    """The extra bit-packed workloads (cfg4_p99, cfg4_planted) on the device."""
+    c = CONFIGS[name]
+    w = device_hash("bits", c["seed"], c["p"], c["rows"], c["cols"], device)
+    if "square" in c:
+        k = c["square"]
+        top, left = planted_pos(c["seed"], c["rows"], k)
+        # whole words inside the square at once, the two partial words bit by bit
+        a0, a1 = (left + 31) // 32, (left + k) // 32
+        w[top:top + k, a0:a1] = -1
+        for cc in list(range(left, min(left + k, 32 * a0))) + list(range(max(32 * a1, left), left + k)):
+            w[top:top + k, cc >> 5] |= (1 << (cc & 31)) if (cc & 31) != 31 else -(1 << 31)
+    return w
 
 
 def blob_mask_torch(n: int, sigma: float, q: float, seed: int, device="cuda"):

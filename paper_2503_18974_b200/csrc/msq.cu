@@ -18,6 +18,7 @@
 #include "msq_team.cuh"
 #include "msq_strip.cuh"
 #include "msq_ustrip.cuh"
+#include "msq_ubits.cuh"
 #include "msq_fixup2.cuh"
 #include "msq_dp.cuh"
 #include "msq_ingest.cuh"
@@ -95,6 +96,16 @@ int ustrip_slots(const msq_plan* p) {
 int ustrip_smem(const msq_plan* p) {
     return ustrip_slots(p) * ustrip_rows_per_slot(p) * p->row_stage_bytes + ustrip_fixed_smem();
 }
+// ---- bit-packed strip pass (msq_ubits.cuh): any threshold, bands <= 504 rows
+int ubits_warps(const msq_plan* p) { return (int)ceil_div(p->words, msq::UB_STRIDE); }
+bool ubits_applies(const msq_plan* p) {
+    if (p->flags & MSQ_PLAN_PASS1) return false;  // experiments
+    const int R = ustrip_rows_per_slot(p);
+    return p->fmt == MSQ_FMT_BITS && p->batch == 1 && p->nbands > 1 && R > 0 && p->words % 4 == 0 &&
+           (p->ld * 4) % 16 == 0 && p->row_stage_bytes == p->words * 4 && ubits_warps(p) <= msq::UB_MAXWARPS &&
+           p->words >= 32 && ceil_div(p->rows, p->nbands) <= msq::ubits_maxh(R);
+}
+
 bool ustrip_applies(const msq_plan* p) {
     if (p->flags & MSQ_PLAN_NO_STRIP) return false;  // experiments
     const int R = ustrip_rows_per_slot(p);
@@ -221,6 +232,24 @@ cudaError_t launch_pass1(const msq_plan* pl, const msq::Pass1Params& prm, cudaSt
 
 // band passes: the strip pass (when it applies) and pass1_kernel for the bands it left
 template <int R>
+cudaError_t launch_ubits_t(const msq_plan* pl, const msq::UStripParams& up, cudaStream_t st) {
+    static bool attr_set[64] = {false};
+    cudaError_t e = set_smem_attr(msq::ubits_kernel<R>, attr_set);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};  // programmatic dependent of the seed
+    cfg.gridDim = dim3((unsigned)pl->nbands);
+    cfg.blockDim = dim3((unsigned)((up.nwarps + 1) * 32));
+    cfg.dynamicSmemBytes = (size_t)ustrip_smem(pl);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, msq::ubits_kernel<R>, up);
+}
+
+template <int R>
 cudaError_t launch_ustrip_t(const msq_plan* pl, const msq::UStripParams& up, cudaStream_t st) {
     static bool attr_set[64] = {false};
     cudaError_t e = set_smem_attr(msq::ustrip_kernel<R>, attr_set);
@@ -236,6 +265,37 @@ cudaError_t launch_ustrip_t(const msq_plan* pl, const msq::UStripParams& up, cud
     cfg.attrs = at;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, msq::ustrip_kernel<R>, up);
+}
+
+cudaError_t launch_ubits(const msq_plan* pl, const msq::Pass1Params& prm, const void* src, const int* redo,
+                         cudaStream_t st) {
+    {
+        msq::UStripParams up{};
+        up.src = (const uint8_t*)src;
+        up.ld = pl->ld * 4;
+        up.rows = (int)pl->rows;
+        up.cols = (int)pl->cols;
+        up.W = pl->words;
+        up.nbands = pl->nbands;
+        up.cols_pad = pl->words * 32;
+        up.row_base = pl->row_base;
+        up.nslots = ustrip_slots(pl);
+        up.row_bytes = pl->row_stage_bytes;
+        up.nwarps = ubits_warps(pl);
+        up.share = pl->deterministic ? 0 : 1;
+        up.zb = prm.zb;
+        up.e_out = prm.e_out;
+        up.ao_out = prm.ao_out;
+        up.band_keys = prm.band_keys;
+        up.results = prm.results;
+        up.redo = redo;
+        switch (ustrip_rows_per_slot(pl)) {
+            case 8: return launch_ubits_t<8>(pl, up, st);
+            case 4: return launch_ubits_t<4>(pl, up, st);
+            case 2: return launch_ubits_t<2>(pl, up, st);
+            default: return launch_ubits_t<1>(pl, up, st);
+        }
+    }
 }
 
 cudaError_t launch_band_pass(const msq_plan* pl, msq::Pass1Params prm, void* ws, const void* src, cudaStream_t st,
@@ -306,6 +366,10 @@ cudaError_t launch_band_pass(const msq_plan* pl, msq::Pass1Params prm, void* ws,
         if (e != cudaSuccess) return e;
         prm.redo = sp.redo;
         *nlaunch = 2;
+        // bands the strip pass left (start threshold outside [96, 222] or passed 222)
+        if (ubits_applies(pl)) return launch_ubits(pl, prm, src, sp.redo, st);
+    } else if (prm.write_summaries && ubits_applies(pl) && ((uintptr_t)src % 16) == 0) {
+        return launch_ubits(pl, prm, src, nullptr, st);
     }
     return launch_pass1(pl, prm, st);
 }
@@ -1213,6 +1277,13 @@ int msq_rank_band_pass(const msq_plan* pl, const void* d_src, void* d_ws, msq_de
     const cudaError_t e = launch_band_pass(pl, p1, d_ws, d_src, (cudaStream_t)stream, &nl);
     g_last_launches = nl;
     return cuda_status(e);
+}
+
+int msq_rank_key_status(const msq_devresult* d_result, int64_t* d_out, void* stream) {
+    if (!d_result || !d_out) return MSQ_EINVAL;
+    msq::key_status_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((const unsigned char*)d_result, (long long*)d_out);
+    g_last_launches = 1;
+    return cuda_status(cudaGetLastError());
 }
 
 int msq_rank_summary(const msq_plan* pl, const void* d_ws, uint32_t* d_summary, void* stream) {

@@ -32,7 +32,8 @@
 //     filter first (a t-run holds ceil((t-62)/32) consecutive whole words with no
 //     zero in their last t rows: the word's last zero row, two ballots, shifted
 //     ANDs); then eligibility E = {z <= q - t} (8 LOP3), the run entering each
-//     word (one shuffle for t <= 33, a segmented warp scan above), and the
+//     word (one shuffle for t <= 33, two for t <= 65, a segmented warp scan
+//     above), and the
 //     leftmost window end in the warp's own words -> raise.
 #pragma once
 
@@ -57,6 +58,7 @@ struct UStripParams {
     uint32_t* ao_out;
     unsigned long long* band_keys;
     unsigned char* results;
+    const int* redo;  // optional [nbands] (ubits_kernel): 0 = band done by strip_kernel
 };
 
 __host__ __device__ __forceinline__ int ustrip_maxh(int R) { return 256 - R; }
@@ -249,6 +251,15 @@ __global__ void __launch_bounds__(640, 1) ustrip_kernel(const UStripParams p) {
                     const int prev1 = __shfl_up_sync(0xFFFFFFFFu, suf1, 1);
                     rin0 = lane ? prev0 : 0;
                     rin1 = lane ? prev1 : last0;
+                } else if (t <= 65) {
+                    // windows span <= 3 words: min(run, 64) from the two previous words
+                    const int s01 = __shfl_up_sync(0xFFFFFFFFu, suf0, 1), s02 = __shfl_up_sync(0xFFFFFFFFu, suf0, 2);
+                    const int s11 = __shfl_up_sync(0xFFFFFFFFu, suf1, 1), s12 = __shfl_up_sync(0xFFFFFFFFu, suf1, 2);
+                    const int q31 = __shfl_sync(0xFFFFFFFFu, suf0, 31), q30 = __shfl_sync(0xFFFFFFFFu, suf0, 30);
+                    const int a0_ = lane >= 1 ? s01 : 0, b0_ = lane >= 2 ? s02 : 0;
+                    const int a1_ = lane >= 1 ? s11 : q31, b1_ = lane >= 2 ? s12 : (lane == 1 ? q31 : q30);
+                    rin0 = a0_ == 32 ? 32 + b0_ : a0_;
+                    rin1 = a1_ == 32 ? 32 + b1_ : a1_;
                 } else {
                     // segmented inclusive scans: run ending at bit 31 of each word
                     int v0 = suf0 | ((int)full0 << 16), v1 = suf1 | ((int)full1 << 16);

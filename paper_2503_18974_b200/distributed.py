@@ -63,6 +63,7 @@ class GpuBackend:
         self.res = torch.zeros(32, dtype=torch.uint8, device=dev)
         self.summary = torch.empty(cols, dtype=torch.int32, device=dev)
         self.base = torch.empty(cols, dtype=torch.int32, device=dev)
+        self.ks = torch.zeros(2, dtype=torch.int64, device=dev)
         self.cols = cols
         self.lib = N.load()
         self.launches = 0
@@ -118,11 +119,12 @@ class GpuBackend:
         self.launches += 2 if nb > 0 else 0  # carry scan + fix-up
 
     def key_status(self):
-        """int64 tensor [key, status] for the all-reduce (keys < 2^63)."""
-        v = self.res.view(self.torch.int64)
-        key = self.torch.maximum(v[0], v[1]).reshape(1)
-        status = (v[2] & 0xFFFFFFFF).reshape(1)
-        return self.torch.cat([key, status])
+        """int64 tensor [key, status] for the all-reduce (keys < 2^63), written
+        by one library kernel (msq_rank_key_status) into a persistent buffer."""
+        N.check(self.lib.msq_rank_key_status(ctypes.c_void_p(self.res.data_ptr()),
+                                             ctypes.c_void_p(self.ks.data_ptr()), self._stream()))
+        self.launches += 1
+        return self.ks
 
 
 def _all_gather(out, t, group=None):

@@ -1,4 +1,4 @@
-"""Row-band sharding logic under gloo (world sizes 2 and 3, CPU, no GPU).
+"""Row-band sharding logic under gloo (world sizes 2, 3 and 4, CPU, no GPU).
 
 RowBandSolver (paper_2503_18974_b200/distributed.py) runs the same exchange it
 runs over NCCL on the GPU box -- all-gather of per-rank bottom runs, carry
@@ -61,7 +61,7 @@ def _worker(rank, world, port, fmt, results):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,fmt", [(2, 0), (3, 0), (2, 1)])
+@pytest.mark.parametrize("world,fmt", [(2, 0), (3, 0), (4, 0), (2, 1), (4, 1)])
 def test_row_band_sharding_matches_whole_matrix(world, fmt):
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     here = os.path.dirname(os.path.abspath(__file__))

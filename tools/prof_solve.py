@@ -12,7 +12,9 @@ from paper_2503_18974_b200.squares import Solver  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
 build.build()
 spec = configs.CONFIGS[cfg]
-if cfg == "cfg4":
+if cfg in ("cfg4_p99", "cfg4_planted"):
+    src, fmt = configs.cfg4_variant_device(cfg), N.FMT_BITS
+elif cfg == "cfg4":
     src, fmt = configs.cfg4_device(), N.FMT_BITS
 elif cfg == "cfg5":
     src, fmt = configs.cfg5_device(), N.FMT_U8
