@@ -166,7 +166,75 @@ __global__ void __launch_bounds__(640, 1) ustrip_kernel(const UStripParams p) {
     bool any_nz = true;
     uint32_t bad = 0u;
 
+    // leftmost end (global column) of a window of t eligible columns ending in one of
+    // the warp's own words, or -1; E0/E1 = eligibility of window words lane, lane+32
+    auto exact_end = [&](const uint32_t E0, const uint32_t E1, const int t) -> int {
+        const uint32_t full0 = E0 == 0xFFFFFFFFu, full1 = E1 == 0xFFFFFFFFu;
+        const int suf0 = full0 ? 32 : __clz(~E0), suf1 = full1 ? 32 : __clz(~E1);
+        const int pre0 = full0 ? 32 : __ffs(~E0) - 1, pre1 = full1 ? 32 : __ffs(~E1) - 1;
+        int rin0, rin1;  // eligible run entering each word from the left (capped where exactness allows)
+        if (t <= 33) {
+            // windows span <= 2 words: min(run, 32) of the previous word suffices
+            const int prev0 = __shfl_up_sync(0xFFFFFFFFu, suf0, 1);
+            const int last0 = __shfl_sync(0xFFFFFFFFu, suf0, 31);
+            const int prev1 = __shfl_up_sync(0xFFFFFFFFu, suf1, 1);
+            rin0 = lane ? prev0 : 0;
+            rin1 = lane ? prev1 : last0;
+        } else if (t <= 65) {
+            // windows span <= 3 words: min(run, 64) from the two previous words
+            const int s01 = __shfl_up_sync(0xFFFFFFFFu, suf0, 1), s02 = __shfl_up_sync(0xFFFFFFFFu, suf0, 2);
+            const int s11 = __shfl_up_sync(0xFFFFFFFFu, suf1, 1), s12 = __shfl_up_sync(0xFFFFFFFFu, suf1, 2);
+            const int q31 = __shfl_sync(0xFFFFFFFFu, suf0, 31), q30 = __shfl_sync(0xFFFFFFFFu, suf0, 30);
+            const int a0_ = lane >= 1 ? s01 : 0, b0_ = lane >= 2 ? s02 : 0;
+            const int a1_ = lane >= 1 ? s11 : q31, b1_ = lane >= 2 ? s12 : (lane == 1 ? q31 : q30);
+            rin0 = a0_ == 32 ? 32 + b0_ : a0_;
+            rin1 = a1_ == 32 ? 32 + b1_ : a1_;
+        } else {
+            // segmented inclusive scans: run ending at bit 31 of each word
+            int v0 = suf0 | ((int)full0 << 16), v1 = suf1 | ((int)full1 << 16);
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u0 = __shfl_up_sync(0xFFFFFFFFu, v0, o);
+                const int u1 = __shfl_up_sync(0xFFFFFFFFu, v1, o);
+                if (lane >= o) {
+                    if (v0 >> 16) v0 = ((v0 & 0xFFFF) + (u0 & 0xFFFF)) | (u0 & 0x10000);
+                    if (v1 >> 16) v1 = ((v1 & 0xFFFF) + (u1 & 0xFFFF)) | (u1 & 0x10000);
+                }
+            }
+            const int run31 = __shfl_sync(0xFFFFFFFFu, v0, 31) & 0xFFFF;  // run at the end of word 31
+            // the second half's scan continues the first half's run where it is all-eligible
+            const int tot1 = (v1 >> 16) ? (v1 & 0xFFFF) + run31 : (v1 & 0xFFFF);
+            const int pv0 = __shfl_up_sync(0xFFFFFFFFu, v0 & 0xFFFF, 1);
+            const int pt1 = __shfl_up_sync(0xFFFFFFFFu, tot1, 1);
+            rin0 = lane ? pv0 : 0;
+            rin1 = lane ? pt1 : run31;
+        }
+        // leftmost window end in each own word (bit index, or -1): the entering run
+        // reaches a window end at bit max(0, t-1-rin) if it continues into the word
+        // that far (pre > that bit); otherwise windows inside the word (t <= 32)
+        int end0 = -1, end1 = -1;
+        if (pre0 > 0 && rin0 + pre0 >= t) end0 = max(0, t - 1 - rin0);
+        else if (t <= 32) {
+            const uint32_t ww = windows_in_word(E0, t);
+            if (ww) end0 = __ffs(ww) - 1 + t - 1;
+        }
+        if (pre1 > 0 && rin1 + pre1 >= t) end1 = max(0, t - 1 - rin1);
+        else if (t <= 32) {
+            const uint32_t ww = windows_in_word(E1, t);
+            if (ww) end1 = __ffs(ww) - 1 + t - 1;
+        }
+        if (!own0) end0 = -1;
+        if (!own1) end1 = -1;
+        const unsigned b0 = __ballot_sync(0xFFFFFFFFu, end0 >= 0);
+        const unsigned b1 = __ballot_sync(0xFFFFFFFFu, end1 >= 0);
+        if (!(b0 | b1)) return -1;
+        const int l = b0 ? __ffs(b0) - 1 : __ffs(b1) - 1;
+        const int e = __shfl_sync(0xFFFFFFFFu, b0 ? end0 : end1, l);
+        return 32 * (base_word + (b0 ? l : 32 + l)) + e;
+    };
+
     int t = sh[0];
+    bool climbing = false;  // every row of the previous slot raised
     unsigned long long key = 0ull;
     const uint32_t ring_s = smem_addr(ring);
     int s = 0;
@@ -182,9 +250,12 @@ __global__ void __launch_bounds__(640, 1) ustrip_kernel(const UStripParams p) {
 #pragma unroll
         for (int pl = 0; pl < USTRIP_P; ++pl) hm[pl] = 0u - ((qbase >> pl) & 1u);
         mbar_wait(&full[s], par);
+        // ---- the slot's rows as bits (bytes validated on the way)
+        uint32_t pw0[R], pw1[R];
 #pragma unroll
         for (int b = 0; b < R; ++b) {
-            if (b >= nrows) break;
+            pw0[b] = pw1[b] = 0xFFFFFFFFu;
+            if (b >= nrows) continue;
             const uint32_t rs = slot_s + (uint32_t)(b * p.row_bytes);
             uint4 v0a, v0b, v1a, v1b;
             asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -197,9 +268,40 @@ __global__ void __launch_bounds__(640, 1) ustrip_kernel(const UStripParams p) {
                          : "=r"(v1b.x), "=r"(v1b.y), "=r"(v1b.z), "=r"(v1b.w) : "r"(rs + off1b));
             bad |= v0a.x | v0a.y | v0a.z | v0a.w | v0b.x | v0b.y | v0b.z | v0b.w;
             bad |= v1a.x | v1a.y | v1a.z | v1a.w | v1b.x | v1b.y | v1b.z | v1b.w;
-            const uint32_t w0 = __byte_perm(us_half(v0a), us_half(v0b), sel);
-            const uint32_t w1 = __byte_perm(us_half(v1a), us_half(v1b), sel);
-            const uint32_t zm0 = ~w0 & VAL0, zm1 = ~w1 & VAL1;
+            pw0[b] = __byte_perm(us_half(v0a), us_half(v0b), sel);
+            pw1[b] = __byte_perm(us_half(v1a), us_half(v1b), sel);
+        }
+        // ---- climbing: every row of the last slot raised.  Test the slot's last row
+        // first at t + R - 1 from the state before the slot (a column zeroed in the
+        // slot is lower than R there): a square of side t + R - 1 ending there
+        // contains one of side t + i ending at row i of the slot, so on success
+        // every row raises in turn and this window is the last raise.
+        bool spec = false;
+        if (climbing && nrows == R && R > 1 && row0 + 1 >= t) {
+            uint32_t cz0 = 0u, cz1 = 0u;
+#pragma unroll
+            for (int b = 0; b < R; ++b) {
+                cz0 |= ~pw0[b];
+                cz1 |= ~pw1[b];
+            }
+            const int ts = t + R - 1;
+            const uint32_t c = (uint32_t)(row0 + R - t);  // q of the last row - ts
+            const int col = exact_end(us_le(Z0, c) & VAL0 & ~cz0, us_le(Z1, c) & VAL1 & ~cz1, ts);
+            if (col >= 0) {
+                key = pack_key(ts, p.row_base + r0 + row0 + R - 1, col);
+                if (lane == 0 && p.share) {
+                    atomicMax(&sh[1], ts);
+                    atomicMax(res_best(result), ts);
+                }
+                t = ts + 1;
+                spec = true;
+            }
+        }
+        int raises = spec ? R : 0;
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+            if (b >= nrows) break;
+            const uint32_t zm0 = ~pw0[b] & VAL0, zm1 = ~pw1[b] & VAL1;
             const int qrow = row0 + R + b;
             ZW0 = zm0 ? qrow : ZW0;
             ZW1 = zm1 ? qrow : ZW1;
@@ -222,6 +324,7 @@ __global__ void __launch_bounds__(640, 1) ustrip_kernel(const UStripParams p) {
                 NZ1 &= ~zm1;
                 any_nz = __any_sync(0xFFFFFFFFu, (NZ0 | NZ1) != 0u);
             }
+            if (spec) continue;
             const int row = row0 + b;  // band-local row (0-based)
             bool test = row + 1 >= t;  // warp-uniform: band-local heights can reach t
             if (test && t >= 63) {
@@ -239,78 +342,19 @@ __global__ void __launch_bounds__(640, 1) ustrip_kernel(const UStripParams p) {
             }
             if (test) {
                 const uint32_t c = (uint32_t)(row + R - t);  // eligible: z <= q - t
-                const uint32_t E0 = us_le(Z0, c) & VAL0, E1 = us_le(Z1, c) & VAL1;
-                const uint32_t full0 = E0 == 0xFFFFFFFFu, full1 = E1 == 0xFFFFFFFFu;
-                const int suf0 = full0 ? 32 : __clz(~E0), suf1 = full1 ? 32 : __clz(~E1);
-                const int pre0 = full0 ? 32 : __ffs(~E0) - 1, pre1 = full1 ? 32 : __ffs(~E1) - 1;
-                int rin0, rin1;  // eligible run entering each word from the left (capped where exactness allows)
-                if (t <= 33) {
-                    // windows span <= 2 words: min(run, 32) of the previous word suffices
-                    const int prev0 = __shfl_up_sync(0xFFFFFFFFu, suf0, 1);
-                    const int last0 = __shfl_sync(0xFFFFFFFFu, suf0, 31);
-                    const int prev1 = __shfl_up_sync(0xFFFFFFFFu, suf1, 1);
-                    rin0 = lane ? prev0 : 0;
-                    rin1 = lane ? prev1 : last0;
-                } else if (t <= 65) {
-                    // windows span <= 3 words: min(run, 64) from the two previous words
-                    const int s01 = __shfl_up_sync(0xFFFFFFFFu, suf0, 1), s02 = __shfl_up_sync(0xFFFFFFFFu, suf0, 2);
-                    const int s11 = __shfl_up_sync(0xFFFFFFFFu, suf1, 1), s12 = __shfl_up_sync(0xFFFFFFFFu, suf1, 2);
-                    const int q31 = __shfl_sync(0xFFFFFFFFu, suf0, 31), q30 = __shfl_sync(0xFFFFFFFFu, suf0, 30);
-                    const int a0_ = lane >= 1 ? s01 : 0, b0_ = lane >= 2 ? s02 : 0;
-                    const int a1_ = lane >= 1 ? s11 : q31, b1_ = lane >= 2 ? s12 : (lane == 1 ? q31 : q30);
-                    rin0 = a0_ == 32 ? 32 + b0_ : a0_;
-                    rin1 = a1_ == 32 ? 32 + b1_ : a1_;
-                } else {
-                    // segmented inclusive scans: run ending at bit 31 of each word
-                    int v0 = suf0 | ((int)full0 << 16), v1 = suf1 | ((int)full1 << 16);
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int u0 = __shfl_up_sync(0xFFFFFFFFu, v0, o);
-                        const int u1 = __shfl_up_sync(0xFFFFFFFFu, v1, o);
-                        if (lane >= o) {
-                            if (v0 >> 16) v0 = ((v0 & 0xFFFF) + (u0 & 0xFFFF)) | (u0 & 0x10000);
-                            if (v1 >> 16) v1 = ((v1 & 0xFFFF) + (u1 & 0xFFFF)) | (u1 & 0x10000);
-                        }
-                    }
-                    const int run31 = __shfl_sync(0xFFFFFFFFu, v0, 31) & 0xFFFF;  // run at the end of word 31
-                    // the second half's scan continues the first half's run where it is all-eligible
-                    const int tot1 = (v1 >> 16) ? (v1 & 0xFFFF) + run31 : (v1 & 0xFFFF);
-                    const int pv0 = __shfl_up_sync(0xFFFFFFFFu, v0 & 0xFFFF, 1);
-                    const int pt1 = __shfl_up_sync(0xFFFFFFFFu, tot1, 1);
-                    rin0 = lane ? pv0 : 0;
-                    rin1 = lane ? pt1 : run31;
-                }
-                // leftmost window end in each own word (bit index, or -1)
-                int end0 = -1, end1 = -1;
-                // the entering run reaches a window end at bit max(0, t-1-rin) if it
-                // continues into the word that far (pre > that bit)
-                if (pre0 > 0 && rin0 + pre0 >= t) end0 = max(0, t - 1 - rin0);
-                else if (t <= 32) {
-                    const uint32_t ww = windows_in_word(E0, t);
-                    if (ww) end0 = __ffs(ww) - 1 + t - 1;
-                }
-                if (pre1 > 0 && rin1 + pre1 >= t) end1 = max(0, t - 1 - rin1);
-                else if (t <= 32) {
-                    const uint32_t ww = windows_in_word(E1, t);
-                    if (ww) end1 = __ffs(ww) - 1 + t - 1;
-                }
-                if (!own0) end0 = -1;
-                if (!own1) end1 = -1;
-                const unsigned b0 = __ballot_sync(0xFFFFFFFFu, end0 >= 0);
-                const unsigned b1 = __ballot_sync(0xFFFFFFFFu, end1 >= 0);
-                if (b0 | b1) {  // warp-uniform: raise at this row
-                    const int l = b0 ? __ffs(b0) - 1 : __ffs(b1) - 1;
-                    const int e = __shfl_sync(0xFFFFFFFFu, b0 ? end0 : end1, l);
-                    const int aw = base_word + (b0 ? l : 32 + l);
-                    key = pack_key(t, p.row_base + r0 + row, 32ll * aw + e);
+                const int col = exact_end(us_le(Z0, c) & VAL0, us_le(Z1, c) & VAL1, t);
+                if (col >= 0) {  // warp-uniform: raise at this row
+                    key = pack_key(t, p.row_base + r0 + row, col);
                     if (lane == 0 && p.share) {
                         atomicMax(&sh[1], t);
                         atomicMax(res_best(result), t);
                     }
                     ++t;
+                    ++raises;
                 }
             }
         }
+        climbing = raises == nrows && nrows == R;
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         // shared best side (ties): the CTA's every slot, the grid's every 8 slots
