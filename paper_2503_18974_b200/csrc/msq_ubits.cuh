@@ -126,7 +126,80 @@ __global__ void __launch_bounds__(640, 1) ubits_kernel(const UStripParams p) {
     }
     const size_t sum_base = (size_t)band * p.cols_pad;
 
+    // leftmost end (global column) of a window of t eligible columns ending in one of
+    // the warp's own words at the row whose stored form minus t is c, or -1;
+    // cz = columns known ineligible (zeroed since the planes were last exact)
+    auto exact_end = [&](const uint32_t c, const int t, const uint32_t (&cz)[4]) -> int {
+        uint32_t E[4];
+        int suf[4], pre[4];
+        bool fl[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            E[i] = ub_le<UB_P>(Z[i], c) & VAL[i] & ~cz[i];
+            fl[i] = E[i] == 0xFFFFFFFFu;
+            suf[i] = fl[i] ? 32 : __clz(~E[i]);
+            pre[i] = fl[i] ? 32 : __ffs(~E[i]) - 1;
+        }
+        int rin[4];
+        if (t <= 33) {
+            int last_prev = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int pv = __shfl_up_sync(0xFFFFFFFFu, suf[i], 1);
+                rin[i] = lane ? pv : last_prev;
+                last_prev = __shfl_sync(0xFFFFFFFFu, suf[i], 31);
+            }
+        } else if (t <= 65) {
+            // windows span <= 3 words: min(run, 64) from the two previous words
+            int p31 = 0, p30 = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int s1 = __shfl_up_sync(0xFFFFFFFFu, suf[i], 1);
+                const int s2 = __shfl_up_sync(0xFFFFFFFFu, suf[i], 2);
+                const int a = lane >= 1 ? s1 : p31;
+                const int bb = lane >= 2 ? s2 : (lane == 1 ? p31 : p30);
+                rin[i] = a == 32 ? 32 + bb : a;
+                p31 = __shfl_sync(0xFFFFFFFFu, suf[i], 31);
+                p30 = __shfl_sync(0xFFFFFFFFu, suf[i], 30);
+            }
+        } else {
+            int carry = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                int v = suf[i] | ((int)fl[i] << 16);
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int u = __shfl_up_sync(0xFFFFFFFFu, v, o);
+                    if (lane >= o && (v >> 16)) v = ((v & 0xFFFF) + (u & 0xFFFF)) | (u & 0x10000);
+                }
+                const int tot = (v >> 16) ? (v & 0xFFFF) + carry : (v & 0xFFFF);
+                const int pt = __shfl_up_sync(0xFFFFFFFFu, tot, 1);
+                rin[i] = lane ? pt : carry;
+                carry = __shfl_sync(0xFFFFFFFFu, tot, 31);
+            }
+        }
+        int endb[4];
+        unsigned bal[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            int e = -1;
+            if (pre[i] > 0 && rin[i] + pre[i] >= t) e = max(0, t - 1 - rin[i]);
+            else if (t <= 32) {
+                const uint32_t ww = windows_in_word(E[i], t);
+                if (ww) e = __ffs(ww) - 1 + t - 1;
+            }
+            endb[i] = own[i] ? e : -1;
+            bal[i] = __ballot_sync(0xFFFFFFFFu, endb[i] >= 0);
+        }
+        if (!(bal[0] | bal[1] | bal[2] | bal[3])) return -1;
+        const int i = bal[0] ? 0 : bal[1] ? 1 : bal[2] ? 2 : 3;
+        const int l = __ffs(bal[i]) - 1;
+        const int ev = __shfl_sync(0xFFFFFFFFu, i == 0 ? endb[0] : i == 1 ? endb[1] : i == 2 ? endb[2] : endb[3], l);
+        return 32 * (base_word + 32 * i + l) + ev;
+    };
+
     int t = sh[0];
+    bool climbing = false;  // every row of the previous slot raised
     unsigned long long key = 0ull;
     const uint32_t ring_s = smem_addr(ring);
     int s = 0;
@@ -153,6 +226,34 @@ __global__ void __launch_bounds__(640, 1) ubits_kernel(const UStripParams p) {
                 lastb[i] = -1;
             }
         };
+        // climbing (every row of the last slot raised): test the slot's last row first
+        // at t + R - 1 from the state before the slot (see ustrip_kernel)
+        bool spec = false;
+        if (climbing && nrows == R && R > 1 && row0 + 1 >= t) {
+            uint32_t cz[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int b = 0; b < R; ++b) {
+                const uint32_t rs = slot_s + (uint32_t)(b * p.row_bytes);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    uint32_t w;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(rs + off[i]));
+                    cz[i] |= ~w & VAL[i];
+                }
+            }
+            const int ts = t + R - 1;
+            const int col = exact_end((uint32_t)(row0 + R - t), ts, cz);
+            if (col >= 0) {
+                key = pack_key(ts, p.row_base + r0 + row0 + R - 1, col);
+                if (lane == 0 && p.share) {
+                    atomicMax(&sh[1], ts);
+                    atomicMax(res_best(result), ts);
+                }
+                t = ts + 1;
+                spec = true;
+            }
+        }
+        int raises = spec ? R : 0;
 #pragma unroll
         for (int b = 0; b < R; ++b) {
             if (b >= nrows) break;
@@ -192,6 +293,7 @@ __global__ void __launch_bounds__(640, 1) ubits_kernel(const UStripParams p) {
                     NZ[i] &= ~zm[i];
                 }
             }
+            if (spec) continue;
             const int row = row0 + b;
             bool test = row + 1 >= t;
             if (test && t <= R) flush();  // exact state for the small thresholds
@@ -211,83 +313,20 @@ __global__ void __launch_bounds__(640, 1) ubits_kernel(const UStripParams p) {
                 test = (X[0] | X[1] | X[2] | X[3]) != 0u;
             }
             if (test) {
-                const uint32_t c = (uint32_t)(row + R - t);
-                uint32_t E[4];
-                int suf[4], pre[4];
-                bool fl[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    E[i] = ub_le<UB_P>(Z[i], c) & VAL[i] & ~anyz[i];
-                    fl[i] = E[i] == 0xFFFFFFFFu;
-                    suf[i] = fl[i] ? 32 : __clz(~E[i]);
-                    pre[i] = fl[i] ? 32 : __ffs(~E[i]) - 1;
-                }
-                int rin[4];
-                if (t <= 33) {
-                    int last_prev = 0;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int pv = __shfl_up_sync(0xFFFFFFFFu, suf[i], 1);
-                        rin[i] = lane ? pv : last_prev;
-                        last_prev = __shfl_sync(0xFFFFFFFFu, suf[i], 31);
-                    }
-                } else if (t <= 65) {
-                    // windows span <= 3 words: min(run, 64) from the two previous words
-                    int p31 = 0, p30 = 0;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int s1 = __shfl_up_sync(0xFFFFFFFFu, suf[i], 1);
-                        const int s2 = __shfl_up_sync(0xFFFFFFFFu, suf[i], 2);
-                        const int a = lane >= 1 ? s1 : p31;
-                        const int bb = lane >= 2 ? s2 : (lane == 1 ? p31 : p30);
-                        rin[i] = a == 32 ? 32 + bb : a;
-                        p31 = __shfl_sync(0xFFFFFFFFu, suf[i], 31);
-                        p30 = __shfl_sync(0xFFFFFFFFu, suf[i], 30);
-                    }
-                } else {
-                    int carry = 0;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        int v = suf[i] | ((int)fl[i] << 16);
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const int u = __shfl_up_sync(0xFFFFFFFFu, v, o);
-                            if (lane >= o && (v >> 16)) v = ((v & 0xFFFF) + (u & 0xFFFF)) | (u & 0x10000);
-                        }
-                        const int tot = (v >> 16) ? (v & 0xFFFF) + carry : (v & 0xFFFF);
-                        const int pt = __shfl_up_sync(0xFFFFFFFFu, tot, 1);
-                        rin[i] = lane ? pt : carry;
-                        carry = __shfl_sync(0xFFFFFFFFu, tot, 31);
-                    }
-                }
-                int endb[4];
-                unsigned bal[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    int e = -1;
-                    if (pre[i] > 0 && rin[i] + pre[i] >= t) e = max(0, t - 1 - rin[i]);
-                    else if (t <= 32) {
-                        const uint32_t ww = windows_in_word(E[i], t);
-                        if (ww) e = __ffs(ww) - 1 + t - 1;
-                    }
-                    endb[i] = own[i] ? e : -1;
-                    bal[i] = __ballot_sync(0xFFFFFFFFu, endb[i] >= 0);
-                }
-                if (bal[0] | bal[1] | bal[2] | bal[3]) {  // warp-uniform: raise at this row
-                    const int i = bal[0] ? 0 : bal[1] ? 1 : bal[2] ? 2 : 3;
-                    const int l = __ffs(bal[i]) - 1;
-                    const int ev = __shfl_sync(0xFFFFFFFFu, i == 0 ? endb[0] : i == 1 ? endb[1] : i == 2 ? endb[2] : endb[3], l);
-                    const int aw = base_word + 32 * i + l;
-                    key = pack_key(t, p.row_base + r0 + row, 32ll * aw + ev);
+                const int col = exact_end((uint32_t)(row + R - t), t, anyz);
+                if (col >= 0) {  // warp-uniform: raise at this row
+                    key = pack_key(t, p.row_base + r0 + row, col);
                     if (lane == 0 && p.share) {
                         atomicMax(&sh[1], t);
                         atomicMax(res_best(result), t);
                     }
                     ++t;
+                    ++raises;
                 }
             }
         }
         flush();
+        climbing = raises == nrows && nrows == R;
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         const int g = max(ld_volatile(&sh[1]), gglob);
