@@ -87,6 +87,11 @@ typedef struct {
     int32_t flags;        /* MSQ_PLAN_* experiment switches; 0 from msq_plan_make */
     int32_t test_floor;   /* TEST ONLY: > 0 presets the shared best side (the caller
                              vouches that the answer is >= it); 0 from msq_plan_make */
+    int32_t col_chunks;   /* column chunks per band for the u8 / any-threshold bit-packed
+                             strip passes (one CTA per band and chunk; 1 from
+                             msq_plan_make): fewer, taller bands with the same CTA count,
+                             so the band summaries (carry scan, fix-up) shrink -- the
+                             tile strip pass then stands aside */
 } msq_plan;
 
 /* msq_plan.flags: experiment switches a caller may set on its own plan

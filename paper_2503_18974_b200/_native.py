@@ -43,7 +43,8 @@ class MsqPlan(ctypes.Structure):
                 ("teams_per_cta", ctypes.c_int32), ("tile_rows_l", ctypes.c_int32),
                 ("tl", ctypes.c_int32), ("grid", ctypes.c_int32), ("fix_threads", ctypes.c_int32),
                 ("fix_wpt", ctypes.c_int32), ("engine", ctypes.c_int32),
-                ("flags", ctypes.c_int32), ("test_floor", ctypes.c_int32)]
+                ("flags", ctypes.c_int32), ("test_floor", ctypes.c_int32),
+                ("col_chunks", ctypes.c_int32)]
 
 
 _lib = None

@@ -70,6 +70,7 @@ int strip_smem(const msq_plan* p) {
 }
 bool strip_applies(const msq_plan* p) {
     if (p->flags & MSQ_PLAN_NO_STRIP) return false;  // experiments
+    if (p->col_chunks > 1) return false;              // chunked plans: ubits_kernel
     const long long ld_bytes = p->ld * 4;
     return p->fmt == MSQ_FMT_BITS && p->batch == 1 && p->nbands > 1 && !p->deterministic &&
            p->words >= 2 * msq::STRIP_WORDS && p->words % 4 == 0 && p->row_stage_bytes % 16 == 0 &&
@@ -77,30 +78,45 @@ bool strip_applies(const msq_plan* p) {
            ceil_div(p->rows, p->nbands) <= 65535;
 }
 
-// ---- u8 strip pass (msq_ustrip.cuh): u8 single matrices, several bands
-int ustrip_warps(const msq_plan* p) { return (int)ceil_div(p->words, msq::USTRIP_STRIDE); }
+// ---- u8 / bit-packed strip passes (msq_ustrip.cuh, msq_ubits.cuh): single
+// matrices, several bands; a band may be split into column chunks (one CTA each)
+// so short bands still fill the GPU with few bands
+struct StripGeom {
+    int chunks, cw, warps, row_bytes;  // chunks per band, own words per chunk, warps, ring row bytes
+};
+StripGeom strip_geom(const msq_plan* p, int stride, int halo, int bpw) {
+    StripGeom g{};
+    g.chunks = std::max(1, p->col_chunks);
+    g.cw = (int)round_up(ceil_div(p->words, g.chunks), 4);
+    g.warps = (int)ceil_div(g.cw, stride);
+    g.row_bytes = (int)std::min<long long>(p->words, (long long)g.cw + halo) * bpw;
+    return g;
+}
+StripGeom ustrip_geom(const msq_plan* p) { return strip_geom(p, msq::USTRIP_STRIDE, msq::USTRIP_HALO, 32); }
+StripGeom ubits_geom(const msq_plan* p) { return strip_geom(p, msq::UB_STRIDE, msq::UB_HALO, 4); }
+int ustrip_warps(const msq_plan* p) { return ustrip_geom(p).warps; }
 int ustrip_fixed_smem() { return 2 * msq::USTRIP_MAXSLOTS * 8 + 64; }
 // rows per ring slot: the largest of 8/4/2/1 that leaves >= 3 slots
-int ustrip_rows_per_slot(const msq_plan* p) {
+int ustrip_rows_per_slot(int row_bytes) {
     const long long avail = kSmemMax - 256 - ustrip_fixed_smem();
     for (int R = 8; R >= 1; R /= 2)
-        if (avail / ((long long)R * p->row_stage_bytes) >= 3) return R;
+        if (avail / ((long long)R * row_bytes) >= 3) return R;
     return 0;
 }
-int ustrip_slots(const msq_plan* p) {
-    const int R = ustrip_rows_per_slot(p);
+int ustrip_slots(int row_bytes) {
+    const int R = ustrip_rows_per_slot(row_bytes);
     if (!R) return 0;
     const long long avail = kSmemMax - 256 - ustrip_fixed_smem();
-    return (int)std::min<long long>(msq::USTRIP_MAXSLOTS, avail / ((long long)R * p->row_stage_bytes));
+    return (int)std::min<long long>(msq::USTRIP_MAXSLOTS, avail / ((long long)R * row_bytes));
 }
-int ustrip_smem(const msq_plan* p) {
-    return ustrip_slots(p) * ustrip_rows_per_slot(p) * p->row_stage_bytes + ustrip_fixed_smem();
+int ustrip_smem(int row_bytes) {
+    return ustrip_slots(row_bytes) * ustrip_rows_per_slot(row_bytes) * row_bytes + ustrip_fixed_smem();
 }
 // ---- bit-packed strip pass (msq_ubits.cuh): any threshold, bands <= 504 rows
-int ubits_warps(const msq_plan* p) { return (int)ceil_div(p->words, msq::UB_STRIDE); }
+int ubits_warps(const msq_plan* p) { return ubits_geom(p).warps; }
 bool ubits_applies(const msq_plan* p) {
     if (p->flags & MSQ_PLAN_PASS1) return false;  // experiments
-    const int R = ustrip_rows_per_slot(p);
+    const int R = ustrip_rows_per_slot(ubits_geom(p).row_bytes);
     return p->fmt == MSQ_FMT_BITS && p->batch == 1 && p->nbands > 1 && R > 0 && p->words % 4 == 0 &&
            (p->ld * 4) % 16 == 0 && p->row_stage_bytes == p->words * 4 && ubits_warps(p) <= msq::UB_MAXWARPS &&
            p->words >= 32 && ceil_div(p->rows, p->nbands) <= msq::ubits_maxh(R);
@@ -108,7 +124,7 @@ bool ubits_applies(const msq_plan* p) {
 
 bool ustrip_applies(const msq_plan* p) {
     if (p->flags & MSQ_PLAN_NO_STRIP) return false;  // experiments
-    const int R = ustrip_rows_per_slot(p);
+    const int R = ustrip_rows_per_slot(ustrip_geom(p).row_bytes);
     return p->fmt == MSQ_FMT_U8 && p->batch == 1 && p->nbands > 1 && R > 0 && p->cols % 32 == 0 &&
            p->ld % 16 == 0 && p->row_stage_bytes == p->cols && ustrip_warps(p) <= msq::USTRIP_MAXWARPS &&
            p->words >= msq::USTRIP_WORDS && ceil_div(p->rows, p->nbands) <= msq::ustrip_maxh(R);
@@ -237,9 +253,9 @@ cudaError_t launch_ubits_t(const msq_plan* pl, const msq::UStripParams& up, cuda
     cudaError_t e = set_smem_attr(msq::ubits_kernel<R>, attr_set);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};  // programmatic dependent of the seed
-    cfg.gridDim = dim3((unsigned)pl->nbands);
+    cfg.gridDim = dim3((unsigned)(pl->nbands * up.nchunks));
     cfg.blockDim = dim3((unsigned)((up.nwarps + 1) * 32));
-    cfg.dynamicSmemBytes = (size_t)ustrip_smem(pl);
+    cfg.dynamicSmemBytes = (size_t)ustrip_smem(up.row_bytes);
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -255,9 +271,9 @@ cudaError_t launch_ustrip_t(const msq_plan* pl, const msq::UStripParams& up, cud
     cudaError_t e = set_smem_attr(msq::ustrip_kernel<R>, attr_set);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};  // programmatic dependent of the seed
-    cfg.gridDim = dim3((unsigned)pl->nbands);
+    cfg.gridDim = dim3((unsigned)(pl->nbands * up.nchunks));
     cfg.blockDim = dim3((unsigned)((up.nwarps + 1) * 32));
-    cfg.dynamicSmemBytes = (size_t)ustrip_smem(pl);
+    cfg.dynamicSmemBytes = (size_t)ustrip_smem(up.row_bytes);
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -279,9 +295,12 @@ cudaError_t launch_ubits(const msq_plan* pl, const msq::Pass1Params& prm, const 
         up.nbands = pl->nbands;
         up.cols_pad = pl->words * 32;
         up.row_base = pl->row_base;
-        up.nslots = ustrip_slots(pl);
-        up.row_bytes = pl->row_stage_bytes;
-        up.nwarps = ubits_warps(pl);
+        const StripGeom g = ubits_geom(pl);
+        up.nslots = ustrip_slots(g.row_bytes);
+        up.row_bytes = g.row_bytes;
+        up.nwarps = g.warps;
+        up.nchunks = g.chunks;
+        up.cw = g.cw;
         up.share = pl->deterministic ? 0 : 1;
         up.zb = prm.zb;
         up.e_out = prm.e_out;
@@ -289,7 +308,10 @@ cudaError_t launch_ubits(const msq_plan* pl, const msq::Pass1Params& prm, const 
         up.band_keys = prm.band_keys;
         up.results = prm.results;
         up.redo = redo;
-        switch (ustrip_rows_per_slot(pl)) {
+        if (g.chunks > 1 &&
+            cudaMemsetAsync(prm.band_keys, 0, sizeof(unsigned long long) * (size_t)pl->nbands, st) != cudaSuccess)
+            return cudaGetLastError();
+        switch (ustrip_rows_per_slot(g.row_bytes)) {
             case 8: return launch_ubits_t<8>(pl, up, st);
             case 4: return launch_ubits_t<4>(pl, up, st);
             case 2: return launch_ubits_t<2>(pl, up, st);
@@ -311,16 +333,22 @@ cudaError_t launch_band_pass(const msq_plan* pl, msq::Pass1Params prm, void* ws,
         up.nbands = pl->nbands;
         up.cols_pad = pl->words * 32;
         up.row_base = pl->row_base;
-        up.nslots = ustrip_slots(pl);
-        up.row_bytes = pl->row_stage_bytes;
-        up.nwarps = ustrip_warps(pl);
+        const StripGeom g = ustrip_geom(pl);
+        up.nslots = ustrip_slots(g.row_bytes);
+        up.row_bytes = g.row_bytes;
+        up.nwarps = g.warps;
+        up.nchunks = g.chunks;
+        up.cw = g.cw;
         up.share = pl->deterministic ? 0 : 1;
         up.zb = prm.zb;
         up.e_out = prm.e_out;
         up.ao_out = prm.ao_out;
         up.band_keys = prm.band_keys;
         up.results = prm.results;
-        switch (ustrip_rows_per_slot(pl)) {
+        if (g.chunks > 1 &&
+            cudaMemsetAsync(prm.band_keys, 0, sizeof(unsigned long long) * (size_t)pl->nbands, st) != cudaSuccess)
+            return cudaGetLastError();
+        switch (ustrip_rows_per_slot(g.row_bytes)) {
             case 8: return launch_ustrip_t<8>(pl, up, st);
             case 4: return launch_ustrip_t<4>(pl, up, st);
             case 2: return launch_ustrip_t<2>(pl, up, st);
@@ -822,6 +850,7 @@ int plan_band(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld
     p.team = p.threads;
     p.teams_per_cta = 1;
     int nb = nbands;
+    const int chunks = 1;  // callers may split the strip passes' bands into column chunks
     if (batch > 1) {
         nb = 1;
     } else if (nb <= 0) {
@@ -832,6 +861,7 @@ int plan_band(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld
     if (nb > 2048) return MSQ_EINVAL;
     if (batch > 1 && nb != 1) return MSQ_EINVAL;
     p.nbands = nb;
+    p.col_chunks = chunks;
     p.grid = nb * batch;
     p.tile_rows = 2;
     p.tile_rows_l = msq::BMAX;
@@ -1290,8 +1320,8 @@ int msq_rank_summary(const msq_plan* pl, const void* d_ws, uint32_t* d_summary, 
     if (!pl || !d_ws || !d_summary || pl->batch != 1) return MSQ_EINVAL;
     WsLayout L = ws_layout(pl);
     const uint8_t* w = (const uint8_t*)d_ws;
-    const int threads = 256;
-    const int blocks = (int)ceil_div(pl->cols, threads);
+    const int threads = 256;  // one warp per 32-column word
+    const int blocks = (int)ceil_div((long long)pl->words * 32, threads);
     msq::rank_summary_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
         (int)pl->rows, (int)pl->cols, pl->words, pl->nbands, pl->words * 32, (const uint16_t*)(w + L.zb),
         (const uint32_t*)(w + L.ao), d_summary);

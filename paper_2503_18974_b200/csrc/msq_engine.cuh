@@ -2014,7 +2014,7 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
 // the map c -> (all ones ? c + h_q : b_q); a segment composes its maps
 // (pass 1), then folds the maps of the segments above from base and writes
 // its carries (pass 2) -- 2 reads of the summaries, CARRY_SEG-way parallel.
-constexpr int CARRY_SEG = 16;
+constexpr int CARRY_SEG = 8;
 __global__ void __launch_bounds__(32 * CARRY_SEG) carry_scan_kernel(int rows, int cols, int W, int nbands,
                                                                     int cols_pad, const uint16_t* b_in,
                                                                     const uint32_t* ao_in, const uint32_t* base,
@@ -2212,23 +2212,38 @@ __global__ void __launch_bounds__(256) seed_climb_kernel(const uint8_t* src, lon
 }
 
 // ======================================================= row-band sharding
-__global__ void rank_summary_kernel(int rows, int cols, int W, int nbands, int cols_pad,
-                                    const uint16_t* b_in, const uint32_t* ao_in, uint32_t* out) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= cols) return;
-    long long acc = 0;
-    uint32_t s = 0;
-    bool done = false;
-    for (int q = nbands - 1; q >= 0; --q) {
-        const bool full = (ao_in[(size_t)q * W + (j >> 5)] >> (j & 31)) & 1u;
-        if (!full) {
-            s = (uint32_t)(acc + b_in[(size_t)q * cols_pad + j]);
-            done = true;
-            break;
+// Bottom run of the rank's slice per column (== local rows when all ones): the
+// last band (from the bottom) whose column is not all ones, plus the heights of
+// the all-ones bands below it.  One warp per 32-column word; lanes take 32 bands
+// at a time from the bottom, one ballot per column finds the band.
+__global__ void __launch_bounds__(256) rank_summary_kernel(int rows, int cols, int W, int nbands, int cols_pad,
+                                                           const uint16_t* b_in, const uint32_t* ao_in,
+                                                           uint32_t* out) {
+    const int lane = threadIdx.x & 31;
+    const int word = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (word >= W) return;
+    uint32_t pending = valid_mask(word, W, cols);  // columns still looking for their band
+    uint32_t res = 0u;                             // this lane's column (word*32 + lane)
+    for (int q0 = nbands - 1; q0 >= 0 && pending; q0 -= 32) {
+        const int q = q0 - lane;  // lane's band
+        const uint32_t notall = q >= 0 ? ~ao_in[(size_t)q * W + word] : 0u;
+        uint32_t todo = pending;
+        while (todo) {  // warp-uniform loop over the pending columns
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, (notall >> j) & 1u);
+            if (m) {  // the lowest lane = the bottom-most band with a zero in column j
+                const int qb = q0 - (__ffs(m) - 1);
+                if (lane == j)
+                    res = (uint32_t)(rows - band_row0(rows, nbands, qb + 1)) +
+                          (uint32_t)b_in[(size_t)qb * cols_pad + 32 * word + j];
+                pending &= ~(1u << j);
+            }
         }
-        acc += band_row0(rows, nbands, q + 1) - band_row0(rows, nbands, q);
     }
-    out[j] = done ? s : (uint32_t)acc;
+    if ((pending >> lane) & 1u) res = (uint32_t)rows;  // all ones through the slice
+    const int col = 32 * word + lane;
+    if (col < cols) out[col] = res;
 }
 
 struct RankRows {

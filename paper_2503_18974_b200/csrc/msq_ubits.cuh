@@ -48,7 +48,12 @@ __global__ void __launch_bounds__(640, 1) ubits_kernel(const UStripParams p) {
     constexpr int LR = R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3;
     static_assert((1 << LR) == R, "R must be 1, 2, 4 or 8");
     extern __shared__ __align__(128) uint8_t smem[];
-    const int band = blockIdx.x;
+    // CTA = (band, column chunk): own words [chunk * cw, chunk * cw + cw); the
+    // ring holds words [s0, s1) of each row (the chunk plus the halo on its left)
+    const int band = blockIdx.x / p.nchunks, chunk = blockIdx.x % p.nchunks;
+    const int cbeg = chunk * p.cw, cend = min(p.W, cbeg + p.cw);
+    const int s0 = max(0, cbeg - UB_HALO), s1 = cend;
+    const int span_bytes = (s1 - s0) * 4;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int r0 = band_row0(p.rows, p.nbands, band);
     const int H = band_row0(p.rows, p.nbands, band + 1) - r0;
@@ -62,7 +67,7 @@ __global__ void __launch_bounds__(640, 1) ubits_kernel(const UStripParams p) {
     unsigned char* result = p.results;
 
     asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the seed / strip pass
-    if (p.redo && ld_volatile(p.redo + band) == 0) return;  // done by strip_kernel
+    if (p.redo && ld_volatile(p.redo + band) == 0) return;  // done by strip_kernel (unchunked plans)
     if (tid == 0) {
         const int t0 = p.share ? max(1, ld_volatile(res_best(result))) : 1;
         sh[0] = t0;
@@ -80,20 +85,20 @@ __global__ void __launch_bounds__(640, 1) ubits_kernel(const UStripParams p) {
     if (warp == p.nwarps) {
         if (lane == 0) {
             const uint64_t pol = l2_evict_first_policy();
-            const uint8_t* bsrc = p.src + (size_t)r0 * p.ld;
-            const bool contiguous = p.ld == (long long)p.row_bytes;
+            const uint8_t* bsrc = p.src + (size_t)r0 * p.ld + (size_t)s0 * 4;
+            const bool contiguous = p.ld == (long long)p.row_bytes && span_bytes == p.row_bytes;
             for (int q = 0; q < nslots_band; ++q) {
                 const int s = q % p.nslots;
                 if (q >= p.nslots) mbar_wait(&empty[s], (uint32_t)((q / p.nslots - 1) & 1));
                 const int n = min(R, H - q * R);
-                mbar_expect_tx(&full[s], (uint32_t)(n * p.row_bytes));
+                mbar_expect_tx(&full[s], (uint32_t)(n * span_bytes));
                 uint8_t* dst = ring + (size_t)s * slot_bytes;
                 const uint8_t* srow = bsrc + (size_t)q * R * p.ld;
                 if (contiguous) {
                     tma_row(dst, srow, (uint32_t)(n * p.row_bytes), &full[s], pol);
                 } else {
                     for (int b = 0; b < n; ++b)
-                        tma_row(dst + (size_t)b * p.row_bytes, srow + (size_t)b * p.ld, (uint32_t)p.row_bytes,
+                        tma_row(dst + (size_t)b * p.row_bytes, srow + (size_t)b * p.ld, (uint32_t)span_bytes,
                                 &full[s], pol);
                 }
             }
@@ -102,15 +107,15 @@ __global__ void __launch_bounds__(640, 1) ubits_kernel(const UStripParams p) {
     }
 
     // ------------------------------------------------------------ consumers
-    const int base_word = UB_STRIDE * warp - UB_HALO;
+    const int base_word = cbeg + UB_STRIDE * warp - UB_HALO;
     uint32_t VAL[4], off[4];
     bool own[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int a = base_word + 32 * i + lane;
-        VAL[i] = (a >= 0 && a < p.W) ? valid_mask(a, p.W, p.cols) : 0u;
-        own[i] = (32 * i + lane) >= UB_HALO && a < p.W;
-        off[i] = (uint32_t)(min(max(a, 0), p.W - 1) * 4);
+        VAL[i] = (a >= s0 && a < s1) ? valid_mask(a, p.W, p.cols) : 0u;  // ring span only
+        own[i] = (32 * i + lane) >= UB_HALO && a < cend;
+        off[i] = (uint32_t)((min(max(a, s0), s1 - 1) - s0) * 4);
     }
     uint32_t Z[4][UB_P];
 #pragma unroll
@@ -337,7 +342,7 @@ __global__ void __launch_bounds__(640, 1) ubits_kernel(const UStripParams p) {
 #pragma unroll 1
     for (int wi = UB_HALO; wi < UB_WORDS; ++wi) {
         const int a = base_word + wi;
-        if (a >= p.W) break;  // warp-uniform
+        if (a >= cend) break;  // warp-uniform
         const int src_lane = wi & 31, qi = wi >> 5;
         uint32_t zv = 0u;
 #pragma unroll
@@ -357,7 +362,8 @@ __global__ void __launch_bounds__(640, 1) ubits_kernel(const UStripParams p) {
     asm volatile("bar.sync 1, %0;" ::"r"(p.nwarps * 32) : "memory");  // consumers only
     if (tid == 0) {
         const unsigned long long k = *skey;
-        p.band_keys[band] = k;
+        if (p.nchunks == 1) p.band_keys[band] = k;
+        else if (k) atomicMax(p.band_keys + band, k);  // chunked: zeroed by the launch
         if (k) atomicMax(res_key1(result), k);
     }
 }

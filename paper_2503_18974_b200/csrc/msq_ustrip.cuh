@@ -51,7 +51,8 @@ struct UStripParams {
     long long ld;  // bytes per row
     int rows, cols, W, nbands, cols_pad;
     long long row_base;
-    int nslots, row_bytes, nwarps;
+    int nslots, row_bytes, nwarps;  // row_bytes: ring row stride (the widest chunk + halo)
+    int nchunks, cw;                // column chunks per band, own words per chunk
     int share;     // 0 (deterministic plans): every band from t = 1, no shared best side
     uint16_t* zb;  // [nbands][cols_pad] bottom runs (band output)
     uint16_t* e_out;
@@ -86,7 +87,12 @@ __global__ void __launch_bounds__(640, 1) ustrip_kernel(const UStripParams p) {
     constexpr int LR = R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3;
     static_assert((1 << LR) == R, "R must be 1, 2, 4 or 8");
     extern __shared__ __align__(128) uint8_t smem[];
-    const int band = blockIdx.x;
+    // CTA = (band, column chunk): own words [chunk * cw, chunk * cw + cw); the
+    // ring holds words [s0, s1) of each row (the chunk plus the halo on its left)
+    const int band = blockIdx.x / p.nchunks, chunk = blockIdx.x % p.nchunks;
+    const int cbeg = chunk * p.cw, cend = min(p.W, cbeg + p.cw);
+    const int s0 = max(0, cbeg - USTRIP_HALO), s1 = cend;
+    const int span_bytes = (s1 - s0) * 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int r0 = band_row0(p.rows, p.nbands, band);
     const int H = band_row0(p.rows, p.nbands, band + 1) - r0;
@@ -118,20 +124,20 @@ __global__ void __launch_bounds__(640, 1) ustrip_kernel(const UStripParams p) {
     if (warp == p.nwarps) {
         if (lane == 0) {
             const uint64_t pol = l2_evict_first_policy();
-            const uint8_t* bsrc = p.src + (size_t)r0 * p.ld;
-            const bool contiguous = p.ld == (long long)p.row_bytes;
+            const uint8_t* bsrc = p.src + (size_t)r0 * p.ld + (size_t)s0 * 32;
+            const bool contiguous = p.ld == (long long)p.row_bytes && span_bytes == p.row_bytes;
             for (int q = 0; q < nslots_band; ++q) {
                 const int s = q % p.nslots;
                 if (q >= p.nslots) mbar_wait(&empty[s], (uint32_t)((q / p.nslots - 1) & 1));
                 const int n = min(R, H - q * R);
-                mbar_expect_tx(&full[s], (uint32_t)(n * p.row_bytes));
+                mbar_expect_tx(&full[s], (uint32_t)(n * span_bytes));
                 uint8_t* dst = ring + (size_t)s * slot_bytes;
                 const uint8_t* srow = bsrc + (size_t)q * R * p.ld;
                 if (contiguous) {
                     tma_row(dst, srow, (uint32_t)(n * p.row_bytes), &full[s], pol);
                 } else {
                     for (int b = 0; b < n; ++b)
-                        tma_row(dst + (size_t)b * p.row_bytes, srow + (size_t)b * p.ld, (uint32_t)p.row_bytes,
+                        tma_row(dst + (size_t)b * p.row_bytes, srow + (size_t)b * p.ld, (uint32_t)span_bytes,
                                 &full[s], pol);
                 }
             }
@@ -140,17 +146,18 @@ __global__ void __launch_bounds__(640, 1) ustrip_kernel(const UStripParams p) {
     }
 
     // ------------------------------------------------------------ consumers
-    const int base_word = USTRIP_STRIDE * warp - USTRIP_HALO;
+    const int base_word = cbeg + USTRIP_STRIDE * warp - USTRIP_HALO;
     const int a0 = base_word + lane, a1 = base_word + 32 + lane;  // global words of window words lane, lane+32
-    const uint32_t VAL0 = (a0 >= 0 && a0 < p.W) ? valid_mask(a0, p.W, p.cols) : 0u;
-    const uint32_t VAL1 = (a1 >= 0 && a1 < p.W) ? valid_mask(a1, p.W, p.cols) : 0u;
-    const bool own0 = lane >= USTRIP_HALO && a0 < p.W;
-    const bool own1 = a1 < p.W;
+    // words outside the ring span (left of the halo, right of the chunk) read as invalid
+    const uint32_t VAL0 = (a0 >= s0 && a0 < s1) ? valid_mask(a0, p.W, p.cols) : 0u;
+    const uint32_t VAL1 = (a1 >= s0 && a1 < s1) ? valid_mask(a1, p.W, p.cols) : 0u;
+    const bool own0 = lane >= USTRIP_HALO && a0 < cend;
+    const bool own1 = a1 < cend;
     // smem offsets of the two words' halves; half order swapped on lanes with bit 2
     // set, so 8 consecutive lanes cover all 32 banks
     const uint32_t swap = (lane >> 2) & 1u;
     const uint32_t sel = swap ? 0x1054u : 0x5410u;
-    const int c0 = min(max(a0, 0), p.W - 1), c1 = min(max(a1, 0), p.W - 1);
+    const int c0 = min(max(a0, s0), s1 - 1) - s0, c1 = min(max(a1, s0), s1 - 1) - s0;
     const uint32_t off0 = (uint32_t)(c0 * 32) + 16u * swap, off0b = (uint32_t)(c0 * 32) + 16u * (swap ^ 1u);
     const uint32_t off1 = (uint32_t)(c1 * 32) + 16u * swap, off1b = (uint32_t)(c1 * 32) + 16u * (swap ^ 1u);
 
@@ -369,7 +376,7 @@ __global__ void __launch_bounds__(640, 1) ustrip_kernel(const UStripParams p) {
 #pragma unroll 1
     for (int i = USTRIP_HALO; i < USTRIP_WORDS; ++i) {
         const int a = base_word + i;
-        if (a >= p.W) break;  // warp-uniform
+        if (a >= cend) break;  // warp-uniform
         const int src_lane = i & 31;
         const bool second = i >= 32;
         uint32_t zv = 0u, fv = 0u;
@@ -392,7 +399,8 @@ __global__ void __launch_bounds__(640, 1) ustrip_kernel(const UStripParams p) {
     asm volatile("bar.sync 1, %0;" ::"r"(p.nwarps * 32) : "memory");  // consumers only
     if (tid == 0) {
         const unsigned long long k = *skey;
-        p.band_keys[band] = k;
+        if (p.nchunks == 1) p.band_keys[band] = k;
+        else if (k) atomicMax(p.band_keys + band, k);  // chunked: zeroed by the launch
         if (k) atomicMax(res_key1(result), k);
         if (ld_volatile(&sh[2])) atomicOr(res_status(result), 1u);
     }

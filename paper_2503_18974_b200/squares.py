@@ -116,7 +116,7 @@ class Solver:
 
     def __init__(self, fmt: int, rows: int, cols: int, ld: int | None = None, batch: int = 1,
                  nbands: int = 0, deterministic: bool = False, device=None, engine: int = -1,
-                 flags: int = 0, test_floor: int = 0):
+                 flags: int = 0, test_floor: int = 0, col_chunks: int = 1):
         """``engine``: -1 automatic, 0 band engine, 1 register team engine.
         ``flags`` (N.PLAN_*) and ``test_floor`` are experiment / test switches
         (``test_floor`` presets the shared best side: the caller vouches that
@@ -128,6 +128,7 @@ class Solver:
         self.plan = N.plan(fmt, batch, rows, cols, self.ld, nbands, deterministic, engine)
         self.plan.flags = flags
         self.plan.test_floor = test_floor
+        self.plan.col_chunks = col_chunks
         self.device = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
         self.ws = torch.empty(max(int(self.plan.ws_bytes), 256), dtype=torch.uint8,

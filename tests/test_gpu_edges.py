@@ -161,3 +161,31 @@ def test_fixup_window_search_vs_climb(torch, fmt):
             for det in (False, True):
                 got = Solver(f, rows, cols, nbands=nb, flags=flags, deterministic=det).solve(src)[0]
                 _same(got, want)
+
+
+@pytest.mark.parametrize("fmt", ["u8", "bits"])
+def test_column_chunked_strip_passes(torch, fmt):
+    """Bands split into column chunks (msq_plan.col_chunks): one CTA per band and
+    chunk, each with the halo on its left; same answers as the oracle."""
+    from paper_2503_18974_b200 import _native as Nn
+    from paper_2503_18974_b200.squares import Solver
+    rng = np.random.default_rng(400 if fmt == "u8" else 401)
+    for it in range(16):
+        rows = int(rng.integers(300, 2000))
+        cols = int(rng.choice([4096, 8192, 12288, 16384]))
+        p = float(rng.choice([0.9, 0.97, 0.995, 0.999]))
+        a = (rng.random((rows, cols)) < p).astype(np.uint8)
+        k = int(rng.integers(20, min(rows, 300)))
+        t0, l0 = int(rng.integers(0, rows - k + 1)), int(rng.integers(0, cols - k + 1))
+        a[t0:t0 + k, l0:l0 + k] = 1
+        if it % 3 == 0:  # a square straddling a chunk boundary
+            c = cols // 2 - k // 2
+            a[rows // 3:rows // 3 + k, c:c + k] = 1
+        want = oracle.freq(a)
+        nb = int(rng.integers(2, 12))
+        if fmt == "u8":
+            src, f = torch.from_numpy(a).cuda(), Nn.FMT_U8
+        else:
+            src, f = torch.from_numpy(grid.pack_bits(a).view(np.int32)).cuda(), Nn.FMT_BITS
+        for ch in (2, 3, 5):
+            _same(Solver(f, rows, cols, nbands=nb, col_chunks=ch).solve(src)[0], want)

@@ -1,0 +1,77 @@
+"""One-GPU emulation of the N-rank row-band split of cfg4 (no kernel waits on another).
+
+For N in 1/2/4/8, the 65536^2 matrix is cut into N row slices; each slice is
+solved by the rank API exactly as rank r of an N-GPU job would (msq_rank_seed
+-> [all-reduce of the best side: here the max of the ranks' seeds, written
+back] -> msq_rank_band_pass -> msq_rank_summary -> [all-gather] ->
+msq_compose_carry -> msq_rank_fixup -> msq_rank_key_status), one rank after
+another, each phase timed with CUDA events.  Per-rank time = what one GPU of
+the N-GPU job spends on device work; the collectives (8 B all-reduce, cols*4 B
+all-gather, 16 B all-reduce) are not included.  Prints one JSON line per N.
+"""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2503_18974_b200 import _native as N, build, configs
+from paper_2503_18974_b200.distributed import GpuBackend, decode_key, slice_rows
+
+build.build()
+cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
+spec = configs.CONFIGS[cfg]
+full = configs.cfg4_device() if cfg == "cfg4" else configs.cfg5_device()
+fmt = N.FMT_BITS if cfg == "cfg4" else N.FMT_U8
+rows, cols = spec["rows"], spec["cols"]
+REPS = 10
+for world in (1, 2, 4, 8):
+    rank_rows = [slice_rows(rows, world, q)[1] for q in range(world)]
+    bes, srcs = [], []
+    for q in range(world):
+        r0, n = slice_rows(rows, world, q)
+        srcs.append(full[r0:r0 + n].contiguous())
+        bes.append(GpuBackend(fmt, n, cols, r0))
+    gathered = torch.empty((world, cols), dtype=torch.int32, device="cuda")
+    phases = {q: {"seed": 0.0, "band_pass": 0.0, "summary": 0.0, "compose+carry+fixup": 0.0} for q in range(world)}
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    for it in range(REPS + 2):
+        marks = {}
+        for q, be in enumerate(bes):
+            a = ev(); be.seed(srcs[q]); b = ev()
+            marks[q] = [a, b]
+        best = torch.stack([be.best_side() for be in bes]).max()
+        for be in bes:
+            be.best_side().copy_(best.reshape(1))
+        for q, be in enumerate(bes):
+            a = ev(); be.band_pass(srcs[q]); b = ev(); s = be.rank_summary(); c = ev()
+            gathered[q].copy_(s)
+            marks[q] += [a, b, c]
+        keys = []
+        for q, be in enumerate(bes):
+            a = ev()
+            base = be.compose(gathered, rank_rows, q) if q > 0 else None
+            be.fixup(base)
+            keys.append(be.key_status())
+            b = ev()
+            marks[q] += [a, b]
+        torch.cuda.synchronize()
+        if it >= 2:
+            for q in range(world):
+                m = marks[q]
+                phases[q]["seed"] += m[0].elapsed_time(m[1]) / REPS
+                phases[q]["band_pass"] += m[2].elapsed_time(m[3]) / REPS
+                phases[q]["summary"] += m[3].elapsed_time(m[4]) / REPS
+                phases[q]["compose+carry+fixup"] += m[5].elapsed_time(m[6]) / REPS
+    ks = torch.stack(keys).max(dim=0).values.cpu().numpy()
+    r = decode_key(int(ks[0]), int(ks[1]), rows, cols)
+    per_rank = [sum(phases[q].values()) for q in range(world)]
+    slowest = max(per_rank)
+    print(json.dumps({"config": cfg, "world": world, "rows_per_rank": rank_rows[0],
+                      "per_rank_ms": [round(x, 4) for x in per_rank],
+                      "phases_ms_rank0": {k: round(v, 4) for k, v in phases[0].items()},
+                      "phases_ms_last": {k: round(v, 4) for k, v in phases[world - 1].items()},
+                      "projected_gcells_s": round(rows * cols / (slowest * 1e-3) / 1e9, 1),
+                      "answer": [r.side, r.top, r.left]}), flush=True)
