@@ -248,6 +248,11 @@ int32_t msq_last_launch_count(void);
  * cycle counters to d_counters[unit*16..] (NULL disables; tools only). */
 void msq_debug_set_profile(void* d_counters);
 
+/* Instrumentation: the pageable-buffer staging of the host-buffer calls
+ * (worker threads, pinned buffers per worker, bytes per buffer; workers <= 0 =
+ * half the hardware threads).  Tools only; the defaults are the measured best. */
+void msq_debug_set_staging(int32_t workers, int32_t buffers, int64_t chunk_bytes);
+
 const char* msq_strerror(int code);
 /* Name and text of the last CUDA error seen by this thread ("" if none). */
 const char* msq_last_cuda_error(void);
