@@ -2160,7 +2160,7 @@ __global__ void __launch_bounds__(256) seed_climb_kernel(const uint8_t* src, lon
     for (int i0 = 0; i0 < nr; i0 += SB) {
         // a strip whose squares grow slower than one side per 4 rows holds no
         // large square; stop early (the bound only has to be a real square)
-        if (i0 >= 64 && 4 * best < i0) break;
+        if (i0 >= 32 && 4 * best < i0) break;
         uint32_t rw[SB];
 #pragma unroll
         for (int q = 0; q < SB; ++q) {
