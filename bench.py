@@ -529,9 +529,9 @@ def main():
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
                 "kernel": ("msq::team_kernel" if use_solver and int(solver.plan.engine) == 1 else
-                           "band pass: msq::strip_kernel (+ pass1_kernel for bands it hands back), "
+                           "band pass: msq::strip_kernel (+ ubits_kernel for the bands it hands back), "
                            "timed with the seed_climb_kernel before it" if fmt == N.FMT_BITS else
-                           "msq::pass1_kernel (timed with the seed_climb_kernel before it)"),
+                           "band pass: msq::ustrip_kernel, timed with the seed_climb_kernel before it"),
                 "kernel_ms": round(p1_ms, 5),
                 "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": int(alg_bytes)}
