@@ -252,6 +252,8 @@ void msq_debug_set_profile(void* d_counters);
  * (worker threads, pinned buffers per worker, bytes per buffer; workers <= 0 =
  * half the hardware threads).  Tools only; the defaults are the measured best. */
 void msq_debug_set_staging(int32_t workers, int32_t buffers, int64_t chunk_bytes);
+/* Instrumentation: band height of the team engine's row-band mode (plans made after the call). */
+void msq_debug_set_team_band_rows(int32_t rows);
 
 const char* msq_strerror(int code);
 /* Name and text of the last CUDA error seen by this thread ("" if none). */

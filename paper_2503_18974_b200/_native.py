@@ -101,6 +101,7 @@ def load():
         "msq_last_launch_count": ([], I32),
         "msq_debug_set_profile": ([P], None),
         "msq_debug_set_staging": ([I32, I32, I64], None),
+        "msq_debug_set_team_band_rows": ([I32], None),
         "msq_strerror": ([ctypes.c_int], ctypes.c_char_p),
         "msq_last_cuda_error": ([], ctypes.c_char_p),
         "msq_version": ([], ctypes.c_char_p),

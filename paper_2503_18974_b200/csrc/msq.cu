@@ -678,6 +678,7 @@ constexpr int kTeamThreads = 32;  // one warp per CTA: fine-grained spread over 
 
 int team_planes(long long rows) { return rows <= 504 ? 9 : 11; }  // rows <= 2^PB - 8
 constexpr int kTeamMaxRows = 2040;  // one team walks <= 2^11 - 8 rows (11 last-zero planes)
+int g_team_band_rows = 16;           // band height of the team engine's row-band mode (instrumentation)
 
 // engine: -1 automatic, 0 band engine, 1 team engine (where it applies)
 bool team_applies(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int32_t nbands, int32_t engine) {
@@ -765,6 +766,13 @@ extern "C" int msq_plan_make_ex(int32_t fmt, int32_t batch, int64_t rows, int64_
                           (fmt == MSQ_FMT_U8 ? ld >= cols : ld >= (cols + 31) / 32);
     if (engine == 1 && !(shape_ok && team_applies(fmt, batch, rows, cols, nbands, engine))) return MSQ_EINVAL;
     if (shape_ok && team_applies(fmt, batch, rows, cols, nbands, engine)) {
+        // one matrix on row bands: short bands (a team walks its rows one by one,
+        // so the band height is the latency), the carry scan and fix-up behind
+        if (rc == MSQ_OK && batch == 1 && nbands <= 0 && rows >= 2 * g_team_band_rows) {
+            msq_plan q{};
+            const int nbt = (int)std::min<long long>(num_sms(), rows / g_team_band_rows);
+            if (nbt > p.nbands && plan_band(fmt, batch, rows, cols, ld, nbt, deterministic, &q) == MSQ_OK) p = q;
+        }
         if (rc != MSQ_OK) {  // the band plan does not fit: the team engine needs no workspace
             p = msq_plan{};
             p.fmt = fmt;
@@ -1541,3 +1549,5 @@ extern "C" void msq_debug_set_staging(int32_t workers, int32_t buffers, int64_t 
     g_stage.bufs = buffers > 0 ? buffers : 4;
     g_stage.chunk = chunk_bytes > 0 ? (size_t)chunk_bytes : (4u << 20);
 }
+
+extern "C" void msq_debug_set_team_band_rows(int32_t rows) { g_team_band_rows = rows > 0 ? rows : 16; }
