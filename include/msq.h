@@ -37,6 +37,9 @@ extern "C" {
 #define MSQ_EVALUE 2   /* a u8 cell outside {0,1} -> Python ValueError       */
 #define MSQ_ECUDA 3    /* CUDA runtime error -> Python RuntimeError          */
 #define MSQ_ENOMEM 4   /* workspace allocation failed                        */
+#define MSQ_EAGAIN 5   /* msq_decode of a sieve-engine launch that could not decide
+                          (status bit 1): launch again with plan.engine = 0; the
+                          msq_solve_* calls do that themselves                  */
 
 /* input formats */
 #define MSQ_FMT_U8 0
@@ -54,7 +57,8 @@ typedef struct {
 typedef struct {
     uint64_t key_pass1;  /* best key from band passes                     */
     uint64_t key_fix;    /* best key from band-boundary fix-ups            */
-    uint32_t status;     /* bit 0: invalid u8 cell                         */
+    uint32_t status;     /* bit 0: invalid u8 cell; bit 1: the sieve engine
+                            could not decide (run the band engine)         */
     int32_t best_side;   /* running best side shared between bands         */
     uint64_t reserved;
 } msq_devresult;
@@ -83,7 +87,12 @@ typedef struct {
     int32_t grid;         /* pass-1 CTAs                                    */
     int32_t fix_threads;  /* fix-up CTA size                                */
     int32_t fix_wpt;      /* fix-up words per thread                        */
-    int32_t engine;       /* 0: band engine; 1: register team engine (small matrices) */
+    int32_t engine;       /* 0: band engine; 1: register team engine (small matrices);
+                             2: sieve engine (large bit-packed matrices, msq_sieve.cuh):
+                             one streaming pass over 8x8-cell blocks + exact windows of
+                             the few candidates; exact for answers 56..222, otherwise the
+                             result block says so (status bit 1) and the same plan with
+                             engine = 0 runs the band engine */
     int32_t flags;        /* MSQ_PLAN_* experiment switches; 0 from msq_plan_make */
     int32_t test_floor;   /* TEST ONLY: > 0 presets the shared best side (the caller
                              vouches that the answer is >= it); 0 from msq_plan_make */
@@ -92,6 +101,8 @@ typedef struct {
                              msq_plan_make): fewer, taller bands with the same CTA count,
                              so the band summaries (carry scan, fix-up) shrink -- the
                              tile strip pass then stands aside */
+    int32_t sv_bands;     /* sieve engine: row bands of the streaming pass */
+    int64_t sv_ws_off;    /* sieve engine: its part of the workspace starts here */
 } msq_plan;
 
 /* msq_plan.flags: experiment switches a caller may set on its own plan
@@ -111,7 +122,9 @@ typedef struct {
 int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld,
                   int32_t nbands, int32_t deterministic, msq_plan* plan);
 /* Same with an engine choice: -1 = automatic (msq_plan_make), 0 = band
- * engine, 1 = register team engine (cols <= 1024; MSQ_EINVAL otherwise). */
+ * engine, 1 = register team engine (cols <= 1024; MSQ_EINVAL otherwise),
+ * 2 = sieve engine (bit-packed, one matrix, rows and cols >= 64, cols a
+ * multiple-of-128 word count, 16-byte row stride; automatic from 4096 x 4096). */
 int msq_plan_make_ex(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld,
                      int32_t nbands, int32_t deterministic, int32_t engine, msq_plan* plan);
 
@@ -226,8 +239,24 @@ int msq_compose_carry(const uint32_t* d_summaries, const int64_t* h_rank_rows, i
                       int32_t rank, int64_t cols, uint32_t* d_base_carry, void* stream);
 int msq_rank_fixup(const msq_plan* plan, void* d_ws, const uint32_t* d_base_carry,
                    msq_devresult* d_result, void* stream);
-/* d_out[0] = max(key_pass1, key_fix), d_out[1] = status & 1: the two int64
- * the ranks all-reduce(max) in step 6 (one tiny kernel on `stream`). */
+/* Sieve engine across ranks (plan->engine == 2): a rank passes its local rows
+ * and, when it is not the first, the last halo_rows (a multiple of 8, <= 256;
+ * 256 unless the rank above is shorter) rows of the rank above (d_halo,
+ * halo_ld words per row).  Every square the sieve can report (side <= 222)
+ * then lies inside the rows of the rank that holds its bottom row, so the only
+ * exchange is that halo before the solve and the all-reduce(max) of the key
+ * after it.  msq_rank_sieve = msq_rank_sieve_pass (the streaming kernel) +
+ * msq_rank_sieve_finish (band-top block rows, exact candidate windows).
+ * Status bit 1 on any rank: all ranks run steps 1-6 above instead. */
+int msq_rank_sieve(const msq_plan* plan, const void* d_src, const void* d_halo, int64_t halo_rows,
+                   int64_t halo_ld, void* d_ws, msq_devresult* d_result, void* stream);
+int msq_rank_sieve_pass(const msq_plan* plan, const void* d_src, const void* d_halo, int64_t halo_rows,
+                        int64_t halo_ld, void* d_ws, msq_devresult* d_result, void* stream);
+int msq_rank_sieve_finish(const msq_plan* plan, const void* d_src, const void* d_halo, int64_t halo_rows,
+                          int64_t halo_ld, void* d_ws, msq_devresult* d_result, void* stream);
+/* d_out[0] = max(key_pass1, key_fix), d_out[1] = 3 for an invalid cell, 2 when
+ * the sieve could not decide, else 0: the two int64 the ranks all-reduce(max)
+ * (one tiny kernel on `stream`). */
 int msq_rank_key_status(const msq_devresult* d_result, int64_t* d_out, void* stream);
 
 /* Intermediate outputs (tests): per band leading-ones depth e, bottom run b
@@ -252,6 +281,8 @@ void msq_debug_set_profile(void* d_counters);
  * (worker threads, pinned buffers per worker, bytes per buffer; workers <= 0 =
  * half the hardware threads).  Tools only; the defaults are the measured best. */
 void msq_debug_set_staging(int32_t workers, int32_t buffers, int64_t chunk_bytes);
+/* Instrumentation: consumer warps per CTA of the sieve engine's streaming pass (plans made after the call). */
+void msq_debug_set_sieve_wpc(int32_t warps);
 /* Instrumentation: band height of the team engine's row-band mode (plans made after the call). */
 void msq_debug_set_team_band_rows(int32_t rows);
 

@@ -14,7 +14,8 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "_lib", "libmsq.so")
 HEADER = os.path.join(os.path.dirname(_PKG), "include", "msq.h")
 
-MSQ_OK, MSQ_EINVAL, MSQ_EVALUE, MSQ_ECUDA, MSQ_ENOMEM = 0, 1, 2, 3, 4
+MSQ_OK, MSQ_EINVAL, MSQ_EVALUE, MSQ_ECUDA, MSQ_ENOMEM, MSQ_EAGAIN = 0, 1, 2, 3, 4, 5
+ENGINE_BAND, ENGINE_TEAM, ENGINE_SIEVE = 0, 1, 2
 FMT_U8, FMT_BITS = 0, 1
 PLAN_NO_STRIP, PLAN_NO_SEED, PLAN_SINGLE_TEAM, PLAN_CLIMB_FIXUP, PLAN_PASS1 = 1, 2, 4, 8, 16
 
@@ -44,7 +45,8 @@ class MsqPlan(ctypes.Structure):
                 ("tl", ctypes.c_int32), ("grid", ctypes.c_int32), ("fix_threads", ctypes.c_int32),
                 ("fix_wpt", ctypes.c_int32), ("engine", ctypes.c_int32),
                 ("flags", ctypes.c_int32), ("test_floor", ctypes.c_int32),
-                ("col_chunks", ctypes.c_int32)]
+                ("col_chunks", ctypes.c_int32), ("sv_bands", ctypes.c_int32),
+                ("sv_ws_off", ctypes.c_int64)]
 
 
 _lib = None
@@ -96,6 +98,10 @@ def load():
         "msq_compose_carry": ([P, P, I32, I32, I64, P, P], ctypes.c_int),
         "msq_rank_fixup": ([PP, P, P, P, P], ctypes.c_int),
         "msq_rank_key_status": ([P, P, P], ctypes.c_int),
+        "msq_rank_sieve": ([PP, P, P, I64, I64, P, P, P], ctypes.c_int),
+        "msq_rank_sieve_pass": ([PP, P, P, I64, I64, P, P, P], ctypes.c_int),
+        "msq_rank_sieve_finish": ([PP, P, P, I64, I64, P, P, P], ctypes.c_int),
+        "msq_debug_set_sieve_wpc": ([I32], None),
         "msq_ws_views": ([PP, P, P, P, P, P], ctypes.c_int),
         "msq_gen_hash": ([I32, U64, U64, I64, I64, I64, I64, P, P], ctypes.c_int),
         "msq_last_launch_count": ([], I32),

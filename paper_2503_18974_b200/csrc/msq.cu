@@ -25,6 +25,7 @@
 #include "msq_cube.cuh"
 #include "msq_hist.cuh"
 #include "msq_rowdp.cuh"
+#include "msq_sieve.cuh"
 
 namespace {
 
@@ -552,6 +553,128 @@ cudaError_t launch_seed(const msq_plan* pl, const void* d_src, msq_devresult* d_
     return cudaGetLastError();
 }
 
+
+bool key_range_ok(const msq_plan* pl);
+
+// ---- sieve engine (msq_sieve.cuh): bit-packed single matrices, sparse zeros
+struct SieveGeom {
+    int CR, CC, CWn, WC, nbands, nchunks, wmax, nslots, slot_row_bytes, smem;
+    size_t ctl, cand, gtop, pbot, total;  // workspace offsets (after the band engine's layout)
+};
+int g_sieve_wpc = 3;  // consumer warps per CTA the plan aims for (instrumentation)
+
+bool sieve_shape_ok(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld) {
+    const int64_t words = ceil_div(cols, 32);
+    return fmt == MSQ_FMT_BITS && batch == 1 && rows >= 64 && cols >= 64 && rows < (1ll << 21) - 1 - msq::SV_HALO_ROWS &&
+           cols <= 65536 && words % 4 == 0 && ld >= words && (ld * 4) % 16 == 0;
+}
+
+// geometry for `rows` rows (halo rows included); nbands_fixed > 0 keeps the plan's band count
+SieveGeom sieve_geom(int64_t rows, int64_t cols, int nbands_fixed) {
+    SieveGeom g{};
+    const int W = (int)ceil_div(cols, 32);
+    g.CR = (int)(rows / 8);
+    g.CC = (int)(cols / 8);
+    g.CWn = (int)ceil_div(g.CC, 32);
+    g.WC = (int)ceil_div(g.CWn, 31);
+    g.nchunks = (int)ceil_div(g.WC, std::max(1, g_sieve_wpc));
+    g.wmax = (int)ceil_div(g.WC, g.nchunks);
+    g.nbands = nbands_fixed > 0 ? nbands_fixed
+                                : (int)std::max<long long>(1, std::min<long long>(num_sms() / g.nchunks, g.CR / 32));
+    int rb = 0;
+    for (int c = 0; c < g.nchunks; ++c) {
+        const int wc0 = g.WC * c / g.nchunks, wc1 = g.WC * (c + 1) / g.nchunks;
+        const int mw0 = std::max(0, 8 * (31 * wc0 - 1)), mw1 = std::min(W, 8 * 31 * wc1);
+        rb = std::max(rb, (mw1 - mw0) * 4);
+    }
+    g.slot_row_bytes = rb;
+    const int fixed = 2 * msq::SV_MAXSLOTS * 8 + 64;
+    g.nslots = (int)std::min<long long>(msq::SV_MAXSLOTS, (kSmemMax - 256 - fixed) / ((long long)msq::SV_TR * rb));
+    g.smem = g.nslots * msq::SV_TR * rb + fixed;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += (size_t)round_up((long long)bytes, 256);
+        return o;
+    };
+    g.ctl = take(sizeof(msq::SieveCtl));
+    g.cand = take((size_t)msq::SV_CAP * 8);
+    g.gtop = take((size_t)g.nbands * msq::SV_EDGE * g.CWn * 4);
+    g.pbot = take((size_t)g.nbands * msq::SV_PL * g.CWn * 4);
+    g.total = off;
+    return g;
+}
+
+msq::SieveParams make_sieve(const msq_plan* pl, const void* d_src, const void* d_halo, int64_t halo_rows,
+                            int64_t halo_ld, void* d_ws, msq_devresult* res) {
+    const SieveGeom g = sieve_geom(pl->rows + halo_rows, pl->cols, pl->sv_bands);
+    uint8_t* w = (uint8_t*)d_ws + pl->sv_ws_off;
+    msq::SieveParams p{};
+    p.src = (const uint8_t*)d_src;
+    p.halo = (const uint8_t*)d_halo;
+    p.ld_bytes = pl->ld * 4;
+    p.halo_ld_bytes = halo_ld * 4;
+    p.halo_rows = (int)halo_rows;
+    p.rows = (int)(pl->rows + halo_rows);
+    p.cols = (int)pl->cols;
+    p.W = pl->words;
+    p.row_base = pl->row_base - halo_rows;
+    p.CR = g.CR;
+    p.CC = g.CC;
+    p.CWn = g.CWn;
+    p.WC = g.WC;
+    p.nbands = g.nbands;
+    p.nchunks = g.nchunks;
+    p.wmax = g.wmax;
+    p.nslots = g.nslots;
+    p.slot_row_bytes = g.slot_row_bytes;
+    p.ctl = (msq::SieveCtl*)(w + g.ctl);
+    p.cand = (unsigned long long*)(w + g.cand);
+    p.gtop = (uint32_t*)(w + g.gtop);
+    p.pbot = (uint32_t*)(w + g.pbot);
+    p.result = (unsigned char*)res;
+    return p;
+}
+
+bool sieve_args_ok(const msq_plan* pl, const void* d_src, const void* d_halo, int64_t halo_rows, int64_t halo_ld,
+                   const void* d_ws, const msq_devresult* d_result) {
+    if (!pl || pl->engine != 2 || !d_src || !d_ws || !d_result || ((uintptr_t)d_src % 16) != 0) return false;
+    if (halo_rows < 0 || halo_rows % 8 != 0 || halo_rows > msq::SV_HALO_ROWS) return false;
+    if (halo_rows > 0 && (!d_halo || ((uintptr_t)d_halo % 16) != 0 || halo_ld < pl->words || (halo_ld * 4) % 16 != 0))
+        return false;
+    return pl->row_base - halo_rows >= 0 && key_range_ok(pl);
+}
+
+// memsets + the streaming pass
+cudaError_t launch_sieve_pass(const msq_plan* pl, const msq::SieveParams& sp, cudaStream_t st) {
+    const SieveGeom g = sieve_geom(sp.rows, sp.cols, pl->sv_bands);
+    if (cudaMemsetAsync(sp.result, 0, sizeof(msq_devresult), st) != cudaSuccess) return cudaGetLastError();
+    if (cudaMemsetAsync(sp.ctl, 0, sizeof(msq::SieveCtl), st) != cudaSuccess) return cudaGetLastError();
+    static bool attr_set[64] = {false};
+    cudaError_t e = set_smem_attr(msq::sieve_pass_kernel, attr_set);
+    if (e != cudaSuccess) return e;
+    msq::sieve_pass_kernel<<<g.nbands * g.nchunks, (g.wmax + 1) * 32, (size_t)g.smem, st>>>(sp);
+    return cudaGetLastError();
+}
+
+// band-top block rows with carried-in heights, then the exact windows
+cudaError_t launch_sieve_finish(const msq::SieveParams& sp, cudaStream_t st) {
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)ceil_div((long long)sp.nbands * sp.WC, msq::SV_EWARPS));
+    cfg.blockDim = dim3(32 * msq::SV_EWARPS);
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, msq::sieve_edge_kernel, sp);
+    if (e != cudaSuccess) return e;
+    cfg.gridDim = dim3((unsigned)(num_sms() * 2));
+    cfg.blockDim = dim3(32 * msq::SV_VWARPS);
+    return cudaLaunchKernelEx(&cfg, msq::sieve_verify_kernel, sp);
+}
+
 // --------------------------------------------------- internal workspace
 struct DevCache {
     std::mutex mu;
@@ -635,6 +758,14 @@ int solve_locked(DevCache& C, int32_t fmt, int64_t batch, const void* d_src, int
                         st) != cudaSuccess)
         return MSQ_ECUDA;
     if (cudaStreamSynchronize(st) != cudaSuccess) return MSQ_ECUDA;
+    if (pl.engine == 2 && (C.hres[0].status & 2u)) {  // the sieve could not decide: band engine
+        pl.engine = 0;
+        rc = msq_launch(&pl, d_src, C.ws, C.res, stream);
+        if (rc) return rc;
+        if (cudaMemcpyAsync(C.hres, C.res, sizeof(msq_devresult), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+            return MSQ_ECUDA;
+        if (cudaStreamSynchronize(st) != cudaSuccess) return MSQ_ECUDA;
+    }
     int worst = MSQ_OK;
     for (int64_t k = 0; k < batch; ++k) {
         int r = msq_decode(&C.hres[k], rows, cols, &out[k]);
@@ -759,11 +890,29 @@ extern "C" int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t c
 
 extern "C" int msq_plan_make_ex(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld, int32_t nbands,
                                 int32_t deterministic, int32_t engine, msq_plan* plan) {
-    if (!plan || engine < -1 || engine > 1) return MSQ_EINVAL;
+    if (!plan || engine < -1 || engine > 2) return MSQ_EINVAL;
     msq_plan p{};
     int rc = plan_band(fmt, batch, rows, cols, ld, nbands, deterministic, &p);
     const bool shape_ok = (fmt == MSQ_FMT_U8 || fmt == MSQ_FMT_BITS) && batch >= 1 && rows >= 1 && cols >= 1 &&
                           (fmt == MSQ_FMT_U8 ? ld >= cols : ld >= (cols + 31) / 32);
+    // sieve engine: large bit-packed single matrices try it first (the band fields
+    // stay valid: they are the fall-back when the sieve cannot decide)
+    const bool sieve_auto = engine == -1 && nbands <= 0 && !deterministic && rows >= 4096 && cols >= 4096;
+    if (engine == 2 || sieve_auto) {
+        const bool ok = rc == MSQ_OK && shape_ok && sieve_shape_ok(fmt, batch, rows, cols, ld);
+        if (ok) {
+            const SieveGeom g = sieve_geom(rows, cols, 0);
+            if (g.nslots >= 2 && g.wmax <= 9) {
+                p.engine = 2;
+                p.sv_bands = g.nbands;
+                p.sv_ws_off = round_up(p.ws_bytes, 256);
+                p.ws_bytes = p.sv_ws_off + (int64_t)g.total;
+                *plan = p;
+                return MSQ_OK;
+            }
+        }
+        if (engine == 2) return MSQ_EINVAL;
+    }
     if (engine == 1 && !(shape_ok && team_applies(fmt, batch, rows, cols, nbands, engine))) return MSQ_EINVAL;
     if (shape_ok && team_applies(fmt, batch, rows, cols, nbands, engine)) {
         // one matrix on row bands: short bands (a team walks its rows one by one,
@@ -945,6 +1094,14 @@ int msq_launch(const msq_plan* pl, const void* d_src, void* d_ws, msq_devresult*
         return MSQ_OK;
     }
     if (!pl || !d_src || !d_result || (!d_ws && pl->ws_bytes > 0)) return MSQ_EINVAL;
+    if (pl->engine == 2) {
+        if (((uintptr_t)d_src % 16) != 0) {  // the sieve's bulk copies need an aligned base
+            msq_plan q = *pl;
+            q.engine = 0;
+            return msq_launch(&q, d_src, d_ws, d_result, stream);
+        }
+        return msq_rank_sieve(pl, d_src, nullptr, 0, 0, d_ws, d_result, stream);
+    }
     if (pl->nstage > 0 && ((uintptr_t)d_src % 16) != 0) {
         msq_plan q = *pl;  // misaligned base: fall back to direct loads
         q.nstage = 0;
@@ -986,7 +1143,8 @@ int msq_decode(const msq_devresult* r, int64_t rows, int64_t cols, msq_result* o
         const int64_t right = (int64_t)(msq::KEY_DIM_MASK - (key & msq::KEY_DIM_MASK));
         *out = msq_result{side, side * side, rows * cols, bottom - side + 1, right - side + 1};
     }
-    return (r->status & 1u) ? MSQ_EVALUE : MSQ_OK;
+    if (r->status & 1u) return MSQ_EVALUE;
+    return (r->status & 2u) ? MSQ_EAGAIN : MSQ_OK;
 }
 
 int msq_solve_u8(const uint8_t* d_cells, int64_t rows, int64_t cols, int64_t ld, msq_result* out,
@@ -1337,6 +1495,31 @@ int msq_rank_band_pass(const msq_plan* pl, const void* d_src, void* d_ws, msq_de
     return cuda_status(e);
 }
 
+int msq_rank_sieve_pass(const msq_plan* pl, const void* d_src, const void* d_halo, int64_t halo_rows,
+                        int64_t halo_ld, void* d_ws, msq_devresult* d_result, void* stream) {
+    if (!sieve_args_ok(pl, d_src, d_halo, halo_rows, halo_ld, d_ws, d_result)) return MSQ_EINVAL;
+    const msq::SieveParams sp = make_sieve(pl, d_src, d_halo, halo_rows, halo_ld, d_ws, d_result);
+    g_last_launches = 1;
+    return cuda_status(launch_sieve_pass(pl, sp, (cudaStream_t)stream));
+}
+
+int msq_rank_sieve_finish(const msq_plan* pl, const void* d_src, const void* d_halo, int64_t halo_rows,
+                          int64_t halo_ld, void* d_ws, msq_devresult* d_result, void* stream) {
+    if (!sieve_args_ok(pl, d_src, d_halo, halo_rows, halo_ld, d_ws, d_result)) return MSQ_EINVAL;
+    const msq::SieveParams sp = make_sieve(pl, d_src, d_halo, halo_rows, halo_ld, d_ws, d_result);
+    g_last_launches = 2;
+    return cuda_status(launch_sieve_finish(sp, (cudaStream_t)stream));
+}
+
+int msq_rank_sieve(const msq_plan* pl, const void* d_src, const void* d_halo, int64_t halo_rows, int64_t halo_ld,
+                   void* d_ws, msq_devresult* d_result, void* stream) {
+    int rc = msq_rank_sieve_pass(pl, d_src, d_halo, halo_rows, halo_ld, d_ws, d_result, stream);
+    if (rc) return rc;
+    rc = msq_rank_sieve_finish(pl, d_src, d_halo, halo_rows, halo_ld, d_ws, d_result, stream);
+    g_last_launches = 3;
+    return rc;
+}
+
 int msq_rank_key_status(const msq_devresult* d_result, int64_t* d_out, void* stream) {
     if (!d_result || !d_out) return MSQ_EINVAL;
     msq::key_status_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((const unsigned char*)d_result, (long long*)d_out);
@@ -1417,6 +1600,7 @@ const char* msq_strerror(int code) {
         case MSQ_EINVAL: return "invalid argument (shape, stride or unsupported width)";
         case MSQ_EVALUE: return "cells must contain only 0 or 1";
         case MSQ_ECUDA: return "CUDA runtime error";
+        case MSQ_EAGAIN: return "the sieve engine could not decide; solve with the band engine (plan.engine = 0)";
         case MSQ_ENOMEM: return "device memory allocation failed";
         default: return "unknown error";
     }
@@ -1550,4 +1734,5 @@ extern "C" void msq_debug_set_staging(int32_t workers, int32_t buffers, int64_t 
     g_stage.chunk = chunk_bytes > 0 ? (size_t)chunk_bytes : (4u << 20);
 }
 
+extern "C" void msq_debug_set_sieve_wpc(int32_t warps) { g_sieve_wpc = warps >= 1 && warps <= 9 ? warps : 3; }
 extern "C" void msq_debug_set_team_band_rows(int32_t rows) { g_team_band_rows = rows > 0 ? rows : 16; }

@@ -29,6 +29,7 @@ from .squares import SquareResult
 
 KEY_DIM_BITS = 21
 KEY_DIM_MASK = (1 << KEY_DIM_BITS) - 1
+SIEVE_HALO = 256  # rows a rank borrows from the rank above (msq_sieve.cuh SV_HALO_ROWS)
 
 
 def slice_rows(rows: int, world: int, rank: int) -> tuple[int, int]:
@@ -118,6 +119,33 @@ class GpuBackend:
         nb = int(self.plan.nbands) - (0 if base is not None else 1)
         self.launches += 2 if nb > 0 else 0  # carry scan + fix-up
 
+    # ---- sieve engine (plan.engine == 2): no band summaries, a halo of rows instead
+    @property
+    def is_sieve(self) -> bool:
+        return int(self.plan.engine) == N.ENGINE_SIEVE
+
+    def new_halo_buffer(self, rows: int, like):
+        return self.torch.empty((rows,) + tuple(like.shape[1:]), dtype=like.dtype, device=like.device)
+
+    def _sieve_call(self, fn, src, halo):
+        hp = ctypes.c_void_p(halo.data_ptr()) if halo is not None else None
+        hr = int(halo.shape[0]) if halo is not None else 0
+        hl = int(halo.stride(0)) if halo is not None else 0
+        N.check(fn(ctypes.byref(self.plan), ctypes.c_void_p(src.data_ptr()), hp, hr, hl,
+                   ctypes.c_void_p(self.ws.data_ptr()), ctypes.c_void_p(self.res.data_ptr()),
+                   self._stream()))
+        self.launches += int(self.lib.msq_last_launch_count())
+
+    def sieve(self, src, halo=None):
+        """Streaming pass + band-top rows + exact candidate windows over (halo, src)."""
+        self._sieve_call(self.lib.msq_rank_sieve, src, halo)
+
+    def sieve_pass(self, src, halo=None):
+        self._sieve_call(self.lib.msq_rank_sieve_pass, src, halo)
+
+    def sieve_finish(self, src, halo=None):
+        self._sieve_call(self.lib.msq_rank_sieve_finish, src, halo)
+
     def key_status(self):
         """int64 tensor [key, status] for the all-reduce (keys < 2^63), written
         by one library kernel (msq_rank_key_status) into a persistent buffer."""
@@ -139,7 +167,13 @@ def _all_gather(out, t, group=None):
 
 
 class RowBandSolver:
-    """Solve one (rows x cols) matrix sharded by rows over a process group."""
+    """Solve one (rows x cols) matrix sharded by rows over a process group.
+
+    Backends whose plan is a sieve plan (``is_sieve``) try the sieve first: each
+    rank borrows the last SIEVE_HALO rows of the rank above (one send/recv, no
+    dependence on any kernel) and solves (halo, local rows) alone; the ranks
+    all-reduce(max) their [key, status].  When any rank's sieve could not
+    decide, all ranks run the band protocol below, now and for later solves."""
 
     def __init__(self, rows: int, cols: int, rank: int, world: int, backend, group=None):
         self.rows, self.cols, self.rank, self.world = rows, cols, rank, world
@@ -149,10 +183,40 @@ class RowBandSolver:
         self.group = group
         self.gathered = backend.new_gather_buffer(world) if world > 1 else None
         self._ks = None
+        self._src = None
+        self._halo = None
+        self.sieve = bool(getattr(backend, "is_sieve", False)) and min(self.rank_rows) >= SIEVE_HALO
+        self.sieve_retries = 0
+
+    def _exchange_halo(self, src):
+        """Rank r receives the last SIEVE_HALO rows of rank r-1."""
+        import torch.distributed as dist
+        be = self.backend
+        if self.rank > 0 and self._halo is None:
+            self._halo = be.new_halo_buffer(SIEVE_HALO, src)
+        ops = []
+        if self.rank + 1 < self.world:
+            ops.append(dist.P2POp(dist.isend, src[-SIEVE_HALO:], self.rank + 1, group=self.group))
+        if self.rank > 0:
+            ops.append(dist.P2POp(dist.irecv, self._halo, self.rank - 1, group=self.group))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        return self._halo if self.rank > 0 else None
 
     def launch(self, src) -> None:
         import torch.distributed as dist
         be = self.backend
+        self._src = src
+        if self.sieve:
+            halo = self._exchange_halo(src) if self.world > 1 else None
+            be.sieve(src, halo)
+            if self.world > 1:
+                ks = be.key_status()
+                dist.all_reduce(ks, op=dist.ReduceOp.MAX, group=self.group)
+                self._ks = ks
+            else:
+                self._ks = None
+            return
         if self.world > 1 and hasattr(be, "seed"):
             # pool the ranks' lower bounds (8 bytes) before the band passes
             be.seed(src)
@@ -176,6 +240,13 @@ class RowBandSolver:
 
     def result(self) -> SquareResult:
         ks = (self._ks if self._ks is not None else self.backend.key_status()).cpu().numpy().astype(np.int64)
+        if self.sieve and int(ks[1]) == 2:
+            # some rank's sieve could not decide (every rank sees the same reduced
+            # status): the band protocol, for this solve and the following ones
+            self.sieve = False
+            self.sieve_retries += 1
+            self.launch(self._src)
+            return self.result()
         return decode_key(int(ks[0]), int(ks[1]), self.rows, self.cols)
 
     def solve(self, src) -> SquareResult:

@@ -117,7 +117,7 @@ class Solver:
     def __init__(self, fmt: int, rows: int, cols: int, ld: int | None = None, batch: int = 1,
                  nbands: int = 0, deterministic: bool = False, device=None, engine: int = -1,
                  flags: int = 0, test_floor: int = 0, col_chunks: int = 1):
-        """``engine``: -1 automatic, 0 band engine, 1 register team engine.
+        """``engine``: -1 automatic, 0 band engine, 1 register team engine, 2 sieve engine.
         ``flags`` (N.PLAN_*) and ``test_floor`` are experiment / test switches
         (``test_floor`` presets the shared best side: the caller vouches that
         the answer is at least that)."""
@@ -142,12 +142,20 @@ class Solver:
     def launch(self, src) -> None:
         if not src.is_cuda:
             raise ValueError("Solver.launch expects a CUDA tensor")
+        self._src = src
         N.check(N.load().msq_launch(ctypes.byref(self.plan), ctypes.c_void_p(src.data_ptr()),
                                     ctypes.c_void_p(self.ws.data_ptr()),
                                     ctypes.c_void_p(self.res.data_ptr()), _stream_handle()))
 
     def result(self) -> list[SquareResult]:
         host = self.res.cpu().numpy()
+        if int(self.plan.engine) == N.ENGINE_SIEVE and (int(host[16]) & 2):
+            # the sieve engine could not decide this input (answer outside 56..222 or
+            # too many candidates): the same plan runs the band engine, from now on
+            self.sieve_retries = getattr(self, "sieve_retries", 0) + 1
+            self.plan.engine = N.ENGINE_BAND
+            self.launch(self._src)
+            host = self.res.cpu().numpy()
         return [_decode(host[32 * k:32 * k + 32], self.rows, self.cols) for k in range(self.batch)]
 
     def solve(self, src) -> list[SquareResult]:
