@@ -558,10 +558,10 @@ bool key_range_ok(const msq_plan* pl);
 
 // ---- sieve engine (msq_sieve.cuh): bit-packed single matrices, sparse zeros
 struct SieveGeom {
-    int CR, CC, CWn, WC, nbands, nchunks, wmax, nslots, slot_row_bytes, smem;
-    size_t ctl, cand, gtop, pbot, total;  // workspace offsets (after the band engine's layout)
+    int CR, CC, CWn, WC, nbands, nchunks, wmax, nslots, slot_row_bytes, smem, nunits;
+    size_t ctl, cand, G, total;  // workspace offsets (after the band engine's layout)
 };
-int g_sieve_wpc = 3;  // consumer warps per CTA the plan aims for (instrumentation)
+int g_sieve_wpc = 8;  // most consumer warps per CTA of the streaming pass (instrumentation)
 
 bool sieve_shape_ok(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld) {
     const int64_t words = ceil_div(cols, 32);
@@ -577,15 +577,16 @@ SieveGeom sieve_geom(int64_t rows, int64_t cols, int nbands_fixed) {
     g.CC = (int)(cols / 8);
     g.CWn = (int)ceil_div(g.CC, 32);
     g.WC = (int)ceil_div(g.CWn, 31);
-    g.nchunks = (int)ceil_div(g.WC, std::max(1, g_sieve_wpc));
-    g.wmax = (int)ceil_div(g.WC, g.nchunks);
+    g.nunits = (int)ceil_div(g.CR, msq::SV_OWN);
+    const int WF = (int)ceil_div(W, 256);  // streaming warps per row
+    g.nchunks = (int)ceil_div(WF, std::max(1, g_sieve_wpc));
+    g.wmax = (int)ceil_div(WF, g.nchunks);
     g.nbands = nbands_fixed > 0 ? nbands_fixed
-                                : (int)std::max<long long>(1, std::min<long long>(num_sms() / g.nchunks, g.CR / 32));
+                                : (int)std::max<long long>(1, std::min<long long>(num_sms() / g.nchunks, g.CR));
     int rb = 0;
     for (int c = 0; c < g.nchunks; ++c) {
-        const int wc0 = g.WC * c / g.nchunks, wc1 = g.WC * (c + 1) / g.nchunks;
-        const int mw0 = std::max(0, 8 * (31 * wc0 - 1)), mw1 = std::min(W, 8 * 31 * wc1);
-        rb = std::max(rb, (mw1 - mw0) * 4);
+        const int wc0 = WF * c / g.nchunks, wc1 = WF * (c + 1) / g.nchunks;
+        rb = std::max(rb, (std::min(W, 256 * wc1) - 256 * wc0) * 4);
     }
     g.slot_row_bytes = rb;
     const int fixed = 2 * msq::SV_MAXSLOTS * 8 + 64;
@@ -599,8 +600,7 @@ SieveGeom sieve_geom(int64_t rows, int64_t cols, int nbands_fixed) {
     };
     g.ctl = take(sizeof(msq::SieveCtl));
     g.cand = take((size_t)msq::SV_CAP * 8);
-    g.gtop = take((size_t)g.nbands * msq::SV_EDGE * g.CWn * 4);
-    g.pbot = take((size_t)g.nbands * msq::SV_PL * g.CWn * 4);
+    g.G = take((size_t)g.CR * g.CWn * 4);
     g.total = off;
     return g;
 }
@@ -628,10 +628,10 @@ msq::SieveParams make_sieve(const msq_plan* pl, const void* d_src, const void* d
     p.wmax = g.wmax;
     p.nslots = g.nslots;
     p.slot_row_bytes = g.slot_row_bytes;
+    p.nunits = g.nunits;
     p.ctl = (msq::SieveCtl*)(w + g.ctl);
     p.cand = (unsigned long long*)(w + g.cand);
-    p.gtop = (uint32_t*)(w + g.gtop);
-    p.pbot = (uint32_t*)(w + g.pbot);
+    p.G = (uint32_t*)(w + g.G);
     p.result = (unsigned char*)res;
     return p;
 }
@@ -657,18 +657,18 @@ cudaError_t launch_sieve_pass(const msq_plan* pl, const msq::SieveParams& sp, cu
     return cudaGetLastError();
 }
 
-// band-top block rows with carried-in heights, then the exact windows
+// Algorithm 1 on the block bitmap, then the exact windows of its candidates
 cudaError_t launch_sieve_finish(const msq::SieveParams& sp, cudaStream_t st) {
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)ceil_div((long long)sp.nbands * sp.WC, msq::SV_EWARPS));
+    cfg.gridDim = dim3((unsigned)ceil_div((long long)sp.nunits * sp.WC, msq::SV_EWARPS));
     cfg.blockDim = dim3(32 * msq::SV_EWARPS);
     cfg.stream = st;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, msq::sieve_edge_kernel, sp);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, msq::sieve_coarse_kernel, sp);
     if (e != cudaSuccess) return e;
     cfg.gridDim = dim3((unsigned)(num_sms() * 2));
     cfg.blockDim = dim3(32 * msq::SV_VWARPS);
@@ -902,7 +902,7 @@ extern "C" int msq_plan_make_ex(int32_t fmt, int32_t batch, int64_t rows, int64_
         const bool ok = rc == MSQ_OK && shape_ok && sieve_shape_ok(fmt, batch, rows, cols, ld);
         if (ok) {
             const SieveGeom g = sieve_geom(rows, cols, 0);
-            if (g.nslots >= 2 && g.wmax <= 9) {
+            if (g.nslots >= 2 && g.wmax <= 8) {
                 p.engine = 2;
                 p.sv_bands = g.nbands;
                 p.sv_ws_off = round_up(p.ws_bytes, 256);
@@ -1734,5 +1734,5 @@ extern "C" void msq_debug_set_staging(int32_t workers, int32_t buffers, int64_t 
     g_stage.chunk = chunk_bytes > 0 ? (size_t)chunk_bytes : (4u << 20);
 }
 
-extern "C" void msq_debug_set_sieve_wpc(int32_t warps) { g_sieve_wpc = warps >= 1 && warps <= 9 ? warps : 3; }
+extern "C" void msq_debug_set_sieve_wpc(int32_t warps) { g_sieve_wpc = warps >= 1 && warps <= 8 ? warps : 8; }
 extern "C" void msq_debug_set_team_band_rows(int32_t rows) { g_team_band_rows = rows > 0 ? rows : 16; }

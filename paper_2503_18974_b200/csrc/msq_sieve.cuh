@@ -24,15 +24,18 @@
 // past the anchor's first row and column.  So:
 //
 //   sieve_pass_kernel   streams the rows (TMA ring, one CTA per row band and
-//                       column chunk), ANDs each 8-row tile into G bits, keeps
-//                       the block heights of G as 5 saturating bit-planes per
-//                       lane (one 32-block word per lane, the warp's lane 0 is
-//                       the left halo) and tests one level per block row:
-//                       "a run of >= l blocks of height >= l", l = best D - 1.
-//                       Hits (rare) get their exact D and go to a candidate list.
-//                       The first 31 block rows of a band have no carried-in
-//                       heights: their G words are stored instead and
-//   sieve_edge_kernel   redoes them from the bottom planes of the band above.
+//                       column chunk, a warp per 1024 columns), ANDs each
+//                       8-row tile into G bits and stores G (1 bit per 64
+//                       cells: 8 MB for 65536^2).  Stateless, so any split of
+//                       the rows works and the kernel runs at the HBM rate.
+//   sieve_coarse_kernel Algorithm 1 on G (read from L2): block heights as 5
+//                       saturating bit-planes per lane (one 32-block word per
+//                       lane, lane 0 of a warp is the left halo), one level
+//                       test per block row -- "a run of >= l blocks of height
+//                       >= l", l = best D - 1 -- four rows per vote.  A unit
+//                       owns 32 block rows and warms its heights up on the 31
+//                       rows above.  Hits (rare) get their exact D and go to a
+//                       candidate list.
 //   sieve_verify_kernel runs Algorithm 1 exactly (per-column heights, one test
 //                       per row, leftmost window) on the <= 229 x 229 cell
 //                       window of every candidate with D >= max D - 1 and keeps
@@ -50,7 +53,8 @@
 namespace msq {
 
 constexpr int SV_PL = 5;           // height planes: block heights saturate at 31
-constexpr int SV_EDGE = 31;        // block rows at a band top that need carried-in heights
+constexpr int SV_EDGE = 31;        // block rows above a unit that warm its heights up (they saturate at 31)
+constexpr int SV_OWN = 32;         // block rows a coarse unit owns
 constexpr int SV_DMAX = 26;        // windows of 8 * 26 + 21 = 229 columns (from column 2 mod 8) fit 8 words
 constexpr int SV_LMIN = 6;         // lowest level tested; the sieve decides for max D >= 7
 constexpr int SV_CAP = 8192;       // candidate list entries
@@ -58,7 +62,7 @@ constexpr int SV_TR = 8;           // rows per tile = block height
 constexpr int SV_MAXSLOTS = 16;    // TMA ring depth
 constexpr int SV_HALO_ROWS = 256;  // rows a rank borrows from the rank above
 constexpr int SV_VROWS = 8 * SV_DMAX + 21;
-constexpr int SV_VWARPS = 4;       // verifier warps per CTA (one candidate each)
+constexpr int SV_VWARPS = 8;       // verifier warps per CTA (one candidate per CTA; a power of two)
 constexpr int SV_EWARPS = 4;       // edge-kernel warps per CTA
 
 struct SieveCtl {
@@ -76,10 +80,10 @@ struct SieveParams {
     int rows;             // halo_rows + local rows
     int cols, W;
     long long row_base;   // global row index of row 0 of (halo, local rows)
-    int CR, CC, CWn, WC;  // block rows, block columns, 32-block words per row, warp columns
-    int nbands, nchunks, wmax, nslots, slot_row_bytes;
-    uint32_t* gtop;       // [nbands][SV_EDGE][CWn] G words of each band's first block rows
-    uint32_t* pbot;       // [nbands][SV_PL][CWn] height planes after each band's last block row
+    int CR, CC, CWn, WC;  // block rows, block columns, 32-block words per row, coarse warp columns (31 words each)
+    int nbands, nchunks, wmax, nslots, slot_row_bytes;  // streaming pass: bands x chunks CTAs, wmax warps of 32 words
+    int nunits;           // coarse pass: ceil(CR / SV_OWN) row units x WC warps
+    uint32_t* G;          // [CR][CWn] block bitmap
     unsigned long long* cand;  // [SV_CAP] D << 40 | block row << 16 | block column
     SieveCtl* ctl;
     unsigned char* result;
@@ -154,7 +158,8 @@ __device__ __noinline__ int sv_rare(const SieveParams& p, uint32_t h0, uint32_t 
     return max(lvl, best - 1);
 }
 
-// One block row of the coarse Algorithm 1: heights, one test at the level.
+// One block row of the coarse Algorithm 1: heights, one test at the level (the
+// replay path of SvBatch and its reference semantics).
 __device__ __forceinline__ void sv_step(const SieveParams& p, uint32_t v, uint32_t (&h)[SV_PL], int& lvl,
                                         bool record, int R, int g, bool own, int lane) {
     planes_step<SV_PL>(h, v);
@@ -162,6 +167,83 @@ __device__ __forceinline__ void sv_step(const SieveParams& p, uint32_t v, uint32
     if (!own) hits = 0u;
     if (__any_sync(0xFFFFFFFFu, hits != 0u))
         lvl = sv_rare(p, h[0], h[1], h[2], h[3], h[4], hits, lvl, record, R, g, lane);
+}
+
+// The same, SV_BATCH block rows at a time.  A block with height >= l at one of
+// the batch's rows had height >= l - SV_BATCH before the batch and a one in its
+// first row, so a run of l such blocks is necessary for a hit anywhere in the
+// batch: one compare, one shuffle, one run filter and one vote per batch; the
+// rows in between only advance the heights.  A batch that passes the filter is
+// replayed row by row (sv_step) from the heights it started with.  The level
+// is the one the batch started with (levels only rise: a stale one adds hits).
+constexpr int SV_BATCH = 4;
+struct SvBatch {
+    uint32_t h0[SV_PL];    // heights before the batch
+    uint32_t v[SV_BATCH];  // G words of its rows
+    // branch-free forms of planes_ge (at lvl - SV_BATCH) / sv_runs (lvl) for the current level
+    uint32_t nb[SV_PL];
+    int sh[5];
+    int lvl_of;
+
+    __device__ __forceinline__ void set_level(int lvl) {
+        lvl_of = lvl;
+        const int lf = max(lvl - SV_BATCH, 0);
+#pragma unroll
+        for (int k = 0; k < SV_PL; ++k) nb[k] = ((lf >> k) & 1) ? 0u : 0xFFFFFFFFu;
+        int have = 1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            sh[k] = 2 * have <= lvl ? have : 0;
+            if (2 * have <= lvl) have *= 2;
+        }
+        sh[4] = lvl - have;
+    }
+    __device__ __forceinline__ void begin(const uint32_t (&h)[SV_PL]) {
+#pragma unroll
+        for (int k = 0; k < SV_PL; ++k) h0[k] = h[k];
+#pragma unroll
+        for (int j = 0; j < SV_BATCH; ++j) v[j] = 0u;
+    }
+    __device__ __forceinline__ void push(uint32_t (&h)[SV_PL], uint32_t vv, int j) {
+        planes_step<SV_PL>(h, vv);
+        v[j] = vv;
+    }
+    // can any row of the batch hold a hit (warp-uniform)
+    __device__ __forceinline__ bool test(bool own, int lane) const {
+        uint32_t ge = 0u, eq = 0xFFFFFFFFu;
+#pragma unroll
+        for (int k = SV_PL - 1; k >= 0; --k) {
+            ge |= eq & h0[k] & nb[k];
+            eq &= h0[k] | nb[k];
+        }
+        uint32_t hi = (ge | eq) & v[0];
+        uint32_t lo = __shfl_up_sync(0xFFFFFFFFu, hi, 1);
+        if (lane == 0) lo = 0u;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            hi &= __funnelshift_l(lo, hi, sh[k]);
+            lo &= lo << sh[k];
+        }
+        if (!own) hi = 0u;
+        return __any_sync(0xFFFFFFFFu, hi != 0u);
+    }
+};
+
+// finish a batch of cnt rows whose first block row is R0; h = heights after it
+__device__ __forceinline__ void sv_batch_end(const SieveParams& p, SvBatch& bt, uint32_t (&h)[SV_PL], int cnt,
+                                             int& lvl, int rec_from, int R0, int g, bool own, int lane) {
+    if (bt.test(own, lane)) {
+#pragma unroll
+        for (int k = 0; k < SV_PL; ++k) h[k] = bt.h0[k];
+        for (int j = 0; j < cnt; ++j) {
+            uint32_t vj = bt.v[0];
+#pragma unroll
+            for (int u = 1; u < SV_BATCH; ++u) vj = j == u ? bt.v[u] : vj;
+            sv_step(p, vj, h, lvl, R0 + j >= rec_from, R0 + j, g, own, lane);
+        }
+    }
+    if (lvl != bt.lvl_of) bt.set_level(lvl);
+    bt.begin(h);
 }
 
 // 4 words -> 16 bits: bit 4k + b = byte b of word k is 0xFF
@@ -175,52 +257,51 @@ __device__ __forceinline__ uint32_t sv_flags16(const uint32_t (&a)[4]) {
     return out;
 }
 
-__global__ void __launch_bounds__(320, 1) sieve_pass_kernel(const SieveParams p) {
+__global__ void __launch_bounds__(288, 1) sieve_pass_kernel(const SieveParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int band = blockIdx.x / p.nchunks, chunk = blockIdx.x - band * p.nchunks;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wc0 = p.WC * chunk / p.nchunks, wc1 = p.WC * (chunk + 1) / p.nchunks;
+    const int WF = (p.W + 255) / 256;  // warp columns of 256 matrix words
+    const int wc0 = WF * chunk / p.nchunks, wc1 = WF * (chunk + 1) / p.nchunks;
     const int ncw = wc1 - wc0;  // consumer warps of this chunk
     const int cr0 = sv_band_cr0(p, band);
     const int ntiles = sv_band_cr0(p, band + 1) - cr0;
-    const int mw0 = max(0, 8 * (31 * wc0 - 1));  // matrix words [mw0, mw1) of each row
-    const int mw1 = min(p.W, 8 * 31 * wc1);
+    const int mw0 = 256 * wc0;  // matrix words [mw0, mw1) of each row
+    const int mw1 = min(p.W, 256 * wc1);
     const uint32_t chunk_bytes = (uint32_t)(mw1 - mw0) * 4u;
     const uint32_t srb = (uint32_t)p.slot_row_bytes;
     const uint32_t slot_bytes = SV_TR * srb;
     uint8_t* ring = smem;
     uint64_t* full = (uint64_t*)(smem + (size_t)p.nslots * slot_bytes);
     uint64_t* empty = full + SV_MAXSLOTS;
-    volatile int* stop = (volatile int*)(empty + SV_MAXSLOTS);  // tile at which the producer gave up
 
     if (tid == 0) {
         for (int s = 0; s < p.nslots; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], (uint32_t)ncw);
         }
-        *stop = -1;
         fence_mbar_init();
     }
     __syncthreads();
+    if (ntiles <= 0 || ncw <= 0) return;
 
     // ------------------------------------------------------------ producer
     if (warp == p.wmax) {
         if (lane == 0) {
             const uint64_t pol = l2_evict_first_policy();
+            int s = 0, lap = 0;
             for (int q = 0; q < ntiles; ++q) {
-                const int s = q % p.nslots;
-                if (q >= p.nslots) mbar_wait(&empty[s], (uint32_t)((q / p.nslots - 1) & 1));
-                if ((q & 3) == 3 && ld_volatile(&p.ctl->abort)) {  // the sieve cannot decide: stop streaming
-                    *stop = q;
-                    mbar_arrive(&full[s]);
-                    break;
-                }
+                if (lap > 0) mbar_wait(&empty[s], (uint32_t)((lap - 1) & 1));
                 mbar_expect_tx(&full[s], SV_TR * chunk_bytes);
                 uint8_t* dst = ring + (size_t)s * slot_bytes;
                 const int r = SV_TR * (cr0 + q);
 #pragma unroll
                 for (int b = 0; b < SV_TR; ++b)
                     tma_row(dst + (size_t)b * srb, sv_row(p, r + b) + (size_t)mw0 * 4, chunk_bytes, &full[s], pol);
+                if (++s == p.nslots) {
+                    s = 0;
+                    ++lap;
+                }
             }
         }
         return;
@@ -228,9 +309,8 @@ __global__ void __launch_bounds__(320, 1) sieve_pass_kernel(const SieveParams p)
     if (warp >= ncw) return;
 
     // ------------------------------------------------------------ consumers
-    const int g = 31 * (wc0 + warp) - 1 + lane;  // the lane's 32-block word (lane 0: left halo)
-    const bool in = g >= 0 && g < p.CWn;
-    const bool own = lane > 0 && in;
+    const int g = 32 * (wc0 + warp) + lane;  // the lane's 32-block word of G
+    const bool in = g < p.CWn;
     uint32_t validc = 0u;
     if (in) {
         const int n = p.CC - 32 * g;
@@ -239,24 +319,17 @@ __global__ void __launch_bounds__(320, 1) sieve_pass_kernel(const SieveParams p)
     // the lane's 8 matrix words = two 16-byte halves; lanes 4..7 (mod 8) read the
     // upper half first so a quarter-warp's 8 loads cover all 32 banks
     const int sw = (lane >> 2) & 1;
-    const bool okA = in && 8 * g + 4 * sw < mw1;
-    const bool okB = in && 8 * g + 4 * (1 - sw) < mw1;
+    const bool okA = 8 * g + 4 * sw < mw1;
+    const bool okB = 8 * g + 4 * (1 - sw) < mw1;
     const uint32_t ring_s = smem_addr(ring);
     const uint32_t offA = okA ? (uint32_t)(8 * g + 4 * sw - mw0) * 4u : 0u;
     const uint32_t offB = okB ? (uint32_t)(8 * g + 4 * (1 - sw) - mw0) * 4u : 0u;
-    uint32_t h[SV_PL] = {0u, 0u, 0u, 0u, 0u};
-    int lvl = SV_LMIN;
-    bool finished = true;
+    uint32_t* grow = p.G + (size_t)cr0 * p.CWn + g;
 
+    int s = 0;
+    uint32_t par = 0u;
     for (int q = 0; q < ntiles; ++q) {
-        const int s = q % p.nslots;
-        const uint32_t par = (uint32_t)((q / p.nslots) & 1);
-        const int gbest = (q & 3) == 0 ? ld_volatile(&p.ctl->best) : 0;  // used after the tile
         mbar_wait(&full[s], par);
-        if (*stop == q) {
-            finished = false;
-            break;
-        }
         const uint32_t slot_s = ring_s + (uint32_t)s * slot_bytes;
         uint32_t A[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
         uint32_t B[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
@@ -275,96 +348,175 @@ __global__ void __launch_bounds__(320, 1) sieve_pass_kernel(const SieveParams p)
         if (lane == 0) mbar_arrive(&empty[s]);
         const uint32_t cA = okA ? sv_flags16(A) : 0u, cB = okB ? sv_flags16(B) : 0u;
         const uint32_t v = (sw ? (cB | (cA << 16)) : (cA | (cB << 16))) & validc;
-        if (q < SV_EDGE && own) p.gtop[((size_t)band * SV_EDGE + q) * p.CWn + g] = v;
-        sv_step(p, v, h, lvl, q >= SV_EDGE, cr0 + q, g, own, lane);
-        if ((q & 3) == 0) lvl = max(lvl, gbest - 1);
-    }
-    if (own && finished) {
-#pragma unroll
-        for (int k = 0; k < SV_PL; ++k) p.pbot[((size_t)band * SV_PL + k) * p.CWn + g] = h[k];
+        if (in) grow[(size_t)q * p.CWn] = v;
+        if (++s == p.nslots) {
+            s = 0;
+            par ^= 1u;
+        }
     }
 }
 
-// The first block rows of every band again, now with the heights carried in
-// from the band above (band 0: zeros).
-__global__ void __launch_bounds__(32 * SV_EWARPS) sieve_edge_kernel(const SieveParams p) {
-    __shared__ uint32_t vs[SV_EWARPS][SV_EDGE][32];
+// Algorithm 1 on the block bitmap G.  Unit = (SV_OWN block rows, warp column of
+// 31 words + the halo word on the left).  The 31 rows above the unit rebuild
+// its carried-in heights (they saturate at 31); one climb at the last of them
+// gives the unit a local lower bound for the shared best before it records
+// anything.  The first unit has no rows above it and walks its own first rows
+// for that bound, then starts again from zero heights.
+__global__ void __launch_bounds__(32 * SV_EWARPS) sieve_coarse_kernel(const SieveParams p) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int unit = blockIdx.x * SV_EWARPS + warp;
-    if (unit >= p.nbands * p.WC) return;
-    if (ld_volatile(&p.ctl->abort)) return;
-    const int band = unit / p.WC, wc = unit - band * p.WC;
+    if (unit >= p.nunits * p.WC) return;
+    const int ru = unit / p.WC, wc = unit - ru * p.WC;
     const int g = 31 * wc - 1 + lane;
     const bool in = g >= 0 && g < p.CWn;
     const bool own = lane > 0 && in;
-    const int cr0 = sv_band_cr0(p, band);
-    const int n = min(SV_EDGE, sv_band_cr0(p, band + 1) - cr0);
-    for (int i = 0; i < n; ++i) vs[warp][i][lane] = in ? p.gtop[((size_t)band * SV_EDGE + i) * p.CWn + g] : 0u;
-    uint32_t h[SV_PL];
+    const int R0 = ru * SV_OWN, R1 = min(p.CR, R0 + SV_OWN);
+    const int Rw = ru > 0 ? R0 - SV_EDGE : 0;               // first warm-up row
+    const int nwarm = ru > 0 ? SV_EDGE : min(SV_EDGE, R1);  // rows walked for heights only
+    const uint32_t* gp = p.G + (in ? g : 0);
+    if (ld_volatile(&p.ctl->abort)) return;
+    uint32_t h[SV_PL] = {0u, 0u, 0u, 0u, 0u};
+    // ---- warm-up: heights only, every row's word in flight at once.  c[k] =
+    // "the last k rows are ones" is monotone in k, so the height (how many k hold)
+    // has bit b set where c[m * 2^b] holds and c[(m + 1) * 2^b] does not, m odd.
+    {
+        uint32_t c[SV_EDGE + 2];
+        c[0] = 0xFFFFFFFFu;
 #pragma unroll
-    for (int k = 0; k < SV_PL; ++k)
-        h[k] = (band > 0 && in) ? p.pbot[((size_t)(band - 1) * SV_PL + k) * p.CWn + g] : 0u;
+        for (int k = 1; k <= SV_EDGE; ++k)
+            c[k] = (in && k <= nwarm) ? __ldcg(gp + (size_t)(Rw + nwarm - k) * p.CWn) : 0u;
+#pragma unroll
+        for (int k = 1; k <= SV_EDGE; ++k) c[k] &= c[k - 1];
+        c[SV_EDGE + 1] = 0u;
+#pragma unroll
+        for (int b = 0; b < SV_PL; ++b) {
+            uint32_t acc = 0u;
+#pragma unroll
+            for (int m = 1; (m << b) <= SV_EDGE; m += 2) acc |= c[m << b] & ~c[min((m + 1) << b, SV_EDGE + 1)];
+            h[b] = acc;
+        }
+    }
     int lvl = max(SV_LMIN, ld_volatile(&p.ctl->best) - 1);
-    __syncwarp();
-    for (int i = 0; i < n; ++i) sv_step(p, vs[warp][i][lane], h, lvl, true, cr0 + i, g, own, lane);
+    {   // one climb at the last warm-up row: a lower bound, nothing recorded
+        uint32_t hits = sv_hits(h, lvl, lane);
+        if (!own) hits = 0u;
+        if (__any_sync(0xFFFFFFFFu, hits != 0u))
+            lvl = sv_rare(p, h[0], h[1], h[2], h[3], h[4], hits, lvl, false, 0, g, lane);
+    }
+    if (ru == 0) {  // the first unit's own rows start from zero heights
+#pragma unroll
+        for (int k = 0; k < SV_PL; ++k) h[k] = 0u;
+    }
+    SvBatch bt;
+    bt.set_level(lvl);
+    bt.begin(h);
+    // ---- own rows: two batches of words in flight
+    for (int i0 = R0; i0 < R1; i0 += 2 * SV_BATCH) {
+        uint32_t vv[2 * SV_BATCH];
+#pragma unroll
+        for (int j = 0; j < 2 * SV_BATCH; ++j)
+            vv[j] = (in && i0 + j < R1) ? __ldcg(gp + (size_t)(i0 + j) * p.CWn) : 0u;
+        const int gbest = ld_volatile(&p.ctl->best);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            const int r0 = i0 + half * SV_BATCH;
+            const int cnt = min(SV_BATCH, R1 - r0);
+            if (cnt > 0) {
+#pragma unroll
+                for (int j = 0; j < SV_BATCH; ++j)
+                    if (j < cnt) bt.push(h, vv[half * SV_BATCH + j], j);
+                if (half == 0) lvl = max(lvl, gbest - 1);
+                sv_batch_end(p, bt, h, cnt, lvl, 0, r0, g, own, lane);
+            }
+        }
+    }
 }
 
-// Algorithm 1 on the cell window of every candidate that can still hold the answer.
+// Algorithm 1 on the cell window of every candidate that can still hold the
+// answer; one CTA per candidate.  All threads load the window (every load in
+// flight at once) and fold the zeros of the rows before the first testable row
+// into per-column last-zero rows.  Every warp then walks the remaining rows
+// (heights from the last-zero rows) and tests every SV_VWARPS-th of them: at the
+// best side so far (a tie), then upwards until the row's own largest square is
+// known.  The largest key -- side, then first bottom row, then leftmost column
+// -- is Algorithm 1's answer for the window (squares.py:93-97).
 __global__ void __launch_bounds__(32 * SV_VWARPS) sieve_verify_kernel(const SieveParams p) {
-    __shared__ __align__(16) uint32_t rowsm[SV_VWARPS][SV_VROWS][8];
+    __shared__ __align__(16) uint32_t rowsm[SV_VROWS][8];
+    __shared__ int lzs[256];
+    __shared__ int tsh;                   // best side so far (this window or any other)
+    __shared__ unsigned long long keysh;  // best key of this window
+    constexpr int NT = 32 * SV_VWARPS;
+    constexpr int LPT = (SV_VROWS * 8 + NT - 1) / NT;  // window words per thread
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int gw = blockIdx.x * SV_VWARPS + warp, nw = gridDim.x * SV_VWARPS;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // the control block, this CTA's first candidate and the best side so far: one round trip
     const int best = ld_volatile(&p.ctl->best);
-    if (ld_volatile(&p.ctl->abort) || best <= SV_LMIN) {  // undecided: the caller runs the band engine
-        if (gw == 0 && lane == 0) atomicOr(res_status(p.result), 2u);
+    const int aborted = ld_volatile(&p.ctl->abort);
+    const int count = min(ld_volatile(&p.ctl->count), SV_CAP);
+    const unsigned long long c_first = blockIdx.x < SV_CAP ? __ldcg(p.cand + blockIdx.x) : 0ull;
+    const int rb0 = ld_volatile(res_best(p.result));
+    if (aborted || best <= SV_LMIN) {  // undecided: the caller runs the band engine
+        if (blockIdx.x == 0 && tid == 0) atomicOr(res_status(p.result), 2u);
         return;
     }
-    const int count = min(ld_volatile(&p.ctl->count), SV_CAP);
     const int T0 = 8 * best;
     for (int pass = 0; pass < 2; ++pass) {
         const int Dp = best - pass;
-        for (int idx = gw; idx < count; idx += nw) {
-            const unsigned long long c = p.cand[idx];
+        for (int idx = blockIdx.x; idx < count; idx += gridDim.x) {
+            const unsigned long long c = idx == (int)blockIdx.x ? c_first : __ldcg(p.cand + idx);
             const int D = (int)(c >> 40);
             if (D != Dp) continue;
-            int t = max(T0, ld_volatile(res_best(p.result)));  // ties at the best side so far
-            if (8 * D + 14 < t) continue;
+            __syncthreads();  // the previous candidate's rows are done with
+            if (tid == 0) {
+                // ties at the best side so far (re-read once this CTA has found something itself)
+                tsh = max(T0, idx == (int)blockIdx.x && pass == 0 ? rb0 : ld_volatile(res_best(p.result)));
+                keysh = 0ull;
+            }
+            for (int i = tid; i < 256; i += NT) lzs[i] = -1;
+            __syncthreads();
+            const int t0 = tsh;
+            if (8 * D + 14 < t0) continue;  // CTA-uniform
             const int Rg = (int)((c >> 16) & 0xFFFFFFull), cg = (int)(c & 0xFFFFull);
             const int r_hi = min(p.rows - 1, 8 * Rg + 14), r_lo = max(0, 8 * (Rg - D) - 6);
             const int c_hi = min(p.cols - 1, 8 * cg + 14), c_lo = max(0, 8 * (cg - D) - 6);
             const int nr = r_hi - r_lo + 1, wa = c_lo >> 5, nwd = (c_hi >> 5) - wa + 1;
-            uint32_t msk[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
+            const int first = t0 - 1;  // first row (window-relative) whose heights can reach t0
+            auto word_mask = [&](int k) -> uint32_t {
                 const int lo = max(c_lo - 32 * (wa + k), 0), hi = min(c_hi - 32 * (wa + k), 31);
-                msk[k] = (k < nwd && hi >= lo) ? ((hi == 31 ? 0xFFFFFFFFu : (1u << (hi + 1)) - 1u) & ~((1u << lo) - 1u))
-                                               : 0u;
+                return (k < nwd && hi >= lo) ? ((hi == 31 ? 0xFFFFFFFFu : (1u << (hi + 1)) - 1u) & ~((1u << lo) - 1u)) : 0u;
+            };
+            uint32_t wv[LPT];
+#pragma unroll
+            for (int u = 0; u < LPT; ++u) {
+                const int i = tid + NT * u, rr = i >> 3, k = i & 7;
+                wv[u] = (rr < nr && k < nwd) ? __ldg((const uint32_t*)(sv_row(p, r_lo + rr)) + wa + k) : 0xFFFFFFFFu;
             }
-            __syncwarp();
-            // the window's words (lanes spread over rows and words, all loads in flight)
-            for (int i = lane; i < nr * 8; i += 32) {
-                const int rr = i >> 3, k = i & 7;
-                uint32_t w = 0u;
-                if (k < nwd) w = __ldg((const uint32_t*)(sv_row(p, r_lo + rr)) + wa + k);
-                rowsm[warp][rr][k] = w;
+#pragma unroll
+            for (int u = 0; u < LPT; ++u) {
+                const int i = tid + NT * u, rr = i >> 3, k = i & 7;
+                if (rr < nr) {
+                    rowsm[rr][k] = wv[u];
+                    if (rr < first) {
+                        uint32_t z = ~wv[u] & word_mask(k);
+                        while (z) {
+                            const int j = __ffs(z) - 1;
+                            z &= z - 1;
+                            atomicMax(&lzs[32 * k + j], rr);
+                        }
+                    }
+                }
             }
-            __syncwarp();
+            __syncthreads();
+            uint32_t msk[8];
             int lz[8];  // last zero row (window-relative) of column 32k + lane
 #pragma unroll
-            for (int k = 0; k < 8; ++k) lz[k] = -1;
-            unsigned long long key = 0ull;
-            int side = 0;
-            for (int rr = 0; rr < nr && t <= nr; ++rr) {
-                const uint4 a = *(const uint4*)&rowsm[warp][rr][0];
-                const uint4 b = *(const uint4*)&rowsm[warp][rr][4];
-                const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    if ((w[k] & msk[k]) != msk[k] && !((w[k] >> lane) & 1u)) lz[k] = rr;
-                if (rr + 1 < t) continue;
-                // leftmost window of t columns of height >= t
+            for (int k = 0; k < 8; ++k) {
+                msk[k] = word_mask(k);
+                lz[k] = lzs[32 * k + lane];
+            }
+            // leftmost window end of t columns of height >= t at row rr, or -1
+            auto window = [&](int rr, int t) -> int {
                 int run = 0, e = -1;
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
@@ -373,15 +525,35 @@ __global__ void __launch_bounds__(32 * SV_VWARPS) sieve_verify_kernel(const Siev
                     if (e < 0 && run + pre >= t) e = 32 * k + (t - run) - 1;
                     run = x == 0xFFFFFFFFu ? run + 32 : __clz(~x);
                 }
-                if (e >= 0) {
-                    key = pack_key(t, p.row_base + r_lo + rr, (long long)32 * wa + e);
-                    side = t;
+                return e;
+            };
+            for (int rr = max(first, 0); rr < nr; ++rr) {
+                const uint4 a = *(const uint4*)&rowsm[rr][0];
+                const uint4 b = *(const uint4*)&rowsm[rr][4];
+                const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if ((w[k] & msk[k]) != msk[k] && !((w[k] >> lane) & 1u)) lz[k] = rr;
+                if (((rr - first) & (SV_VWARPS - 1)) != warp) continue;  // another warp's row
+                int t = *(volatile int*)&tsh;
+                if (rr + 1 < t || t > nr) continue;
+                int e = window(rr, t);
+                if (e < 0) continue;
+                for (;;) {  // the row's own largest square
+                    const int e2 = rr + 1 > t ? window(rr, t + 1) : -1;
+                    if (e2 < 0) break;
+                    e = e2;
                     ++t;
                 }
+                if (lane == 0) {
+                    atomicMax(&tsh, t);
+                    atomicMax(&keysh, pack_key(t, p.row_base + r_lo + rr, (long long)32 * wa + e));
+                }
             }
-            if (key && lane == 0) {
-                atomicMax(res_key1(p.result), key);
-                atomicMax(res_best(p.result), side);
+            __syncthreads();
+            if (tid == 0 && keysh) {
+                atomicMax(res_key1(p.result), keysh);
+                atomicMax(res_best(p.result), (int)(keysh >> (2 * KEY_DIM_BITS)));
             }
         }
     }
