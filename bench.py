@@ -439,6 +439,25 @@ def main():
                 e1.record(stream)
                 p1_ev.append((e0, e1))
             return 1
+        if instrument and band_solver.sieve:
+            # as RowBandSolver.launch on the sieve engine, with events around its
+            # streaming pass (the kernel that reads the matrix)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            be_ = band_solver.backend
+            halo = band_solver._exchange_halo(src) if world > 1 else None
+            e0.record(stream)
+            be_.sieve_pass(src, halo)
+            e1.record(stream)
+            p1_ev.append((e0, e1))
+            be_.sieve_finish(src, halo)
+            if world > 1:
+                ks = be_.key_status()
+                dist.all_reduce(ks, op=dist.ReduceOp.MAX)
+                band_solver._ks = ks
+            else:
+                band_solver._ks = None
+            return 0
         if instrument:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -529,6 +548,8 @@ def main():
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
                 "kernel": ("msq::team_kernel" if use_solver and int(solver.plan.engine) == 1 else
+                           "msq::sieve_pass_kernel (the sieve engine's streaming pass: every input byte once, "
+                           "block bitmap out)" if not use_solver and band_solver.sieve else
                            "band pass: msq::strip_kernel (+ ubits_kernel for the bands it hands back), "
                            "timed with the seed_climb_kernel before it" if fmt == N.FMT_BITS else
                            "band pass: msq::ustrip_kernel, timed with the seed_climb_kernel before it"),
@@ -604,7 +625,14 @@ def main():
             "config": {"workload": spec["workload"], "rows": rows, "cols": cols, "batch": batch,
                        "format": "bits" if fmt == N.FMT_BITS else "u8",
                        "parallelism": (f"matrices x{world}" if batch > 1 else
-                                       "one team (register engine)" if use_solver else f"row-bands x{world}"),
+                                       "one team (register engine)" if use_solver else
+                                       f"sieve engine, row slices x{world}" if band_solver.sieve else
+                                       f"row-bands x{world}"),
+                       "engine": ("team" if use_solver and int(solver.plan.engine) == 1 else
+                                  "batch teams" if use_solver else
+                                  "sieve" if band_solver.sieve else
+                                  "band" + (" (sieve undecided on this input: %d retry)" % band_solver.sieve_retries
+                                            if band_solver.sieve_retries else "")),
                        "nbands_per_rank": int(be.plan.nbands) if not use_solver else 1,
                        "l2": ("input > 126 MB L2, no flush" if flush is None
                               else "256 MiB L2 flush between steps"),

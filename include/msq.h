@@ -38,7 +38,7 @@ extern "C" {
 #define MSQ_ECUDA 3    /* CUDA runtime error -> Python RuntimeError          */
 #define MSQ_ENOMEM 4   /* workspace allocation failed                        */
 #define MSQ_EAGAIN 5   /* msq_decode of a sieve-engine launch that could not decide
-                          (status bit 1): launch again with plan.engine = 0; the
+                          (status bits 1, 2): launch again with plan.engine = 0; the
                           msq_solve_* calls do that themselves                  */
 
 /* input formats */
@@ -57,8 +57,10 @@ typedef struct {
 typedef struct {
     uint64_t key_pass1;  /* best key from band passes                     */
     uint64_t key_fix;    /* best key from band-boundary fix-ups            */
-    uint32_t status;     /* bit 0: invalid u8 cell; bit 1: the sieve engine
-                            could not decide (run the band engine)         */
+    uint32_t status;     /* bit 0: invalid u8 cell; bits 1, 2: the sieve engine
+                            could not decide (bit 1: block squares beyond its
+                            windows or too many candidates; bit 2: nothing
+                            above side 62 in these rows): run the band engine */
     int32_t best_side;   /* running best side shared between bands         */
     uint64_t reserved;
 } msq_devresult;
@@ -123,8 +125,8 @@ int msq_plan_make(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_
                   int32_t nbands, int32_t deterministic, msq_plan* plan);
 /* Same with an engine choice: -1 = automatic (msq_plan_make), 0 = band
  * engine, 1 = register team engine (cols <= 1024; MSQ_EINVAL otherwise),
- * 2 = sieve engine (bit-packed, one matrix, rows and cols >= 64, cols a
- * multiple-of-128 word count, 16-byte row stride; automatic from 4096 x 4096). */
+ * 2 = sieve engine (bit-packed, one matrix, rows and cols >= 64, row stride a
+ * multiple of 16 bytes; automatic from 4096 x 4096). */
 int msq_plan_make_ex(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld,
                      int32_t nbands, int32_t deterministic, int32_t engine, msq_plan* plan);
 
@@ -247,7 +249,8 @@ int msq_rank_fixup(const msq_plan* plan, void* d_ws, const uint32_t* d_base_carr
  * exchange is that halo before the solve and the all-reduce(max) of the key
  * after it.  msq_rank_sieve = msq_rank_sieve_pass (the streaming kernel) +
  * msq_rank_sieve_finish (band-top block rows, exact candidate windows).
- * Status bit 1 on any rank: all ranks run steps 1-6 above instead. */
+ * Status bit 1 on any rank, or bit 2 on some rank while the reduced key's side
+ * is <= 62: all ranks run steps 1-6 above instead. */
 int msq_rank_sieve(const msq_plan* plan, const void* d_src, const void* d_halo, int64_t halo_rows,
                    int64_t halo_ld, void* d_ws, msq_devresult* d_result, void* stream);
 int msq_rank_sieve_pass(const msq_plan* plan, const void* d_src, const void* d_halo, int64_t halo_rows,
@@ -255,7 +258,8 @@ int msq_rank_sieve_pass(const msq_plan* plan, const void* d_src, const void* d_h
 int msq_rank_sieve_finish(const msq_plan* plan, const void* d_src, const void* d_halo, int64_t halo_rows,
                           int64_t halo_ld, void* d_ws, msq_devresult* d_result, void* stream);
 /* d_out[0] = max(key_pass1, key_fix), d_out[1] = 3 for an invalid cell, 2 when
- * the sieve could not decide, else 0: the two int64 the ranks all-reduce(max)
+ * the sieve could not decide (status bit 1), 1 when it found nothing above side
+ * 62 in this rank's rows (bit 2), else 0: the two int64 the ranks all-reduce(max)
  * (one tiny kernel on `stream`). */
 int msq_rank_key_status(const msq_devresult* d_result, int64_t* d_out, void* stream);
 

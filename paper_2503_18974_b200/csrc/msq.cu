@@ -566,13 +566,13 @@ int g_sieve_wpc = 8;  // most consumer warps per CTA of the streaming pass (inst
 bool sieve_shape_ok(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld) {
     const int64_t words = ceil_div(cols, 32);
     return fmt == MSQ_FMT_BITS && batch == 1 && rows >= 64 && cols >= 64 && rows < (1ll << 21) - 1 - msq::SV_HALO_ROWS &&
-           cols <= 65536 && words % 4 == 0 && ld >= words && (ld * 4) % 16 == 0;
+           cols <= 65536 && ld >= words && (ld * 4) % 16 == 0;
 }
 
 // geometry for `rows` rows (halo rows included); nbands_fixed > 0 keeps the plan's band count
 SieveGeom sieve_geom(int64_t rows, int64_t cols, int nbands_fixed) {
     SieveGeom g{};
-    const int W = (int)ceil_div(cols, 32);
+    const int W = (int)round_up(ceil_div(cols, 32), 4);  // rows are copied in 16-byte units
     g.CR = (int)(rows / 8);
     g.CC = (int)(cols / 8);
     g.CWn = (int)ceil_div(g.CC, 32);
@@ -758,7 +758,7 @@ int solve_locked(DevCache& C, int32_t fmt, int64_t batch, const void* d_src, int
                         st) != cudaSuccess)
         return MSQ_ECUDA;
     if (cudaStreamSynchronize(st) != cudaSuccess) return MSQ_ECUDA;
-    if (pl.engine == 2 && (C.hres[0].status & 2u)) {  // the sieve could not decide: band engine
+    if (pl.engine == 2 && (C.hres[0].status & 6u)) {  // the sieve could not decide: band engine
         pl.engine = 0;
         rc = msq_launch(&pl, d_src, C.ws, C.res, stream);
         if (rc) return rc;
@@ -906,7 +906,8 @@ extern "C" int msq_plan_make_ex(int32_t fmt, int32_t batch, int64_t rows, int64_
                 p.engine = 2;
                 p.sv_bands = g.nbands;
                 p.sv_ws_off = round_up(p.ws_bytes, 256);
-                p.ws_bytes = p.sv_ws_off + (int64_t)g.total;
+                // the bitmap also covers the halo rows a rank may pass (msq_rank_sieve)
+                p.ws_bytes = p.sv_ws_off + (int64_t)sieve_geom(rows + msq::SV_HALO_ROWS, cols, g.nbands).total;
                 *plan = p;
                 return MSQ_OK;
             }
@@ -1144,7 +1145,7 @@ int msq_decode(const msq_devresult* r, int64_t rows, int64_t cols, msq_result* o
         *out = msq_result{side, side * side, rows * cols, bottom - side + 1, right - side + 1};
     }
     if (r->status & 1u) return MSQ_EVALUE;
-    return (r->status & 2u) ? MSQ_EAGAIN : MSQ_OK;
+    return (r->status & 6u) ? MSQ_EAGAIN : MSQ_OK;
 }
 
 int msq_solve_u8(const uint8_t* d_cells, int64_t rows, int64_t cols, int64_t ld, msq_result* out,

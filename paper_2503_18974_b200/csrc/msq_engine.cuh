@@ -2262,13 +2262,13 @@ __global__ void compose_carry_kernel(const uint32_t* summaries, RankRows rr, int
     out[j] = c > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c;
 }
 
-// [max(key_pass1, key_fix), 3 = invalid cell / 2 = sieve undecided / 0] as two int64 for the ranks' all-reduce(max)
+// [max(key_pass1, key_fix), 3 = invalid cell / 2 = sieve undecided / 1 = sieve: nothing above 62 here / 0] as two int64 for the ranks' all-reduce(max)
 __global__ void key_status_kernel(const unsigned char* result, long long* out) {
     const unsigned long long k1 = *(const unsigned long long*)result;
     const unsigned long long k2 = *(const unsigned long long*)(result + 8);
     out[0] = (long long)(k1 > k2 ? k1 : k2);
     const unsigned s = *(const unsigned*)(result + 16);
-    out[1] = (s & 1u) ? 3ll : (long long)(s & 2u);
+    out[1] = (s & 1u) ? 3ll : (s & 2u) ? 2ll : (s & 4u) ? 1ll : 0ll;
 }
 
 // ======================================================= input generator

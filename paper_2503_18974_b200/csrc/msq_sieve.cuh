@@ -43,7 +43,9 @@
 //
 // The answer is exact whenever the sieve decides: max D in [7, 26] (answers
 // 56..222) and the candidate list did not overflow.  Otherwise status bit 1
-// asks the caller to run the band engine (MSQ_EAGAIN); nothing is guessed.
+// (blocks too large, list overflow) or bit 2 (max D < 7: nothing above 62 in
+// these rows) asks the caller to run the band engine (MSQ_EAGAIN); nothing is
+// guessed.
 //
 // Multi-GPU: a rank prepends the last SV_HALO_ROWS (256 >= 222) rows of the
 // rank above (`halo`), so every square the sieve can report lies wholly inside
@@ -176,7 +178,11 @@ __device__ __forceinline__ void sv_step(const SieveParams& p, uint32_t v, uint32
 // rows in between only advance the heights.  A batch that passes the filter is
 // replayed row by row (sv_step) from the heights it started with.  The level
 // is the one the batch started with (levels only rise: a stale one adds hits).
-constexpr int SV_BATCH = 4;
+#ifndef MSQ_SV_BATCH
+#define MSQ_SV_BATCH 2
+#endif
+constexpr int SV_BATCH = MSQ_SV_BATCH;
+constexpr int SV_GROUP = 8;  // G rows a coarse unit keeps in flight
 struct SvBatch {
     uint32_t h0[SV_PL];    // heights before the batch
     uint32_t v[SV_BATCH];  // G words of its rows
@@ -261,13 +267,17 @@ __global__ void __launch_bounds__(288, 1) sieve_pass_kernel(const SieveParams p)
     extern __shared__ __align__(128) uint8_t smem[];
     const int band = blockIdx.x / p.nchunks, chunk = blockIdx.x - band * p.nchunks;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int WF = (p.W + 255) / 256;  // warp columns of 256 matrix words
+    const int Wp = (p.W + 3) & ~3;     // rows are copied in 16-byte units (the stride covers the pad words)
+    const int WF = (Wp + 255) / 256;   // warp columns of 256 matrix words
     const int wc0 = WF * chunk / p.nchunks, wc1 = WF * (chunk + 1) / p.nchunks;
     const int ncw = wc1 - wc0;  // consumer warps of this chunk
+    // a contiguous band of block rows per CTA (interleaving the CTAs' tiles so that the
+    // bitmap fills top down -- to run the coarse pass beside this kernel -- cost 30% of
+    // the bandwidth: 89 -> 116 us on cfg4)
     const int cr0 = sv_band_cr0(p, band);
     const int ntiles = sv_band_cr0(p, band + 1) - cr0;
     const int mw0 = 256 * wc0;  // matrix words [mw0, mw1) of each row
-    const int mw1 = min(p.W, 256 * wc1);
+    const int mw1 = min(Wp, 256 * wc1);
     const uint32_t chunk_bytes = (uint32_t)(mw1 - mw0) * 4u;
     const uint32_t srb = (uint32_t)p.slot_row_bytes;
     const uint32_t slot_bytes = SV_TR * srb;
@@ -324,7 +334,7 @@ __global__ void __launch_bounds__(288, 1) sieve_pass_kernel(const SieveParams p)
     const uint32_t ring_s = smem_addr(ring);
     const uint32_t offA = okA ? (uint32_t)(8 * g + 4 * sw - mw0) * 4u : 0u;
     const uint32_t offB = okB ? (uint32_t)(8 * g + 4 * (1 - sw) - mw0) * 4u : 0u;
-    uint32_t* grow = p.G + (size_t)cr0 * p.CWn + g;
+    uint32_t* grow = p.G + (size_t)cr0 * p.CWn + (in ? g : 0);
 
     int s = 0;
     uint32_t par = 0u;
@@ -411,22 +421,22 @@ __global__ void __launch_bounds__(32 * SV_EWARPS) sieve_coarse_kernel(const Siev
     SvBatch bt;
     bt.set_level(lvl);
     bt.begin(h);
-    // ---- own rows: two batches of words in flight
-    for (int i0 = R0; i0 < R1; i0 += 2 * SV_BATCH) {
-        uint32_t vv[2 * SV_BATCH];
+    // ---- own rows: SV_GROUP words in flight
+    for (int i0 = R0; i0 < R1; i0 += SV_GROUP) {
+        uint32_t vv[SV_GROUP];
 #pragma unroll
-        for (int j = 0; j < 2 * SV_BATCH; ++j)
+        for (int j = 0; j < SV_GROUP; ++j)
             vv[j] = (in && i0 + j < R1) ? __ldcg(gp + (size_t)(i0 + j) * p.CWn) : 0u;
         const int gbest = ld_volatile(&p.ctl->best);
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            const int r0 = i0 + half * SV_BATCH;
+        for (int part = 0; part < SV_GROUP / SV_BATCH; ++part) {
+            const int r0 = i0 + part * SV_BATCH;
             const int cnt = min(SV_BATCH, R1 - r0);
             if (cnt > 0) {
 #pragma unroll
                 for (int j = 0; j < SV_BATCH; ++j)
-                    if (j < cnt) bt.push(h, vv[half * SV_BATCH + j], j);
-                if (half == 0) lvl = max(lvl, gbest - 1);
+                    if (j < cnt) bt.push(h, vv[part * SV_BATCH + j], j);
+                if (part == 0) lvl = max(lvl, gbest - 1);
                 sv_batch_end(p, bt, h, cnt, lvl, 0, r0, g, own, lane);
             }
         }
@@ -456,8 +466,11 @@ __global__ void __launch_bounds__(32 * SV_VWARPS) sieve_verify_kernel(const Siev
     const int count = min(ld_volatile(&p.ctl->count), SV_CAP);
     const unsigned long long c_first = blockIdx.x < SV_CAP ? __ldcg(p.cand + blockIdx.x) : 0ull;
     const int rb0 = ld_volatile(res_best(p.result));
-    if (aborted || best <= SV_LMIN) {  // undecided: the caller runs the band engine
-        if (blockIdx.x == 0 && tid == 0) atomicOr(res_status(p.result), 2u);
+    if (aborted || best <= SV_LMIN) {
+        // undecided: blocks too large for the windows / too many candidates (bit 1), or
+        // no block square of side 7 in these rows, i.e. nothing above 8 * 6 + 14 = 62
+        // here (bit 2: still decided if another rank holds a larger square)
+        if (blockIdx.x == 0 && tid == 0) atomicOr(res_status(p.result), aborted ? 2u : 4u);
         return;
     }
     const int T0 = 8 * best;

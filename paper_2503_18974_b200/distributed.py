@@ -29,6 +29,7 @@ from .squares import SquareResult
 
 KEY_DIM_BITS = 21
 KEY_DIM_MASK = (1 << KEY_DIM_BITS) - 1
+SIEVE_LOW_MAX = 62  # status 1 (no block square of side 7 on some rank) is harmless above this side
 SIEVE_HALO = 256  # rows a rank borrows from the rank above (msq_sieve.cuh SV_HALO_ROWS)
 
 
@@ -38,7 +39,7 @@ def slice_rows(rows: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def decode_key(key: int, status: int, rows: int, cols: int) -> SquareResult:
-    if status & 1:
+    if status & 1:  # 1 (device status) / 3 (reduced [key, status]): an invalid cell
         raise ValueError("cells must contain only 0 or 1")
     if key == 0:
         return SquareResult(0, 0, rows * cols)
@@ -52,12 +53,12 @@ class GpuBackend:
     """Per-rank steps on the local GPU through libmsq."""
 
     def __init__(self, fmt: int, local_rows: int, cols: int, row_base: int, ld: int | None = None,
-                 nbands: int = 0, device=None):
+                 nbands: int = 0, device=None, engine: int = -1):
         import torch
         self.torch = torch
         words = (cols + 31) // 32
         ld = ld if ld is not None else (cols if fmt == N.FMT_U8 else words)
-        self.plan = N.plan(fmt, 1, local_rows, cols, ld, nbands)
+        self.plan = N.plan(fmt, 1, local_rows, cols, ld, nbands, engine=engine)
         self.plan.row_base = row_base
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.ws = torch.empty(max(int(self.plan.ws_bytes), 256), dtype=torch.uint8, device=dev)
@@ -170,7 +171,7 @@ class RowBandSolver:
     """Solve one (rows x cols) matrix sharded by rows over a process group.
 
     Backends whose plan is a sieve plan (``is_sieve``) try the sieve first: each
-    rank borrows the last SIEVE_HALO rows of the rank above (one send/recv, no
+    rank borrows the last SIEVE_HALO (256) rows of the rank above (one send/recv, no
     dependence on any kernel) and solves (halo, local rows) alone; the ranks
     all-reduce(max) their [key, status].  When any rank's sieve could not
     decide, all ranks run the band protocol below, now and for later solves."""
@@ -185,18 +186,21 @@ class RowBandSolver:
         self._ks = None
         self._src = None
         self._halo = None
-        self.sieve = bool(getattr(backend, "is_sieve", False)) and min(self.rank_rows) >= SIEVE_HALO
+        self.halo_rows = int(getattr(backend, "halo_rows", SIEVE_HALO))
+        # a rank that finds no 7x7 block square has nothing above 8 * 6 + 14 cells
+        self.sieve_low_max = int(getattr(backend, "sieve_low_max", SIEVE_LOW_MAX))
+        self.sieve = bool(getattr(backend, "is_sieve", False)) and min(self.rank_rows) >= self.halo_rows
         self.sieve_retries = 0
 
     def _exchange_halo(self, src):
-        """Rank r receives the last SIEVE_HALO rows of rank r-1."""
+        """Rank r receives the last halo_rows rows of rank r-1."""
         import torch.distributed as dist
         be = self.backend
         if self.rank > 0 and self._halo is None:
-            self._halo = be.new_halo_buffer(SIEVE_HALO, src)
+            self._halo = be.new_halo_buffer(self.halo_rows, src)
         ops = []
         if self.rank + 1 < self.world:
-            ops.append(dist.P2POp(dist.isend, src[-SIEVE_HALO:], self.rank + 1, group=self.group))
+            ops.append(dist.P2POp(dist.isend, src[-self.halo_rows:], self.rank + 1, group=self.group))
         if self.rank > 0:
             ops.append(dist.P2POp(dist.irecv, self._halo, self.rank - 1, group=self.group))
         for req in dist.batch_isend_irecv(ops):
@@ -240,14 +244,15 @@ class RowBandSolver:
 
     def result(self) -> SquareResult:
         ks = (self._ks if self._ks is not None else self.backend.key_status()).cpu().numpy().astype(np.int64)
-        if self.sieve and int(ks[1]) == 2:
+        undecided = int(ks[1]) == 2 or (int(ks[1]) == 1 and (int(ks[0]) >> (2 * KEY_DIM_BITS)) <= self.sieve_low_max)
+        if self.sieve and undecided:
             # some rank's sieve could not decide (every rank sees the same reduced
             # status): the band protocol, for this solve and the following ones
             self.sieve = False
             self.sieve_retries += 1
             self.launch(self._src)
             return self.result()
-        return decode_key(int(ks[0]), int(ks[1]), self.rows, self.cols)
+        return decode_key(int(ks[0]), int(ks[1]) if int(ks[1]) == 3 else 0, self.rows, self.cols)
 
     def solve(self, src) -> SquareResult:
         self.launch(src)

@@ -149,7 +149,7 @@ class Solver:
 
     def result(self) -> list[SquareResult]:
         host = self.res.cpu().numpy()
-        if int(self.plan.engine) == N.ENGINE_SIEVE and (int(host[16]) & 2):
+        if int(self.plan.engine) == N.ENGINE_SIEVE and (int(host[16]) & 6):
             # the sieve engine could not decide this input (answer outside 56..222 or
             # too many candidates): the same plan runs the band engine, from now on
             self.sieve_retries = getattr(self, "sieve_retries", 0) + 1

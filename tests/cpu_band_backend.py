@@ -79,3 +79,48 @@ class CpuBandBackend:
 
     def key_status(self):
         return torch.tensor([max(self.key1, self.keyfix), 0], dtype=torch.int64)
+
+
+class CpuSieveBackend(CpuBandBackend):
+    """The sieve protocol's per-rank step (msq_rank_sieve) restated on the
+    oracle: Algorithm 1 over (halo rows, local rows); decided when the answer is
+    in [lo, hi] with hi <= halo_rows (the real engine: 56..222 with a 256-row
+    halo), otherwise status 2 and the solver falls back to the band protocol."""
+    is_sieve = True
+
+    def __init__(self, local, fmt, cols, row_base, nbands, halo_rows=16, lo=4, hi=16):
+        super().__init__(local, fmt, cols, row_base, nbands)
+        self.halo_rows, self.lo, self.hi = halo_rows, lo, hi
+        self.sieve_low_max = lo - 1
+        self._sieve_ks = None
+        self.sieve_calls = 0
+
+    def new_halo_buffer(self, rows, like):
+        return torch.zeros((rows,) + tuple(like.shape[1:]), dtype=like.dtype)
+
+    def _cells(self, a):
+        a = np.ascontiguousarray(a)
+        if self.fmt == 0:
+            return a.astype(np.uint8)
+        w = a.view(np.uint32)
+        bits = ((w[:, :, None] >> np.arange(32, dtype=np.uint32)) & 1).astype(np.uint8)
+        return bits.reshape(w.shape[0], -1)[:, :self.cols]
+
+    def sieve(self, src, halo=None):
+        self.sieve_calls += 1
+        parts = ([self._cells(halo.numpy())] if halo is not None else []) + [self._cells(self.local)]
+        a = np.concatenate(parts, axis=0)
+        r = oracle.freq(a)
+        base = self.row_base - (a.shape[0] - self.rows)
+        if self.lo <= r.side <= self.hi:
+            key = oracle.pack_key(r.side, base + r.top + r.side - 1, r.left + r.side - 1)
+            self._sieve_ks = torch.tensor([key, 0], dtype=torch.int64)
+        else:  # too large: undecided; too small: nothing above lo - 1 in these rows
+            self._sieve_ks = torch.tensor([0, 2 if r.side > self.hi else 1], dtype=torch.int64)
+
+    def pass1(self, src):
+        self._sieve_ks = None
+        super().pass1(src)
+
+    def key_status(self):
+        return self._sieve_ks.clone() if self._sieve_ks is not None else super().key_status()

@@ -77,10 +77,38 @@ def test_engine_selection(lib):
     p = N.plan(N.FMT_U8, 1, 512, 512, 512)                              # cfg1
     assert p.engine == 1 and p.nbands > 1 and p.ws_bytes > 0
     assert N.plan(N.FMT_U8, 1, 100, 64, 64).engine == 1                 # one band, one team
-    assert N.plan(N.FMT_BITS, 1, 65536, 65536, 2048).engine == 0        # cfg4: band engine (+ strip pass)
+    p4 = N.plan(N.FMT_BITS, 1, 65536, 65536, 2048)                      # cfg4: sieve engine first
+    assert p4.engine == 2 and p4.sv_bands >= 1 and p4.ws_bytes > p4.sv_ws_off > 0
+    assert N.plan(N.FMT_BITS, 1, 65536, 65536, 2048, engine=0).engine == 0
+    assert N.plan(N.FMT_BITS, 1, 65536, 65536, 2048, deterministic=True).engine == 0
+    assert N.plan(N.FMT_BITS, 1, 2048, 65536, 2048).engine == 0         # below 4096 rows: band engine
+    assert N.plan(N.FMT_BITS, 1, 700, 768, 24, engine=2).engine == 2    # any shape the sieve can stream
+    assert N.plan(N.FMT_BITS, 1, 700, 800, 28, engine=2).engine == 2    # 25 words in a 16-byte-multiple stride
+    with pytest.raises(ValueError):
+        N.plan(N.FMT_BITS, 1, 700, 800, 25, engine=2)                   # stride of 25 words: not 16-byte rows
+    with pytest.raises(ValueError):
+        N.plan(N.FMT_U8, 1, 4096, 4096, 4096, engine=2)                 # bit-packed only
     assert N.plan(N.FMT_U8, 1, 512, 512, 512, nbands=4).engine == 0     # explicit bands
     assert N.plan(N.FMT_U8, 1, 512, 2048, 2048).engine == 0             # wider than 1024
     assert N.plan(N.FMT_U8, 3, 4000, 64, 64).engine == 0                # batch rows > 2040
+
+
+def test_sieve_entry_points_reject_bad_arguments(lib):
+    p = N.plan(N.FMT_BITS, 1, 4096, 4096, 128)
+    assert p.engine == 2
+    band = N.plan(N.FMT_BITS, 1, 4096, 4096, 128, engine=0)
+    ptr = ctypes.c_void_p(4096)  # aligned, never dereferenced: every check fails first
+    for fn in (lib.msq_rank_sieve, lib.msq_rank_sieve_pass, lib.msq_rank_sieve_finish):
+        assert fn(None, ptr, None, 0, 0, ptr, ptr, None) == N.MSQ_EINVAL
+        assert fn(ctypes.byref(band), ptr, None, 0, 0, ptr, ptr, None) == N.MSQ_EINVAL      # not a sieve plan
+        assert fn(ctypes.byref(p), None, None, 0, 0, ptr, ptr, None) == N.MSQ_EINVAL
+        assert fn(ctypes.byref(p), ctypes.c_void_p(4100), None, 0, 0, ptr, ptr, None) == N.MSQ_EINVAL  # misaligned
+        assert fn(ctypes.byref(p), ptr, None, 256, 128, ptr, ptr, None) == N.MSQ_EINVAL     # halo rows, no halo
+        assert fn(ctypes.byref(p), ptr, ptr, 12, 128, ptr, ptr, None) == N.MSQ_EINVAL       # not a multiple of 8
+        assert fn(ctypes.byref(p), ptr, ptr, 512, 128, ptr, ptr, None) == N.MSQ_EINVAL      # more than 256
+        assert fn(ctypes.byref(p), ptr, ptr, 256, 64, ptr, ptr, None) == N.MSQ_EINVAL       # halo stride < words
+        assert fn(ctypes.byref(p), ptr, ptr, 256, 128, ptr, ptr, None) == N.MSQ_EINVAL      # row_base 0 with a halo
+    assert lib.msq_strerror(N.MSQ_EAGAIN).decode().startswith("the sieve engine could not decide")
 
 
 def test_new_entry_points_reject_bad_arguments(lib):

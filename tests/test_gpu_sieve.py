@@ -1,0 +1,210 @@
+"""Sieve engine (csrc/msq_sieve.cuh, plan.engine == 2) against the oracle.
+
+The engine streams the bit-packed matrix once into a bitmap of all-ones 8x8
+blocks, runs Algorithm 1 (reference squares.py:84-103) on that bitmap and then
+exactly on the cell windows of its few candidates.  It must either return the
+reference's answer (side and the implied location) or say it cannot decide
+(status bits 1/2 -> MSQ_EAGAIN), in which case the same plan runs the band
+engine.  Covered: random sparse-zero matrices with planted squares around the
+decidable range 56..222, every alignment of a square against the 8-cell grid,
+squares on the matrix borders, ties (first in row-major order of the bottom-right
+cell), ragged widths and strides, undecided inputs, and row slices with the
+256-row halo (the multi-GPU protocol on virtual ranks).
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2503_18974_b200 import _native as N
+from paper_2503_18974_b200 import grid
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    from paper_2503_18974_b200 import build
+    build.build()
+    oracle.build()
+    return t
+
+
+def _same(got, want):
+    assert (got.side, got.area, got.top, got.left) == (want.side, want.area, want.top, want.left), (got, want)
+
+
+def _solve(torch, a, engine=2, ld=None):
+    from paper_2503_18974_b200.squares import Solver
+    rows, cols = a.shape
+    w = grid.pack_bits(a)
+    if ld is None and w.shape[1] % 4:
+        ld = (w.shape[1] + 3) // 4 * 4  # the sieve streams rows in 16-byte units
+    if ld is not None:
+        pad = np.zeros((rows, ld), np.uint32)
+        pad[:, :w.shape[1]] = w
+        pad[:, w.shape[1]:] = 0xDEADBEEF  # never read as cells
+        w = pad
+    s = Solver(N.FMT_BITS, rows, cols, ld=w.shape[1], engine=engine)
+    got = s.solve(torch.from_numpy(w.view(np.int32)).cuda())[0]
+    return got, getattr(s, "sieve_retries", 0)
+
+
+def test_random_sparse_matrices(torch):
+    rng = np.random.default_rng(7)
+    decided = 0
+    for it in range(48):
+        rows = int(rng.integers(64, 2600))
+        cols = max(64, 128 * int(rng.integers(1, 28)) - int(rng.choice([0, 0, 5, 31, 64, 95])))
+        p = [0.999, 0.9995, 0.998, 0.9999, 0.995][it % 5]
+        a = (rng.random((rows, cols)) < p).astype(np.uint8)
+        k = int(rng.integers(40, 250))
+        if it % 4 != 3 and min(rows, cols) > k:
+            top, left = int(rng.integers(0, rows - k + 1)), int(rng.integers(0, cols - k + 1))
+            a[top:top + k, left:left + k] = 1
+        got, retried = _solve(torch, a)
+        _same(got, oracle.freq(a))
+        decided += 0 if retried else 1
+    assert decided >= 24  # most of these are the sieve's own answers, not the fall-back's
+
+
+@pytest.mark.parametrize("side", [55, 56, 57, 63, 64, 65, 133, 221, 222, 223, 229])
+def test_every_alignment_of_a_planted_square(torch, side):
+    """A square of the given side at every offset mod 8 in both directions over a
+    background whose own squares stay far below it."""
+    rng = np.random.default_rng(side)
+    rows, cols = 700, 768
+    base = (rng.random((rows, cols)) < 0.97).astype(np.uint8)
+    for dr in range(8):
+        for dc in (dr, (3 * dr + 5) % 8):
+            a = base.copy()
+            top, left = 200 + dr, 264 + dc
+            a[top:top + side, left:left + side] = 1
+            if top + side < rows:
+                a[top + side, left:left + side:7] = 0  # the square is exactly this tall
+            if left + side < cols:
+                a[top:top + side:5, left + side] = 0
+            a[top - 1, left:left + side:6] = 0
+            a[top:top + side:6, left - 1] = 0
+            got, _ = _solve(torch, a)
+            _same(got, oracle.freq(a))
+            assert got.side == side
+
+
+def test_squares_on_the_borders_and_ties(torch):
+    rows, cols = 1000, 1152
+    rng = np.random.default_rng(11)
+    base = (rng.random((rows, cols)) < 0.98).astype(np.uint8)
+    k = 100
+    spots = [(0, 0), (0, cols - k), (rows - k, 0), (rows - k, cols - k), (3, cols - k - 2), (rows - k - 1, 5)]
+    for top, left in spots:
+        a = base.copy()
+        a[top:top + k, left:left + k] = 1
+        got, _ = _solve(torch, a)
+        _same(got, oracle.freq(a))
+    # several maximal squares: the first bottom-right cell in row-major order wins
+    a = base.copy()
+    for top, left in [(500, 700), (500, 100), (493, 400), (120, 900), (121, 30)]:
+        a[top:top + k, left:left + k] = 1
+    got, _ = _solve(torch, a)
+    want = oracle.freq(a)
+    _same(got, want)
+    assert got.side >= k
+
+
+def test_strided_rows_and_heights_not_multiples_of_eight(torch):
+    rng = np.random.default_rng(12)
+    for rows, cols, ld in [(777, 1000, 36), (1501, 2017, 64), (95, 128, 8), (64, 3000, 96), (900, 1100, 36)]:
+        a = (rng.random((rows, cols)) < 0.999).astype(np.uint8)
+        k = min(rows, 150)
+        top = rows - k  # ends in the last (partial) block row
+        a[top:top + k, cols - k:cols] = 1
+        got, _ = _solve(torch, a, ld=ld)
+        _same(got, oracle.freq(a))
+
+
+def test_undecided_inputs_fall_back_to_the_band_engine(torch):
+    from paper_2503_18974_b200.squares import Solver
+    rng = np.random.default_rng(13)
+    rows, cols = 1200, 1280
+    cases = {
+        "dense zeros": (rng.random((rows, cols)) < 0.9).astype(np.uint8),
+        "all ones": np.ones((rows, cols), np.uint8),
+        "all zeros": np.zeros((rows, cols), np.uint8),
+    }
+    big = (rng.random((rows, cols)) < 0.999).astype(np.uint8)
+    big[100:500, 300:700] = 1
+    cases["planted 400"] = big
+    stripes = np.ones((3072, 3072), np.uint8)
+    stripes[:, ::64] = 0  # 2304 maximal squares of side 63: the candidate list overflows
+    stripes[::64, :] = 0
+    cases["grid of 63-squares"] = stripes
+    lib = N.load()
+    for name, a in cases.items():
+        rows, cols = a.shape
+        want = oracle.freq(a)
+        got, retried = _solve(torch, a)
+        _same(got, want)
+        assert retried == 1, name
+        # the C ABI says so itself: msq_decode of the undecided launch is MSQ_EAGAIN
+        s = Solver(N.FMT_BITS, rows, cols, engine=2)
+        w = torch.from_numpy(grid.pack_bits(a).view(np.int32)).cuda()
+        s.launch(w)
+        host = s.res.cpu().numpy()
+        block = N.MsqDevResult.from_buffer_copy(host[:32].tobytes())
+        out = N.MsqResult()
+        assert lib.msq_decode(ctypes.byref(block), rows, cols, ctypes.byref(out)) == N.MSQ_EAGAIN, name
+        assert block.status & 6
+        # and the synchronous call retries on its own
+        from paper_2503_18974_b200.squares import freq_square_bits
+        _same(freq_square_bits(w, cols), want)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_slices_with_halo(torch, world):
+    """The multi-GPU sieve protocol on virtual ranks: every rank solves (the last
+    256 rows of the rank above, its own rows) alone; the max of the keys is the
+    whole matrix's answer, also for squares that cross a rank boundary."""
+    from paper_2503_18974_b200.distributed import SIEVE_HALO, GpuBackend, decode_key, slice_rows
+    rng = np.random.default_rng(200 + world)
+    for it in range(4):
+        rows, cols = world * 1024 + 8 * int(rng.integers(0, 40)), 4096
+        a = (rng.random((rows, cols)) < 0.9992).astype(np.uint8)
+        k = int(rng.integers(90, 215))
+        bound = slice_rows(rows, world, 1)[0]
+        top = [bound - k // 2, bound - k + 1, bound - 1, bound - k - 3][it]
+        left = int(rng.integers(0, cols - k))
+        a[top:top + k, left:left + k] = 1
+        full = grid.pack_bits(a).view(np.int32)
+        keys = []
+        for q in range(world):
+            r0, n = slice_rows(rows, world, q)
+            src = torch.from_numpy(np.ascontiguousarray(full[r0:r0 + n])).cuda()
+            halo = torch.from_numpy(np.ascontiguousarray(full[r0 - SIEVE_HALO:r0])).cuda() if q > 0 else None
+            be = GpuBackend(N.FMT_BITS, n, cols, r0, engine=2)
+            assert be.is_sieve
+            be.sieve(src, halo)
+            keys.append(be.key_status().clone())
+        ks = torch.stack(keys).max(dim=0).values.cpu().numpy()
+        assert int(ks[1]) in (0, 1), (ks, [k.cpu().numpy() for k in keys])
+        _same(decode_key(int(ks[0]), 0, rows, cols), oracle.freq(a))
+
+
+def test_row_band_solver_single_rank_uses_the_sieve(torch):
+    from paper_2503_18974_b200.distributed import GpuBackend, RowBandSolver
+    rng = np.random.default_rng(14)
+    rows, cols = 4096, 4096
+    a = (rng.random((rows, cols)) < 0.999).astype(np.uint8)
+    a[1000:1150, 2000:2150] = 1
+    w = torch.from_numpy(grid.pack_bits(a).view(np.int32)).cuda()
+    be = GpuBackend(N.FMT_BITS, rows, cols, 0)
+    assert be.is_sieve  # automatic from 4096 x 4096
+    solver = RowBandSolver(rows, cols, 0, 1, be)
+    _same(solver.solve(w), oracle.freq(a))
+    assert solver.sieve and solver.sieve_retries == 0
+    a2 = (rng.random((rows, cols)) < 0.97).astype(np.uint8)  # squares far below 56: the band protocol
+    w2 = torch.from_numpy(grid.pack_bits(a2).view(np.int32)).cuda()
+    _same(solver.solve(w2), oracle.freq(a2))
+    assert not solver.sieve and solver.sieve_retries == 1
