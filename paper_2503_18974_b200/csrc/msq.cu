@@ -598,7 +598,7 @@ SieveGeom sieve_geom(int64_t rows, int64_t cols, int nbands_fixed) {
         off += (size_t)round_up((long long)bytes, 256);
         return o;
     };
-    g.ctl = take(sizeof(msq::SieveCtl));
+    g.ctl = take(sizeof(msq::SieveCtl) + msq::SV_PHASES * 4);  // + phase counters, zeroed together
     g.cand = take((size_t)msq::SV_CAP * 8);
     g.G = take((size_t)g.CR * g.CWn * 4);
     g.total = off;
@@ -632,6 +632,8 @@ msq::SieveParams make_sieve(const msq_plan* pl, const void* d_src, const void* d
     p.ctl = (msq::SieveCtl*)(w + g.ctl);
     p.cand = (unsigned long long*)(w + g.cand);
     p.G = (uint32_t*)(w + g.G);
+    p.pcnt = (int*)(w + g.ctl + sizeof(msq::SieveCtl));
+    p.ptarget = g.nbands * (int)ceil_div(round_up(pl->words, 4), 256);
     p.result = (unsigned char*)res;
     return p;
 }
@@ -649,7 +651,8 @@ bool sieve_args_ok(const msq_plan* pl, const void* d_src, const void* d_halo, in
 cudaError_t launch_sieve_pass(const msq_plan* pl, const msq::SieveParams& sp, cudaStream_t st) {
     const SieveGeom g = sieve_geom(sp.rows, sp.cols, pl->sv_bands);
     if (cudaMemsetAsync(sp.result, 0, sizeof(msq_devresult), st) != cudaSuccess) return cudaGetLastError();
-    if (cudaMemsetAsync(sp.ctl, 0, sizeof(msq::SieveCtl), st) != cudaSuccess) return cudaGetLastError();
+    if (cudaMemsetAsync(sp.ctl, 0, sizeof(msq::SieveCtl) + msq::SV_PHASES * 4, st) != cudaSuccess)
+        return cudaGetLastError();
     static bool attr_set[64] = {false};
     cudaError_t e = set_smem_attr(msq::sieve_pass_kernel, attr_set);
     if (e != cudaSuccess) return e;

@@ -27,8 +27,10 @@
 //                       column chunk, a warp per 1024 columns), ANDs each
 //                       8-row tile into G bits and stores G (1 bit per 64
 //                       cells: 8 MB for 65536^2).  Stateless, so any split of
-//                       the rows works and the kernel runs at the HBM rate.
-//   sieve_coarse_kernel Algorithm 1 on G (read from L2): block heights as 5
+//                       the rows works and the kernel runs at the HBM rate; the
+//                       CTAs cover the matrix a quarter at a time.
+//   sieve_coarse_kernel (runs beside the streaming pass, one quarter behind it)
+//                       Algorithm 1 on G (read from L2): block heights as 5
 //                       saturating bit-planes per lane (one 32-block word per
 //                       lane, lane 0 of a warp is the left halo), one level
 //                       test per block row -- "a run of >= l blocks of height
@@ -56,10 +58,11 @@ namespace msq {
 
 constexpr int SV_PL = 5;           // height planes: block heights saturate at 31
 constexpr int SV_EDGE = 31;        // block rows above a unit that warm its heights up (they saturate at 31)
-constexpr int SV_OWN = 32;         // block rows a coarse unit owns
+constexpr int SV_OWN = 16;         // block rows a coarse unit owns
+constexpr int SV_PHASES = 4;       // the streaming pass covers the matrix in this many sweeps (top quarter first, ...)
 constexpr int SV_DMAX = 26;        // windows of 8 * 26 + 21 = 229 columns (from column 2 mod 8) fit 8 words
 constexpr int SV_LMIN = 6;         // lowest level tested; the sieve decides for max D >= 7
-constexpr int SV_CAP = 8192;       // candidate list entries
+constexpr int SV_CAP = 32768;      // candidate list entries
 constexpr int SV_TR = 8;           // rows per tile = block height
 constexpr int SV_MAXSLOTS = 16;    // TMA ring depth
 constexpr int SV_HALO_ROWS = 256;  // rows a rank borrows from the rank above
@@ -86,6 +89,8 @@ struct SieveParams {
     int nbands, nchunks, wmax, nslots, slot_row_bytes;  // streaming pass: bands x chunks CTAs, wmax warps of 32 words
     int nunits;           // coarse pass: ceil(CR / SV_OWN) row units x WC warps
     uint32_t* G;          // [CR][CWn] block bitmap
+    int* pcnt;            // [SV_PHASES] streaming warps done with each phase (zeroed with ctl)
+    int ptarget;          // = CTAs' consumer warps in total: a phase is complete at this count
     unsigned long long* cand;  // [SV_CAP] D << 40 | block row << 16 | block column
     SieveCtl* ctl;
     unsigned char* result;
@@ -95,8 +100,16 @@ __device__ __forceinline__ const uint8_t* sv_row(const SieveParams& p, int r) {
     return r < p.halo_rows ? p.halo + (size_t)r * p.halo_ld_bytes
                            : p.src + (size_t)(r - p.halo_rows) * p.ld_bytes;
 }
-__device__ __forceinline__ int sv_band_cr0(const SieveParams& p, int band) {
-    return (int)(((long long)p.CR * band) / p.nbands);
+// Sub-band j of SV_PHASES * nbands covers block rows [sv_band_cr0(j), sv_band_cr0(j + 1));
+// CTA (band b) streams sub-bands b, nbands + b, 2 * nbands + b, ...: phase ph of the
+// pass is the ph-th quarter of the matrix, each CTA reading one contiguous piece of it.
+__device__ __forceinline__ int sv_band_cr0(const SieveParams& p, int j) {
+    return (int)(((long long)p.CR * j) / (SV_PHASES * p.nbands));
+}
+// the phase that produces block row R
+__device__ __forceinline__ int sv_phase_of(const SieveParams& p, int R) {
+    const long long nb = (long long)SV_PHASES * p.nbands;
+    return (int)((((long long)R + 1) * nb - 1) / p.CR) / p.nbands;
 }
 
 // bit c of the result: bits [c - m + 1, c] of the 64-bit (hi:lo) are all set (1 <= m <= 31)
@@ -182,7 +195,6 @@ __device__ __forceinline__ void sv_step(const SieveParams& p, uint32_t v, uint32
 #define MSQ_SV_BATCH 2
 #endif
 constexpr int SV_BATCH = MSQ_SV_BATCH;
-constexpr int SV_GROUP = 8;  // G rows a coarse unit keeps in flight
 struct SvBatch {
     uint32_t h0[SV_PL];    // heights before the batch
     uint32_t v[SV_BATCH];  // G words of its rows
@@ -271,11 +283,17 @@ __global__ void __launch_bounds__(288, 1) sieve_pass_kernel(const SieveParams p)
     const int WF = (Wp + 255) / 256;   // warp columns of 256 matrix words
     const int wc0 = WF * chunk / p.nchunks, wc1 = WF * (chunk + 1) / p.nchunks;
     const int ncw = wc1 - wc0;  // consumer warps of this chunk
-    // a contiguous band of block rows per CTA (interleaving the CTAs' tiles so that the
-    // bitmap fills top down -- to run the coarse pass beside this kernel -- cost 30% of
-    // the bandwidth: 89 -> 116 us on cfg4)
-    const int cr0 = sv_band_cr0(p, band);
-    const int ntiles = sv_band_cr0(p, band + 1) - cr0;
+    // SV_PHASES contiguous sub-bands per CTA, one per quarter of the matrix, so the
+    // bitmap of a quarter is complete while the next one streams and the coarse pass
+    // (launched beside this kernel) works on it.  (Interleaving single tiles instead
+    // cost 30% of the bandwidth: 89 -> 116 us on cfg4.)
+    int tiles_of[SV_PHASES], first_of[SV_PHASES], ntiles = 0;
+#pragma unroll
+    for (int ph = 0; ph < SV_PHASES; ++ph) {
+        first_of[ph] = sv_band_cr0(p, ph * p.nbands + band);
+        tiles_of[ph] = sv_band_cr0(p, ph * p.nbands + band + 1) - first_of[ph];
+        ntiles += tiles_of[ph];
+    }
     const int mw0 = 256 * wc0;  // matrix words [mw0, mw1) of each row
     const int mw1 = min(Wp, 256 * wc1);
     const uint32_t chunk_bytes = (uint32_t)(mw1 - mw0) * 4u;
@@ -293,24 +311,28 @@ __global__ void __launch_bounds__(288, 1) sieve_pass_kernel(const SieveParams p)
         fence_mbar_init();
     }
     __syncthreads();
-    if (ntiles <= 0 || ncw <= 0) return;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the coarse pass waits on the phase counters
+    if (ncw <= 0) return;
 
     // ------------------------------------------------------------ producer
     if (warp == p.wmax) {
         if (lane == 0) {
             const uint64_t pol = l2_evict_first_policy();
             int s = 0, lap = 0;
-            for (int q = 0; q < ntiles; ++q) {
-                if (lap > 0) mbar_wait(&empty[s], (uint32_t)((lap - 1) & 1));
-                mbar_expect_tx(&full[s], SV_TR * chunk_bytes);
-                uint8_t* dst = ring + (size_t)s * slot_bytes;
-                const int r = SV_TR * (cr0 + q);
+#pragma unroll 1
+            for (int ph = 0; ph < SV_PHASES; ++ph) {
+                for (int q = 0; q < tiles_of[ph]; ++q) {
+                    if (lap > 0) mbar_wait(&empty[s], (uint32_t)((lap - 1) & 1));
+                    mbar_expect_tx(&full[s], SV_TR * chunk_bytes);
+                    uint8_t* dst = ring + (size_t)s * slot_bytes;
+                    const int r = SV_TR * (first_of[ph] + q);
 #pragma unroll
-                for (int b = 0; b < SV_TR; ++b)
-                    tma_row(dst + (size_t)b * srb, sv_row(p, r + b) + (size_t)mw0 * 4, chunk_bytes, &full[s], pol);
-                if (++s == p.nslots) {
-                    s = 0;
-                    ++lap;
+                    for (int b = 0; b < SV_TR; ++b)
+                        tma_row(dst + (size_t)b * srb, sv_row(p, r + b) + (size_t)mw0 * 4, chunk_bytes, &full[s], pol);
+                    if (++s == p.nslots) {
+                        s = 0;
+                        ++lap;
+                    }
                 }
             }
         }
@@ -334,35 +356,41 @@ __global__ void __launch_bounds__(288, 1) sieve_pass_kernel(const SieveParams p)
     const uint32_t ring_s = smem_addr(ring);
     const uint32_t offA = okA ? (uint32_t)(8 * g + 4 * sw - mw0) * 4u : 0u;
     const uint32_t offB = okB ? (uint32_t)(8 * g + 4 * (1 - sw) - mw0) * 4u : 0u;
-    uint32_t* grow = p.G + (size_t)cr0 * p.CWn + (in ? g : 0);
-
     int s = 0;
     uint32_t par = 0u;
-    for (int q = 0; q < ntiles; ++q) {
-        mbar_wait(&full[s], par);
-        const uint32_t slot_s = ring_s + (uint32_t)s * slot_bytes;
-        uint32_t A[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
-        uint32_t B[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+#pragma unroll 1
+    for (int ph = 0; ph < SV_PHASES; ++ph) {
+        uint32_t* grow = p.G + (size_t)first_of[ph] * p.CWn + (in ? g : 0);
+        for (int q = 0; q < tiles_of[ph]; ++q) {
+            mbar_wait(&full[s], par);
+            const uint32_t slot_s = ring_s + (uint32_t)s * slot_bytes;
+            uint32_t A[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+            uint32_t B[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
 #pragma unroll
-        for (int b = 0; b < SV_TR; ++b) {
-            uint32_t wa[4], wb[4];
-            lds_words<4>(slot_s + (uint32_t)b * srb + offA, wa);
-            lds_words<4>(slot_s + (uint32_t)b * srb + offB, wb);
+            for (int b = 0; b < SV_TR; ++b) {
+                uint32_t wa[4], wb[4];
+                lds_words<4>(slot_s + (uint32_t)b * srb + offA, wa);
+                lds_words<4>(slot_s + (uint32_t)b * srb + offB, wb);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                A[k] &= wa[k];
-                B[k] &= wb[k];
+                for (int k = 0; k < 4; ++k) {
+                    A[k] &= wa[k];
+                    B[k] &= wb[k];
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            const uint32_t cA = okA ? sv_flags16(A) : 0u, cB = okB ? sv_flags16(B) : 0u;
+            const uint32_t v = (sw ? (cB | (cA << 16)) : (cA | (cB << 16))) & validc;
+            if (in) grow[(size_t)q * p.CWn] = v;
+            if (++s == p.nslots) {
+                s = 0;
+                par ^= 1u;
             }
         }
+        // this warp's words of the phase are out: release the phase counter
+        __threadfence();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        const uint32_t cA = okA ? sv_flags16(A) : 0u, cB = okB ? sv_flags16(B) : 0u;
-        const uint32_t v = (sw ? (cB | (cA << 16)) : (cA | (cB << 16))) & validc;
-        if (in) grow[(size_t)q * p.CWn] = v;
-        if (++s == p.nslots) {
-            s = 0;
-            par ^= 1u;
-        }
+        if (lane == 0) atomicAdd(p.pcnt + ph, 1);
     }
 }
 
@@ -373,8 +401,34 @@ __global__ void __launch_bounds__(288, 1) sieve_pass_kernel(const SieveParams p)
 // anything.  The first unit has no rows above it and walks its own first rows
 // for that bound, then starts again from zero heights.
 __global__ void __launch_bounds__(32 * SV_EWARPS) sieve_coarse_kernel(const SieveParams p) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // Launched beside sieve_pass_kernel (programmatic dependent launch without
+    // griddepcontrol.wait): the CTA starts when the phases that produce its units'
+    // block rows are complete (counters released by the streaming warps).
+    __shared__ int go;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    {
+        const int last_unit = min(blockIdx.x * SV_EWARPS + SV_EWARPS, p.nunits * p.WC) - 1;
+        const int last_row = min(p.CR, (last_unit / p.WC + 1) * SV_OWN) - 1;
+        if (threadIdx.x == 0) {
+            const int ph1 = sv_phase_of(p, last_row);
+            const volatile int* c = p.pcnt;
+            int ok = 1;
+            long long spins = 0;
+            for (int ph = 0; ph <= ph1 && ok; ++ph)
+                while (c[ph] < p.ptarget) {
+                    __nanosleep(1000);
+                    if (++spins > (1ll << 23)) {  // never in practice: hand the input to the band engine
+                        atomicOr(&p.ctl->abort, 2);
+                        ok = 0;
+                        break;
+                    }
+                }
+            __threadfence();
+            go = ok;
+        }
+        __syncthreads();
+        if (!go) return;
+    }
     const int unit = blockIdx.x * SV_EWARPS + warp;
     if (unit >= p.nunits * p.WC) return;
     const int ru = unit / p.WC, wc = unit - ru * p.WC;
@@ -385,29 +439,32 @@ __global__ void __launch_bounds__(32 * SV_EWARPS) sieve_coarse_kernel(const Siev
     const int Rw = ru > 0 ? R0 - SV_EDGE : 0;               // first warm-up row
     const int nwarm = ru > 0 ? SV_EDGE : min(SV_EDGE, R1);  // rows walked for heights only
     const uint32_t* gp = p.G + (in ? g : 0);
+    // every word the unit needs in flight at once: the warm-up rows (last first), its
+    // own rows, the control block
+    uint32_t c[SV_EDGE + 2], vv[SV_OWN];
+#pragma unroll
+    for (int k = 1; k <= SV_EDGE; ++k)
+        c[k] = (in && k <= nwarm) ? __ldcg(gp + (size_t)(Rw + nwarm - k) * p.CWn) : 0u;
+#pragma unroll
+    for (int j = 0; j < SV_OWN; ++j) vv[j] = (in && R0 + j < R1) ? __ldcg(gp + (size_t)(R0 + j) * p.CWn) : 0u;
+    const int gbest = ld_volatile(&p.ctl->best);
     if (ld_volatile(&p.ctl->abort)) return;
-    uint32_t h[SV_PL] = {0u, 0u, 0u, 0u, 0u};
-    // ---- warm-up: heights only, every row's word in flight at once.  c[k] =
-    // "the last k rows are ones" is monotone in k, so the height (how many k hold)
-    // has bit b set where c[m * 2^b] holds and c[(m + 1) * 2^b] does not, m odd.
-    {
-        uint32_t c[SV_EDGE + 2];
-        c[0] = 0xFFFFFFFFu;
+    // ---- warm-up: heights only.  c[k] = "the last k rows are ones" is monotone in k,
+    // so the height (how many k hold) has bit b set where c[m * 2^b] holds and
+    // c[(m + 1) * 2^b] does not, m odd.
+    uint32_t h[SV_PL];
+    c[0] = 0xFFFFFFFFu;
 #pragma unroll
-        for (int k = 1; k <= SV_EDGE; ++k)
-            c[k] = (in && k <= nwarm) ? __ldcg(gp + (size_t)(Rw + nwarm - k) * p.CWn) : 0u;
+    for (int k = 1; k <= SV_EDGE; ++k) c[k] &= c[k - 1];
+    c[SV_EDGE + 1] = 0u;
 #pragma unroll
-        for (int k = 1; k <= SV_EDGE; ++k) c[k] &= c[k - 1];
-        c[SV_EDGE + 1] = 0u;
+    for (int b = 0; b < SV_PL; ++b) {
+        uint32_t acc = 0u;
 #pragma unroll
-        for (int b = 0; b < SV_PL; ++b) {
-            uint32_t acc = 0u;
-#pragma unroll
-            for (int m = 1; (m << b) <= SV_EDGE; m += 2) acc |= c[m << b] & ~c[min((m + 1) << b, SV_EDGE + 1)];
-            h[b] = acc;
-        }
+        for (int m = 1; (m << b) <= SV_EDGE; m += 2) acc |= c[m << b] & ~c[min((m + 1) << b, SV_EDGE + 1)];
+        h[b] = acc;
     }
-    int lvl = max(SV_LMIN, ld_volatile(&p.ctl->best) - 1);
+    int lvl = max(SV_LMIN, gbest - 1);
     {   // one climb at the last warm-up row: a lower bound, nothing recorded
         uint32_t hits = sv_hits(h, lvl, lane);
         if (!own) hits = 0u;
@@ -421,24 +478,16 @@ __global__ void __launch_bounds__(32 * SV_EWARPS) sieve_coarse_kernel(const Siev
     SvBatch bt;
     bt.set_level(lvl);
     bt.begin(h);
-    // ---- own rows: SV_GROUP words in flight
-    for (int i0 = R0; i0 < R1; i0 += SV_GROUP) {
-        uint32_t vv[SV_GROUP];
+    // ---- own rows
 #pragma unroll
-        for (int j = 0; j < SV_GROUP; ++j)
-            vv[j] = (in && i0 + j < R1) ? __ldcg(gp + (size_t)(i0 + j) * p.CWn) : 0u;
-        const int gbest = ld_volatile(&p.ctl->best);
+    for (int part = 0; part < SV_OWN / SV_BATCH; ++part) {
+        const int r0 = R0 + part * SV_BATCH;
+        const int cnt = min(SV_BATCH, R1 - r0);
+        if (cnt > 0) {
 #pragma unroll
-        for (int part = 0; part < SV_GROUP / SV_BATCH; ++part) {
-            const int r0 = i0 + part * SV_BATCH;
-            const int cnt = min(SV_BATCH, R1 - r0);
-            if (cnt > 0) {
-#pragma unroll
-                for (int j = 0; j < SV_BATCH; ++j)
-                    if (j < cnt) bt.push(h, vv[part * SV_BATCH + j], j);
-                if (part == 0) lvl = max(lvl, gbest - 1);
-                sv_batch_end(p, bt, h, cnt, lvl, 0, r0, g, own, lane);
-            }
+            for (int j = 0; j < SV_BATCH; ++j)
+                if (j < cnt) bt.push(h, vv[part * SV_BATCH + j], j);
+            sv_batch_end(p, bt, h, cnt, lvl, 0, r0, g, own, lane);
         }
     }
 }

@@ -137,8 +137,8 @@ def test_undecided_inputs_fall_back_to_the_band_engine(torch):
     big = (rng.random((rows, cols)) < 0.999).astype(np.uint8)
     big[100:500, 300:700] = 1
     cases["planted 400"] = big
-    stripes = np.ones((3072, 3072), np.uint8)
-    stripes[:, ::64] = 0  # 2304 maximal squares of side 63: the candidate list overflows
+    stripes = np.ones((8192, 8192), np.uint8)
+    stripes[:, ::64] = 0  # 16384 maximal squares of side 63: the candidate list overflows
     stripes[::64, :] = 0
     cases["grid of 63-squares"] = stripes
     lib = N.load()
@@ -208,3 +208,30 @@ def test_row_band_solver_single_rank_uses_the_sieve(torch):
     w2 = torch.from_numpy(grid.pack_bits(a2).view(np.int32)).cuda()
     _same(solver.solve(w2), oracle.freq(a2))
     assert not solver.sieve and solver.sieve_retries == 1
+
+
+def test_workspace_is_not_overrun(torch):
+    """compute-sanitizer is closed on this GPU pool: a guard band behind the
+    plan's workspace (and around the result block) must survive a solve with the
+    largest halo, on a shape whose block bitmap ends exactly at the plan's size."""
+    from paper_2503_18974_b200.distributed import SIEVE_HALO, GpuBackend
+    rng = np.random.default_rng(15)
+    for rows, cols in [(1024, 4096), (1000, 2304), (4096, 8192)]:
+        a = (rng.random((rows + SIEVE_HALO, cols)) < 0.9993).astype(np.uint8)
+        a[200:340, 100:240] = 1
+        full = torch.from_numpy(grid.pack_bits(a).view(np.int32)).cuda()
+        be = GpuBackend(N.FMT_BITS, rows, cols, SIEVE_HALO, engine=2)
+        need, guard = int(be.plan.ws_bytes), 1 << 16
+        buf = torch.full((guard + need + guard,), 0x5A, dtype=torch.uint8, device="cuda")
+        be.ws = buf[guard:guard + need]
+        resbuf = torch.full((256 + 32 + 256,), 0x5A, dtype=torch.uint8, device="cuda")
+        be.res = resbuf[256:288]
+        be.sieve(full[SIEVE_HALO:], full[:SIEVE_HALO])
+        torch.cuda.synchronize()
+        assert bool((buf[:guard] == 0x5A).all()) and bool((buf[guard + need:] == 0x5A).all())
+        assert bool((resbuf[:256] == 0x5A).all()) and bool((resbuf[288:] == 0x5A).all())
+        from paper_2503_18974_b200.distributed import decode_key
+        ks = be.key_status().cpu().numpy()
+        want = oracle.freq(a)
+        got = decode_key(int(ks[0]), 0, rows + SIEVE_HALO, cols)
+        assert int(ks[1]) == 0 and (got.side, got.top, got.left) == (want.side, want.top, want.left)

@@ -8,6 +8,12 @@ msq_compose_carry -> msq_rank_fixup -> msq_rank_key_status), one rank after
 another, each phase timed with CUDA events.  Per-rank time = what one GPU of
 the N-GPU job spends on device work; the collectives (8 B all-reduce, cols*4 B
 all-gather, 16 B all-reduce) are not included.  Prints one JSON line per N.
+
+Bit-packed slices whose plan is a sieve plan (cfg4) take the sieve protocol
+instead, as RowBandSolver does: rank r gets the last 256 rows of rank r-1 (the
+halo send/recv, 2 MB, is not timed) and runs msq_rank_sieve_pass +
+msq_rank_sieve_finish over (halo, local rows); `rank_emulation.py cfg4 band`
+forces the band protocol for comparison.
 """
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -22,13 +28,44 @@ full = configs.cfg4_device() if cfg == "cfg4" else configs.cfg5_device()
 fmt = N.FMT_BITS if cfg == "cfg4" else N.FMT_U8
 rows, cols = spec["rows"], spec["cols"]
 REPS = 10
+FORCE_BAND = len(sys.argv) > 2 and sys.argv[2] == "band"
+HALO = 256
 for world in (1, 2, 4, 8):
     rank_rows = [slice_rows(rows, world, q)[1] for q in range(world)]
     bes, srcs = [], []
     for q in range(world):
         r0, n = slice_rows(rows, world, q)
         srcs.append(full[r0:r0 + n].contiguous())
-        bes.append(GpuBackend(fmt, n, cols, r0))
+        bes.append(GpuBackend(fmt, n, cols, r0, engine=0 if FORCE_BAND else -1))
+    if bes[0].is_sieve:
+        halos = [None] + [srcs[q - 1][-HALO:].contiguous() for q in range(1, world)]
+        ph = {q: {"sieve_pass": 0.0, "coarse+verify": 0.0} for q in range(world)}
+        for it in range(REPS + 2):
+            marks, keys = {}, []
+            for q, be in enumerate(bes):
+                a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+                c = torch.cuda.Event(enable_timing=True)
+                a.record(); be.sieve_pass(srcs[q], halos[q]); b.record(); be.sieve_finish(srcs[q], halos[q]); c.record()
+                keys.append(be.key_status().clone())
+                marks[q] = (a, b, c)
+            torch.cuda.synchronize()
+            if it >= 2:
+                for q in range(world):
+                    a, b, c = marks[q]
+                    ph[q]["sieve_pass"] += a.elapsed_time(b) / REPS
+                    ph[q]["coarse+verify"] += b.elapsed_time(c) / REPS
+        ks = torch.stack(keys).max(dim=0).values.cpu().numpy()
+        r = decode_key(int(ks[0]), 0, rows, cols)
+        per_rank = [sum(ph[q].values()) for q in range(world)]
+        slowest = max(per_rank)
+        print(json.dumps({"config": cfg, "protocol": "sieve", "world": world, "rows_per_rank": rank_rows[0],
+                          "halo_rows": HALO if world > 1 else 0, "status": int(ks[1]),
+                          "per_rank_ms": [round(x, 4) for x in per_rank],
+                          "phases_ms_rank0": {k: round(v, 4) for k, v in ph[0].items()},
+                          "phases_ms_last": {k: round(v, 4) for k, v in ph[world - 1].items()},
+                          "projected_gcells_s": round(rows * cols / (slowest * 1e-3) / 1e9, 1),
+                          "answer": [r.side, r.top, r.left]}), flush=True)
+        continue
     gathered = torch.empty((world, cols), dtype=torch.int32, device="cuda")
     phases = {q: {"seed": 0.0, "band_pass": 0.0, "summary": 0.0, "compose+carry+fixup": 0.0} for q in range(world)}
 
