@@ -59,6 +59,7 @@ class GpuBackend:
         words = (cols + 31) // 32
         ld = ld if ld is not None else (cols if fmt == N.FMT_U8 else words)
         self.plan = N.plan(fmt, 1, local_rows, cols, ld, nbands, engine=engine)
+        self.sieve_min_rows = 4096 if engine == -1 else 0  # msq_plan_make's automatic choice
         self.plan.row_base = row_base
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.ws = torch.empty(max(int(self.plan.ws_bytes), 256), dtype=torch.uint8, device=dev)
@@ -189,7 +190,10 @@ class RowBandSolver:
         self.halo_rows = int(getattr(backend, "halo_rows", SIEVE_HALO))
         # a rank that finds no 7x7 block square has nothing above 8 * 6 + 14 cells
         self.sieve_low_max = int(getattr(backend, "sieve_low_max", SIEVE_LOW_MAX))
-        self.sieve = bool(getattr(backend, "is_sieve", False)) and min(self.rank_rows) >= self.halo_rows
+        # every rank must take the same protocol: the automatic plan picks the sieve from
+        # 4096 local rows on, so slices on both sides of that line all take the bands
+        self.sieve = (bool(getattr(backend, "is_sieve", False)) and min(self.rank_rows) >= self.halo_rows and
+                      min(self.rank_rows) >= int(getattr(backend, "sieve_min_rows", 0)))
         self.sieve_retries = 0
 
     def _exchange_halo(self, src):

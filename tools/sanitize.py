@@ -35,6 +35,17 @@ g = Solver(N.FMT_BITS, 1600, 8192, nbands=10, test_floor=120).solve(src)[0]
 checks.append(("strip_bits", (g.side, g.top, g.left) == (wb.side, wb.top, wb.left)))
 g = Solver(N.FMT_BITS, 1600, 8192, nbands=10, flags=N.PLAN_CLIMB_FIXUP).solve(src)[0]
 checks.append(("pass1_bits_climb", (g.side, g.top, g.left) == (wb.side, wb.top, wb.left)))
+# sieve engine (streaming pass, coarse pass beside it, verifier) incl. a halo and an undecided input
+sv = (rng.random((1300, 4096)) < 0.9993).astype(np.uint8)
+sv[640:790, 1000:1150] = 1
+wsv = oracle.freq(sv)
+g = Solver(N.FMT_BITS, 1300, 4096, engine=2).solve(torch.from_numpy(grid.pack_bits(sv).view(np.int32)).cuda())[0]
+checks.append(("sieve", (g.side, g.top, g.left) == (wsv.side, wsv.top, wsv.left)))
+dense = (rng.random((1300, 4096)) < 0.95).astype(np.uint8)
+wd = oracle.freq(dense)
+sd = Solver(N.FMT_BITS, 1300, 4096, engine=2)
+g = sd.solve(torch.from_numpy(grid.pack_bits(dense).view(np.int32)).cuda())[0]
+checks.append(("sieve_undecided_retry", (g.side, g.top, g.left) == (wd.side, wd.top, wd.left) and sd.sieve_retries == 1))
 # team engine row-band mode (single matrix, <= 1024 columns)
 c = (rng.random((2000, 1000)) < 0.9).astype(np.uint8)
 wc = oracle.freq(c)
