@@ -629,6 +629,7 @@ msq::SieveParams make_sieve(const msq_plan* pl, const void* d_src, const void* d
     p.nslots = g.nslots;
     p.slot_row_bytes = g.slot_row_bytes;
     p.nunits = g.nunits;
+    p.coarse_warps = (int)ceil_div((long long)g.nunits * g.WC, msq::SV_EWARPS) * msq::SV_EWARPS;
     p.ctl = (msq::SieveCtl*)(w + g.ctl);
     p.cand = (unsigned long long*)(w + g.cand);
     p.G = (uint32_t*)(w + g.G);
@@ -650,8 +651,9 @@ bool sieve_args_ok(const msq_plan* pl, const void* d_src, const void* d_halo, in
 // memsets + the streaming pass
 cudaError_t launch_sieve_pass(const msq_plan* pl, const msq::SieveParams& sp, cudaStream_t st) {
     const SieveGeom g = sieve_geom(sp.rows, sp.cols, pl->sv_bands);
-    if (cudaMemsetAsync(sp.result, 0, sizeof(msq_devresult), st) != cudaSuccess) return cudaGetLastError();
-    if (cudaMemsetAsync(sp.ctl, 0, sizeof(msq::SieveCtl) + msq::SV_PHASES * 4, st) != cudaSuccess)
+    // one memset: control block, phase counters and the candidate list behind them
+    // (the result block is zeroed by the streaming pass itself)
+    if (cudaMemsetAsync(sp.ctl, 0, g.cand - g.ctl + (size_t)msq::SV_CAP * 8, st) != cudaSuccess)
         return cudaGetLastError();
     static bool attr_set[64] = {false};
     cudaError_t e = set_smem_attr(msq::sieve_pass_kernel, attr_set);

@@ -74,7 +74,7 @@ struct SieveCtl {
     int best;   // largest D found so far
     int count;  // candidates appended
     int abort;  // bit 0: D beyond SV_DMAX, bit 1: candidate list overflow
-    int pad;
+    int done;   // coarse-pass warps that have finished (the verifier's cue that the list is final)
 };
 
 struct SieveParams {
@@ -89,6 +89,7 @@ struct SieveParams {
     int nbands, nchunks, wmax, nslots, slot_row_bytes;  // streaming pass: bands x chunks CTAs, wmax warps of 32 words
     int nunits;           // coarse pass: ceil(CR / SV_OWN) row units x WC warps
     uint32_t* G;          // [CR][CWn] block bitmap
+    int coarse_warps;     // warps of sieve_coarse_kernel's grid: ctl->done ends there
     int* pcnt;            // [SV_PHASES] streaming warps done with each phase (zeroed with ctl)
     int ptarget;          // = CTAs' consumer warps in total: a phase is complete at this count
     unsigned long long* cand;  // [SV_CAP] D << 40 | block row << 16 | block column
@@ -137,9 +138,9 @@ __device__ __forceinline__ void sv_emit(const SieveParams& p, uint32_t mask, int
         const int j = __ffs(mask) - 1;
         mask &= mask - 1;
         const int idx = atomicAdd(&p.ctl->count, 1);
-        if (idx < SV_CAP)
-            p.cand[idx] = ((unsigned long long)D << 40) | ((unsigned long long)R << 16) |
-                          (unsigned long long)(32 * g + j);
+        if (idx < SV_CAP)  // entries are nonzero; the verifier waits for a reserved slot to fill
+            *(volatile unsigned long long*)(p.cand + idx) =
+                ((unsigned long long)D << 40) | ((unsigned long long)R << 16) | (unsigned long long)(32 * g + j);
         else
             atomicOr(&p.ctl->abort, 2);
     }
@@ -310,6 +311,7 @@ __global__ void __launch_bounds__(288, 1) sieve_pass_kernel(const SieveParams p)
         }
         fence_mbar_init();
     }
+    if (blockIdx.x == 0 && tid < 8) ((uint32_t*)p.result)[tid] = 0u;  // written again by the verifier only
     __syncthreads();
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the coarse pass waits on the phase counters
     if (ncw <= 0) return;
@@ -400,36 +402,7 @@ __global__ void __launch_bounds__(288, 1) sieve_pass_kernel(const SieveParams p)
 // gives the unit a local lower bound for the shared best before it records
 // anything.  The first unit has no rows above it and walks its own first rows
 // for that bound, then starts again from zero heights.
-__global__ void __launch_bounds__(32 * SV_EWARPS) sieve_coarse_kernel(const SieveParams p) {
-    // Launched beside sieve_pass_kernel (programmatic dependent launch without
-    // griddepcontrol.wait): the CTA starts when the phases that produce its units'
-    // block rows are complete (counters released by the streaming warps).
-    __shared__ int go;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    {
-        const int last_unit = min(blockIdx.x * SV_EWARPS + SV_EWARPS, p.nunits * p.WC) - 1;
-        const int last_row = min(p.CR, (last_unit / p.WC + 1) * SV_OWN) - 1;
-        if (threadIdx.x == 0) {
-            const int ph1 = sv_phase_of(p, last_row);
-            const volatile int* c = p.pcnt;
-            int ok = 1;
-            long long spins = 0;
-            for (int ph = 0; ph <= ph1 && ok; ++ph)
-                while (c[ph] < p.ptarget) {
-                    __nanosleep(1000);
-                    if (++spins > (1ll << 23)) {  // never in practice: hand the input to the band engine
-                        atomicOr(&p.ctl->abort, 2);
-                        ok = 0;
-                        break;
-                    }
-                }
-            __threadfence();
-            go = ok;
-        }
-        __syncthreads();
-        if (!go) return;
-    }
-    const int unit = blockIdx.x * SV_EWARPS + warp;
+__device__ __forceinline__ void sv_coarse_unit(const SieveParams& p, int unit, int lane) {
     if (unit >= p.nunits * p.WC) return;
     const int ru = unit / p.WC, wc = unit - ru * p.WC;
     const int g = 31 * wc - 1 + lane;
@@ -492,132 +465,194 @@ __global__ void __launch_bounds__(32 * SV_EWARPS) sieve_coarse_kernel(const Siev
     }
 }
 
+__global__ void __launch_bounds__(32 * SV_EWARPS) sieve_coarse_kernel(const SieveParams p) {
+    // Launched beside sieve_pass_kernel (programmatic dependent launch without
+    // griddepcontrol.wait): the CTA starts when the phases that produce its units'
+    // block rows are complete (counters released by the streaming warps).
+    __shared__ int go;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // the verifier's CTAs launch once every CTA of this grid has started and take the
+    // candidates while the last units still run
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    {
+        const int last_unit = min(blockIdx.x * SV_EWARPS + SV_EWARPS, p.nunits * p.WC) - 1;
+        const int last_row = min(p.CR, (last_unit / p.WC + 1) * SV_OWN) - 1;
+        if (threadIdx.x == 0) {
+            const int ph1 = sv_phase_of(p, last_row);
+            const volatile int* c = p.pcnt;
+            int ok = 1;
+            long long spins = 0;
+            for (int ph = 0; ph <= ph1 && ok; ++ph)
+                while (c[ph] < p.ptarget) {
+                    __nanosleep(1000);
+                    if (++spins > (1ll << 23)) {  // never in practice: hand the input to the band engine
+                        atomicOr(&p.ctl->abort, 2);
+                        ok = 0;
+                        break;
+                    }
+                }
+            __threadfence();
+            go = ok;
+        }
+        __syncthreads();
+    }
+    if (go) sv_coarse_unit(p, blockIdx.x * SV_EWARPS + warp, lane);
+    __threadfence();  // this warp's candidates before its count in ctl->done
+    __syncwarp();
+    if (lane == 0) atomicAdd(&p.ctl->done, 1);
+}
+
 // Algorithm 1 on the cell window of every candidate that can still hold the
-// answer; one CTA per candidate.  All threads load the window (every load in
-// flight at once) and fold the zeros of the rows before the first testable row
-// into per-column last-zero rows.  Every warp then walks the remaining rows
-// (heights from the last-zero rows) and tests every SV_VWARPS-th of them: at the
-// best side so far (a tie), then upwards until the row's own largest square is
-// known.  The largest key -- side, then first bottom row, then leftmost column
-// -- is Algorithm 1's answer for the window (squares.py:93-97).
+// answer; one CTA per candidate.  The grid is launched while the coarse pass
+// still runs (programmatic dependent launch, no griddepcontrol.wait): CTA b takes
+// list entries b, b + CTAs, ... as they appear and leaves when every coarse warp
+// has finished (ctl->done) and its entries are used up.  A candidate is skipped
+// when the shared best D or the best side so far already rule it out (both only
+// grow).  All threads load the window (every load in flight at once) and fold
+// the zeros of the rows before the first testable row into per-column last-zero
+// rows.  Every warp then walks the remaining rows (heights from the last-zero
+// rows) and tests every SV_VWARPS-th of them: at the best side so far (a tie),
+// then upwards until the row's own largest square is known.  The largest key --
+// side, then first bottom row, then leftmost column -- is Algorithm 1's answer
+// for the window (squares.py:93-97).
 __global__ void __launch_bounds__(32 * SV_VWARPS) sieve_verify_kernel(const SieveParams p) {
     __shared__ __align__(16) uint32_t rowsm[SV_VROWS][8];
     __shared__ int lzs[256];
     __shared__ int tsh;                   // best side so far (this window or any other)
     __shared__ unsigned long long keysh;  // best key of this window
+    __shared__ unsigned long long csh;    // the candidate being worked on (0: none, 1: leave)
+    __shared__ int bsh;                   // shared best D when it was taken
     constexpr int NT = 32 * SV_VWARPS;
     constexpr int LPT = (SV_VROWS * 8 + NT - 1) / NT;  // window words per thread
-    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // the control block, this CTA's first candidate and the best side so far: one round trip
-    const int best = ld_volatile(&p.ctl->best);
-    const int aborted = ld_volatile(&p.ctl->abort);
-    const int count = min(ld_volatile(&p.ctl->count), SV_CAP);
-    const unsigned long long c_first = blockIdx.x < SV_CAP ? __ldcg(p.cand + blockIdx.x) : 0ull;
-    const int rb0 = ld_volatile(res_best(p.result));
-    if (aborted || best <= SV_LMIN) {
-        // undecided: blocks too large for the windows / too many candidates (bit 1), or
-        // no block square of side 7 in these rows, i.e. nothing above 8 * 6 + 14 = 62
-        // here (bit 2: still decided if another rank holds a larger square)
-        if (blockIdx.x == 0 && tid == 0) atomicOr(res_status(p.result), aborted ? 2u : 4u);
-        return;
-    }
-    const int T0 = 8 * best;
-    for (int pass = 0; pass < 2; ++pass) {
-        const int Dp = best - pass;
-        for (int idx = blockIdx.x; idx < count; idx += gridDim.x) {
-            const unsigned long long c = idx == (int)blockIdx.x ? c_first : __ldcg(p.cand + idx);
-            const int D = (int)(c >> 40);
-            if (D != Dp) continue;
-            __syncthreads();  // the previous candidate's rows are done with
-            if (tid == 0) {
-                // ties at the best side so far (re-read once this CTA has found something itself)
-                tsh = max(T0, idx == (int)blockIdx.x && pass == 0 ? rb0 : ld_volatile(res_best(p.result)));
-                keysh = 0ull;
+    int next = blockIdx.x;
+    for (;;) {
+        __syncthreads();  // the previous candidate's rows are done with
+        if (tid == 0) {
+            // wait for entry `next`, or for the end of the coarse pass
+            unsigned long long c = 1ull;
+            long long spins = 0;
+            for (;;) {
+                const int done = ld_volatile(&p.ctl->done) >= p.coarse_warps;  // read before the count
+                const int count = min(ld_volatile(&p.ctl->count), SV_CAP);
+                if (ld_volatile(&p.ctl->abort) && done) {  // undecided: nothing left to verify
+                    c = 1ull;
+                    break;
+                }
+                if (next < count) {
+                    c = *(volatile unsigned long long*)(p.cand + next);
+                    if (c) break;  // (a reserved slot whose entry has not landed yet reads 0)
+                } else if (done) {
+                    c = 1ull;
+                    break;
+                }
+                __nanosleep(500);
+                if (++spins > (1ll << 24)) {  // never in practice
+                    atomicOr(&p.ctl->abort, 2);
+                    c = 1ull;
+                    break;
+                }
             }
-            for (int i = tid; i < 256; i += NT) lzs[i] = -1;
-            __syncthreads();
-            const int t0 = tsh;
-            if (8 * D + 14 < t0) continue;  // CTA-uniform
-            const int Rg = (int)((c >> 16) & 0xFFFFFFull), cg = (int)(c & 0xFFFFull);
-            const int r_hi = min(p.rows - 1, 8 * Rg + 14), r_lo = max(0, 8 * (Rg - D) - 6);
-            const int c_hi = min(p.cols - 1, 8 * cg + 14), c_lo = max(0, 8 * (cg - D) - 6);
-            const int nr = r_hi - r_lo + 1, wa = c_lo >> 5, nwd = (c_hi >> 5) - wa + 1;
-            const int first = t0 - 1;  // first row (window-relative) whose heights can reach t0
-            auto word_mask = [&](int k) -> uint32_t {
-                const int lo = max(c_lo - 32 * (wa + k), 0), hi = min(c_hi - 32 * (wa + k), 31);
-                return (k < nwd && hi >= lo) ? ((hi == 31 ? 0xFFFFFFFFu : (1u << (hi + 1)) - 1u) & ~((1u << lo) - 1u)) : 0u;
-            };
-            uint32_t wv[LPT];
+            csh = c;
+            bsh = ld_volatile(&p.ctl->best);
+            tsh = max(8 * bsh, ld_volatile(res_best(p.result)));  // ties at the best side so far
+            keysh = 0ull;
+        }
+        for (int i = tid; i < 256; i += NT) lzs[i] = -1;
+        __syncthreads();
+        const unsigned long long c = csh;
+        if (c == 1ull) break;
+        next += gridDim.x;
+        const int D = (int)(c >> 40), t0 = tsh;
+        // CTA-uniform.  (D beyond SV_DMAX: the solve is already marked undecided and the
+        // window would not fit.)
+        if (D < bsh - 1 || D > SV_DMAX || 8 * D + 14 < t0) continue;
+        const int Rg = (int)((c >> 16) & 0xFFFFFFull), cg = (int)(c & 0xFFFFull);
+        const int r_hi = min(p.rows - 1, 8 * Rg + 14), r_lo = max(0, 8 * (Rg - D) - 6);
+        const int c_hi = min(p.cols - 1, 8 * cg + 14), c_lo = max(0, 8 * (cg - D) - 6);
+        const int nr = r_hi - r_lo + 1, wa = c_lo >> 5, nwd = (c_hi >> 5) - wa + 1;
+        const int first = t0 - 1;  // first row (window-relative) whose heights can reach t0
+        auto word_mask = [&](int k) -> uint32_t {
+            const int lo = max(c_lo - 32 * (wa + k), 0), hi = min(c_hi - 32 * (wa + k), 31);
+            return (k < nwd && hi >= lo) ? ((hi == 31 ? 0xFFFFFFFFu : (1u << (hi + 1)) - 1u) & ~((1u << lo) - 1u)) : 0u;
+        };
+        uint32_t wv[LPT];
 #pragma unroll
-            for (int u = 0; u < LPT; ++u) {
-                const int i = tid + NT * u, rr = i >> 3, k = i & 7;
-                wv[u] = (rr < nr && k < nwd) ? __ldg((const uint32_t*)(sv_row(p, r_lo + rr)) + wa + k) : 0xFFFFFFFFu;
-            }
+        for (int u = 0; u < LPT; ++u) {
+            const int i = tid + NT * u, rr = i >> 3, k = i & 7;
+            wv[u] = (rr < nr && k < nwd) ? __ldg((const uint32_t*)(sv_row(p, r_lo + rr)) + wa + k) : 0xFFFFFFFFu;
+        }
 #pragma unroll
-            for (int u = 0; u < LPT; ++u) {
-                const int i = tid + NT * u, rr = i >> 3, k = i & 7;
-                if (rr < nr) {
-                    rowsm[rr][k] = wv[u];
-                    if (rr < first) {
-                        uint32_t z = ~wv[u] & word_mask(k);
-                        while (z) {
-                            const int j = __ffs(z) - 1;
-                            z &= z - 1;
-                            atomicMax(&lzs[32 * k + j], rr);
-                        }
+        for (int u = 0; u < LPT; ++u) {
+            const int i = tid + NT * u, rr = i >> 3, k = i & 7;
+            if (rr < nr) {
+                rowsm[rr][k] = wv[u];
+                if (rr < first) {
+                    uint32_t z = ~wv[u] & word_mask(k);
+                    while (z) {
+                        const int j = __ffs(z) - 1;
+                        z &= z - 1;
+                        atomicMax(&lzs[32 * k + j], rr);
                     }
                 }
             }
-            __syncthreads();
-            uint32_t msk[8];
-            int lz[8];  // last zero row (window-relative) of column 32k + lane
+        }
+        __syncthreads();
+        uint32_t msk[8];
+        int lz[8];  // last zero row (window-relative) of column 32k + lane
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            msk[k] = word_mask(k);
+            lz[k] = lzs[32 * k + lane];
+        }
+        // leftmost window end of t columns of height >= t at row rr, or -1
+        auto window = [&](int rr, int t) -> int {
+            int run = 0, e = -1;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                msk[k] = word_mask(k);
-                lz[k] = lzs[32 * k + lane];
+                const uint32_t x = __ballot_sync(0xFFFFFFFFu, rr - lz[k] >= t) & msk[k];
+                const int pre = x == 0xFFFFFFFFu ? 32 : __ffs(~x) - 1;
+                if (e < 0 && run + pre >= t) e = 32 * k + (t - run) - 1;
+                run = x == 0xFFFFFFFFu ? run + 32 : __clz(~x);
             }
-            // leftmost window end of t columns of height >= t at row rr, or -1
-            auto window = [&](int rr, int t) -> int {
-                int run = 0, e = -1;
+            return e;
+        };
+        for (int rr = max(first, 0); rr < nr; ++rr) {
+            const uint4 a = *(const uint4*)&rowsm[rr][0];
+            const uint4 b = *(const uint4*)&rowsm[rr][4];
+            const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const uint32_t x = __ballot_sync(0xFFFFFFFFu, rr - lz[k] >= t) & msk[k];
-                    const int pre = x == 0xFFFFFFFFu ? 32 : __ffs(~x) - 1;
-                    if (e < 0 && run + pre >= t) e = 32 * k + (t - run) - 1;
-                    run = x == 0xFFFFFFFFu ? run + 32 : __clz(~x);
-                }
-                return e;
-            };
-            for (int rr = max(first, 0); rr < nr; ++rr) {
-                const uint4 a = *(const uint4*)&rowsm[rr][0];
-                const uint4 b = *(const uint4*)&rowsm[rr][4];
-                const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    if ((w[k] & msk[k]) != msk[k] && !((w[k] >> lane) & 1u)) lz[k] = rr;
-                if (((rr - first) & (SV_VWARPS - 1)) != warp) continue;  // another warp's row
-                int t = *(volatile int*)&tsh;
-                if (rr + 1 < t || t > nr) continue;
-                int e = window(rr, t);
-                if (e < 0) continue;
-                for (;;) {  // the row's own largest square
-                    const int e2 = rr + 1 > t ? window(rr, t + 1) : -1;
-                    if (e2 < 0) break;
-                    e = e2;
-                    ++t;
-                }
-                if (lane == 0) {
-                    atomicMax(&tsh, t);
-                    atomicMax(&keysh, pack_key(t, p.row_base + r_lo + rr, (long long)32 * wa + e));
-                }
+            for (int k = 0; k < 8; ++k)
+                if ((w[k] & msk[k]) != msk[k] && !((w[k] >> lane) & 1u)) lz[k] = rr;
+            if (((rr - first) & (SV_VWARPS - 1)) != warp) continue;  // another warp's row
+            int t = *(volatile int*)&tsh;
+            if (rr + 1 < t || t > nr) continue;
+            int e = window(rr, t);
+            if (e < 0) continue;
+            for (;;) {  // the row's own largest square
+                const int e2 = rr + 1 > t ? window(rr, t + 1) : -1;
+                if (e2 < 0) break;
+                e = e2;
+                ++t;
             }
-            __syncthreads();
-            if (tid == 0 && keysh) {
-                atomicMax(res_key1(p.result), keysh);
-                atomicMax(res_best(p.result), (int)(keysh >> (2 * KEY_DIM_BITS)));
+            if (lane == 0) {
+                atomicMax(&tsh, t);
+                atomicMax(&keysh, pack_key(t, p.row_base + r_lo + rr, (long long)32 * wa + e));
             }
         }
+        __syncthreads();
+        if (tid == 0 && keysh) {
+            atomicMax(res_key1(p.result), keysh);
+            atomicMax(res_best(p.result), (int)(keysh >> (2 * KEY_DIM_BITS)));
+        }
+    }
+    // the coarse pass is complete here: can the sieve answer at all?
+    if (blockIdx.x == 0 && tid == 0) {
+        const int aborted = ld_volatile(&p.ctl->abort), best = ld_volatile(&p.ctl->best);
+        // undecided: blocks too large for the windows / too many candidates (bit 1), or
+        // no block square of side 7 in these rows, i.e. nothing above 8 * 6 + 14 = 62
+        // here (bit 2: still decided if another rank holds a larger square)
+        if (aborted || best <= SV_LMIN) atomicOr(res_status(p.result), aborted ? 2u : 4u);
     }
 }
 
