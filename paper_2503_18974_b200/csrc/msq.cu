@@ -633,6 +633,8 @@ msq::SieveParams make_sieve(const msq_plan* pl, const void* d_src, const void* d
     p.ctl = (msq::SieveCtl*)(w + g.ctl);
     p.cand = (unsigned long long*)(w + g.cand);
     p.G = (uint32_t*)(w + g.G);
+    // a sweep should give every CTA a few tiles: short slices (one rank of many) take fewer
+    p.nphases = (int)std::max<long long>(1, std::min<long long>(msq::SV_PHASES, g.CR / (8ll * g.nbands)));
     p.pcnt = (int*)(w + g.ctl + sizeof(msq::SieveCtl));
     p.ptarget = g.nbands * (int)ceil_div(round_up(pl->words, 4), 256);
     p.result = (unsigned char*)res;

@@ -59,7 +59,7 @@ namespace msq {
 constexpr int SV_PL = 5;           // height planes: block heights saturate at 31
 constexpr int SV_EDGE = 31;        // block rows above a unit that warm its heights up (they saturate at 31)
 constexpr int SV_OWN = 16;         // block rows a coarse unit owns
-constexpr int SV_PHASES = 4;       // the streaming pass covers the matrix in this many sweeps (top quarter first, ...)
+constexpr int SV_PHASES = 4;       // the streaming pass covers the matrix in up to this many sweeps (top quarter first, ...)
 constexpr int SV_DMAX = 26;        // windows of 8 * 26 + 21 = 229 columns (from column 2 mod 8) fit 8 words
 constexpr int SV_LMIN = 6;         // lowest level tested; the sieve decides for max D >= 7
 constexpr int SV_CAP = 32768;      // candidate list entries
@@ -90,6 +90,7 @@ struct SieveParams {
     int nunits;           // coarse pass: ceil(CR / SV_OWN) row units x WC warps
     uint32_t* G;          // [CR][CWn] block bitmap
     int coarse_warps;     // warps of sieve_coarse_kernel's grid: ctl->done ends there
+    int nphases;          // sweeps of the streaming pass over the matrix (<= SV_PHASES; 1 for short slices)
     int* pcnt;            // [SV_PHASES] streaming warps done with each phase (zeroed with ctl)
     int ptarget;          // = CTAs' consumer warps in total: a phase is complete at this count
     unsigned long long* cand;  // [SV_CAP] D << 40 | block row << 16 | block column
@@ -101,15 +102,15 @@ __device__ __forceinline__ const uint8_t* sv_row(const SieveParams& p, int r) {
     return r < p.halo_rows ? p.halo + (size_t)r * p.halo_ld_bytes
                            : p.src + (size_t)(r - p.halo_rows) * p.ld_bytes;
 }
-// Sub-band j of SV_PHASES * nbands covers block rows [sv_band_cr0(j), sv_band_cr0(j + 1));
+// Sub-band j of nphases * nbands covers block rows [sv_band_cr0(j), sv_band_cr0(j + 1));
 // CTA (band b) streams sub-bands b, nbands + b, 2 * nbands + b, ...: phase ph of the
 // pass is the ph-th quarter of the matrix, each CTA reading one contiguous piece of it.
 __device__ __forceinline__ int sv_band_cr0(const SieveParams& p, int j) {
-    return (int)(((long long)p.CR * j) / (SV_PHASES * p.nbands));
+    return (int)(((long long)p.CR * j) / (p.nphases * p.nbands));
 }
 // the phase that produces block row R
 __device__ __forceinline__ int sv_phase_of(const SieveParams& p, int R) {
-    const long long nb = (long long)SV_PHASES * p.nbands;
+    const long long nb = (long long)p.nphases * p.nbands;
     return (int)((((long long)R + 1) * nb - 1) / p.CR) / p.nbands;
 }
 
@@ -288,12 +289,11 @@ __global__ void __launch_bounds__(288, 1) sieve_pass_kernel(const SieveParams p)
     // bitmap of a quarter is complete while the next one streams and the coarse pass
     // (launched beside this kernel) works on it.  (Interleaving single tiles instead
     // cost 30% of the bandwidth: 89 -> 116 us on cfg4.)
-    int tiles_of[SV_PHASES], first_of[SV_PHASES], ntiles = 0;
+    int tiles_of[SV_PHASES], first_of[SV_PHASES];
 #pragma unroll
     for (int ph = 0; ph < SV_PHASES; ++ph) {
-        first_of[ph] = sv_band_cr0(p, ph * p.nbands + band);
-        tiles_of[ph] = sv_band_cr0(p, ph * p.nbands + band + 1) - first_of[ph];
-        ntiles += tiles_of[ph];
+        first_of[ph] = ph < p.nphases ? sv_band_cr0(p, ph * p.nbands + band) : 0;
+        tiles_of[ph] = ph < p.nphases ? sv_band_cr0(p, ph * p.nbands + band + 1) - first_of[ph] : 0;
     }
     const int mw0 = 256 * wc0;  // matrix words [mw0, mw1) of each row
     const int mw1 = min(Wp, 256 * wc1);
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(288, 1) sieve_pass_kernel(const SieveParams p)
             const uint64_t pol = l2_evict_first_policy();
             int s = 0, lap = 0;
 #pragma unroll 1
-            for (int ph = 0; ph < SV_PHASES; ++ph) {
+            for (int ph = 0; ph < p.nphases; ++ph) {
                 for (int q = 0; q < tiles_of[ph]; ++q) {
                     if (lap > 0) mbar_wait(&empty[s], (uint32_t)((lap - 1) & 1));
                     mbar_expect_tx(&full[s], SV_TR * chunk_bytes);
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(288, 1) sieve_pass_kernel(const SieveParams p)
     int s = 0;
     uint32_t par = 0u;
 #pragma unroll 1
-    for (int ph = 0; ph < SV_PHASES; ++ph) {
+    for (int ph = 0; ph < p.nphases; ++ph) {
         uint32_t* grow = p.G + (size_t)first_of[ph] * p.CWn + (in ? g : 0);
         for (int q = 0; q < tiles_of[ph]; ++q) {
             mbar_wait(&full[s], par);
@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(32 * SV_EWARPS) sieve_coarse_kernel(const Siev
             long long spins = 0;
             for (int ph = 0; ph <= ph1 && ok; ++ph)
                 while (c[ph] < p.ptarget) {
-                    __nanosleep(1000);
+                    __nanosleep(400);
                     if (++spins > (1ll << 23)) {  // never in practice: hand the input to the band engine
                         atomicOr(&p.ctl->abort, 2);
                         ok = 0;
