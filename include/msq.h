@@ -287,6 +287,9 @@ void msq_debug_set_profile(void* d_counters);
 void msq_debug_set_staging(int32_t workers, int32_t buffers, int64_t chunk_bytes);
 /* Instrumentation: consumer warps per CTA of the sieve engine's streaming pass (plans made after the call). */
 void msq_debug_set_sieve_wpc(int32_t warps);
+/* Tests: sweeps of the sieve engine's streaming pass (1..4; 0 = by the height: the coarse pass
+ * and the verifier run beside the streaming pass from the second sweep on). */
+void msq_debug_set_sieve_phases(int32_t phases);
 /* Instrumentation: band height of the team engine's row-band mode (plans made after the call). */
 void msq_debug_set_team_band_rows(int32_t rows);
 

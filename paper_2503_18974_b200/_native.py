@@ -102,6 +102,7 @@ def load():
         "msq_rank_sieve_pass": ([PP, P, P, I64, I64, P, P, P], ctypes.c_int),
         "msq_rank_sieve_finish": ([PP, P, P, I64, I64, P, P, P], ctypes.c_int),
         "msq_debug_set_sieve_wpc": ([I32], None),
+        "msq_debug_set_sieve_phases": ([I32], None),
         "msq_ws_views": ([PP, P, P, P, P, P], ctypes.c_int),
         "msq_gen_hash": ([I32, U64, U64, I64, I64, I64, I64, P, P], ctypes.c_int),
         "msq_last_launch_count": ([], I32),

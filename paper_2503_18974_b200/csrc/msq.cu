@@ -562,6 +562,7 @@ struct SieveGeom {
     size_t ctl, cand, G, total;  // workspace offsets (after the band engine's layout)
 };
 int g_sieve_wpc = 8;  // most consumer warps per CTA of the streaming pass (instrumentation)
+int g_sieve_phases = 0;  // > 0: sweeps of the streaming pass whatever the height (tests)
 
 bool sieve_shape_ok(int32_t fmt, int32_t batch, int64_t rows, int64_t cols, int64_t ld) {
     const int64_t words = ceil_div(cols, 32);
@@ -634,7 +635,8 @@ msq::SieveParams make_sieve(const msq_plan* pl, const void* d_src, const void* d
     p.cand = (unsigned long long*)(w + g.cand);
     p.G = (uint32_t*)(w + g.G);
     // a sweep should give every CTA a few tiles: short slices (one rank of many) take fewer
-    p.nphases = (int)std::max<long long>(1, std::min<long long>(msq::SV_PHASES, g.CR / (8ll * g.nbands)));
+    p.nphases = g_sieve_phases > 0 ? std::min(g_sieve_phases, msq::SV_PHASES)
+                                   : (int)std::max<long long>(1, std::min<long long>(msq::SV_PHASES, g.CR / (8ll * g.nbands)));
     p.pcnt = (int*)(w + g.ctl + sizeof(msq::SieveCtl));
     p.ptarget = g.nbands * (int)ceil_div(round_up(pl->words, 4), 256);
     p.result = (unsigned char*)res;
@@ -1742,5 +1744,6 @@ extern "C" void msq_debug_set_staging(int32_t workers, int32_t buffers, int64_t 
     g_stage.chunk = chunk_bytes > 0 ? (size_t)chunk_bytes : (4u << 20);
 }
 
+extern "C" void msq_debug_set_sieve_phases(int32_t phases) { g_sieve_phases = phases > 0 ? phases : 0; }
 extern "C" void msq_debug_set_sieve_wpc(int32_t warps) { g_sieve_wpc = warps >= 1 && warps <= 8 ? warps : 8; }
 extern "C" void msq_debug_set_team_band_rows(int32_t rows) { g_team_band_rows = rows > 0 ? rows : 16; }

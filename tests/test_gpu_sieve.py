@@ -235,3 +235,45 @@ def test_workspace_is_not_overrun(torch):
         want = oracle.freq(a)
         got = decode_key(int(ks[0]), 0, rows + SIEVE_HALO, cols)
         assert int(ks[1]) == 0 and (got.side, got.top, got.left) == (want.side, want.top, want.left)
+
+
+@pytest.mark.parametrize("phases", [2, 3, 4])
+def test_streaming_in_sweeps_with_the_coarse_pass_beside_it(torch, phases):
+    """From the second sweep on the coarse pass and the verifier run while the
+    streaming pass still writes the bitmap (phase counters, done counter).  Forced
+    sweeps on small shapes (also fewer block rows than sweeps x bands), squares
+    across the sweeps' borders, CTA shapes of 1..8 streaming warps, repeated solves
+    on one plan."""
+    lib = N.load()
+    rng = np.random.default_rng(40 + phases)
+    try:
+        lib.msq_debug_set_sieve_phases(phases)
+        for it in range(10):
+            rows = int(rng.choice([200, 1000, 3000, 6000]))
+            cols = int(rng.choice([256, 2048, 8192]))
+            lib.msq_debug_set_sieve_wpc(int(rng.choice([1, 3, 8])))
+            a = (rng.random((rows, cols)) < 0.9994).astype(np.uint8)
+            for q in range(1, phases):  # squares over the borders between sweeps
+                k = int(rng.integers(60, min(rows, cols, 210)))
+                top = max(0, min(rows - k, rows * q // phases - k // 2))
+                left = int(rng.integers(0, cols - k + 1))
+                a[top:top + k, left:left + k] = 1
+            want = oracle.freq(a)
+            for _ in range(3):
+                got, _ = _solve(torch, a)
+                _same(got, want)
+    finally:
+        lib.msq_debug_set_sieve_phases(0)
+        lib.msq_debug_set_sieve_wpc(8)
+
+
+@pytest.mark.slow
+def test_tall_matrix_takes_four_sweeps_on_its_own(torch):
+    rng = np.random.default_rng(50)
+    rows, cols = 40960, 2048  # 5120 block rows: four sweeps by the plan's own rule
+    a = (rng.random((rows, cols)) < 0.9993).astype(np.uint8)
+    for top in (10200, 20400, 30700):
+        a[top:top + 150, 700:850] = 1
+    got, retried = _solve(torch, a, engine=-1)
+    _same(got, oracle.freq(a))
+    assert retried == 0
