@@ -38,10 +38,12 @@
 //                       owns 32 block rows and warms its heights up on the 31
 //                       rows above.  Hits (rare) get their exact D and go to a
 //                       candidate list.
-//   sieve_verify_kernel runs Algorithm 1 exactly (per-column heights, one test
-//                       per row, leftmost window) on the <= 229 x 229 cell
-//                       window of every candidate with D >= max D - 1 and keeps
-//                       the best (side, first bottom row, leftmost column) key.
+//   sieve_verify_kernel (runs beside the coarse pass, taking candidates as they
+//                       appear) runs Algorithm 1 exactly (per-column heights,
+//                       one test per row, leftmost window) on the <= 229 x 229
+//                       cell window of every candidate with D >= max D - 1 and
+//                       keeps the best (side, first bottom row, leftmost column)
+//                       key.
 //
 // The answer is exact whenever the sieve decides: max D in [7, 26] (answers
 // 56..222) and the candidate list did not overflow.  Otherwise status bit 1
