@@ -313,7 +313,10 @@ __global__ void __launch_bounds__(288, 1) sieve_pass_kernel(const SieveParams p)
         }
         fence_mbar_init();
     }
-    if (blockIdx.x == 0 && tid < 8) ((uint32_t*)p.result)[tid] = 0u;  // written again by the verifier only
+    if (blockIdx.x == 0 && tid < 8) {  // written again by the verifier only (tens of microseconds later)
+        ((uint32_t*)p.result)[tid] = 0u;
+        __threadfence();
+    }
     __syncthreads();
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the coarse pass waits on the phase counters
     if (ncw <= 0) return;
@@ -536,6 +539,7 @@ __global__ void __launch_bounds__(32 * SV_VWARPS) sieve_verify_kernel(const Siev
             long long spins = 0;
             for (;;) {
                 const int done = ld_volatile(&p.ctl->done) >= p.coarse_warps;  // read before the count
+                __threadfence();
                 const int count = min(ld_volatile(&p.ctl->count), SV_CAP);
                 if (ld_volatile(&p.ctl->abort) && done) {  // undecided: nothing left to verify
                     c = 1ull;

@@ -277,3 +277,26 @@ def test_tall_matrix_takes_four_sweeps_on_its_own(torch):
     got, retried = _solve(torch, a, engine=-1)
     _same(got, oracle.freq(a))
     assert retried == 0
+
+
+def test_repeated_solves_give_one_answer(torch):
+    """The coarse pass and the verifier race the streaming pass by design
+    (candidates appear in any order, levels rise at different moments): the
+    answer must not depend on it.  200 solves of one input, four sweeps."""
+    from paper_2503_18974_b200.squares import Solver
+    lib = N.load()
+    rng = np.random.default_rng(60)
+    rows, cols = 6000, 8192
+    a = (rng.random((rows, cols)) < 0.9992).astype(np.uint8)
+    for top, left in [(1400, 300), (1499, 4000), (2950, 7000), (4490, 5000), (4500, 100)]:
+        a[top:top + 120, left:left + 120] = 1  # ties across the sweeps' borders
+    want = oracle.freq(a)
+    w = torch.from_numpy(grid.pack_bits(a).view(np.int32)).cuda()
+    try:
+        lib.msq_debug_set_sieve_phases(4)
+        s = Solver(N.FMT_BITS, rows, cols, engine=2)
+        for _ in range(200):
+            _same(s.solve(w)[0], want)
+        assert getattr(s, "sieve_retries", 0) == 0
+    finally:
+        lib.msq_debug_set_sieve_phases(0)
