@@ -637,6 +637,13 @@ msq::SieveParams make_sieve(const msq_plan* pl, const void* d_src, const void* d
     // a sweep should give every CTA a few tiles: short slices (one rank of many) take fewer
     p.nphases = g_sieve_phases > 0 ? std::min(g_sieve_phases, msq::SV_PHASES)
                                    : (int)std::max<long long>(1, std::min<long long>(msq::SV_PHASES, g.CR / (8ll * g.nbands)));
+    // equal sweeps.  (A short last sweep -- 3:3:3:1 or 4:3:2:1 of the rows, to leave less
+    // of the coarse pass behind the streaming pass -- measured slower on cfg4: 0.114 and
+    // 0.107 ms against 0.1045: the short pieces cost the streaming pass more than the
+    // coarse pass gains.)
+    for (int k = 0; k <= msq::SV_PHASES; ++k)
+        p.prow[k] = (int)((long long)g.CR * std::min(k, p.nphases) / p.nphases);
+    p.prow[p.nphases] = g.CR;
     p.pcnt = (int*)(w + g.ctl + sizeof(msq::SieveCtl));
     p.ptarget = g.nbands * (int)ceil_div(round_up(pl->words, 4), 256);
     p.result = (unsigned char*)res;

@@ -93,6 +93,7 @@ struct SieveParams {
     uint32_t* G;          // [CR][CWn] block bitmap
     int coarse_warps;     // warps of sieve_coarse_kernel's grid: ctl->done ends there
     int nphases;          // sweeps of the streaming pass over the matrix (<= SV_PHASES; 1 for short slices)
+    int prow[SV_PHASES + 1];  // their block-row borders: 0 = prow[0] < ... < prow[nphases] = CR
     int* pcnt;            // [SV_PHASES] streaming warps done with each phase (zeroed with ctl)
     int ptarget;          // = CTAs' consumer warps in total: a phase is complete at this count
     unsigned long long* cand;  // [SV_CAP] D << 40 | block row << 16 | block column
@@ -104,16 +105,17 @@ __device__ __forceinline__ const uint8_t* sv_row(const SieveParams& p, int r) {
     return r < p.halo_rows ? p.halo + (size_t)r * p.halo_ld_bytes
                            : p.src + (size_t)(r - p.halo_rows) * p.ld_bytes;
 }
-// Sub-band j of nphases * nbands covers block rows [sv_band_cr0(j), sv_band_cr0(j + 1));
-// CTA (band b) streams sub-bands b, nbands + b, 2 * nbands + b, ...: phase ph of the
-// pass is the ph-th quarter of the matrix, each CTA reading one contiguous piece of it.
-__device__ __forceinline__ int sv_band_cr0(const SieveParams& p, int j) {
-    return (int)(((long long)p.CR * j) / (p.nphases * p.nbands));
+// Phase ph of the streaming pass covers block rows [prow[ph], prow[ph + 1]) (the last
+// phase is the short one: what the coarse pass still has to do when the streaming
+// pass ends); CTA (band b) streams one contiguous piece of every phase.
+__device__ __forceinline__ int sv_band_cr0(const SieveParams& p, int ph, int band) {
+    return p.prow[ph] + (int)(((long long)(p.prow[ph + 1] - p.prow[ph]) * band) / p.nbands);
 }
 // the phase that produces block row R
 __device__ __forceinline__ int sv_phase_of(const SieveParams& p, int R) {
-    const long long nb = (long long)p.nphases * p.nbands;
-    return (int)((((long long)R + 1) * nb - 1) / p.CR) / p.nbands;
+    int ph = 0;
+    while (ph + 1 < p.nphases && R >= p.prow[ph + 1]) ++ph;
+    return ph;
 }
 
 // bit c of the result: bits [c - m + 1, c] of the 64-bit (hi:lo) are all set (1 <= m <= 31)
@@ -294,8 +296,8 @@ __global__ void __launch_bounds__(288, 1) sieve_pass_kernel(const SieveParams p)
     int tiles_of[SV_PHASES], first_of[SV_PHASES];
 #pragma unroll
     for (int ph = 0; ph < SV_PHASES; ++ph) {
-        first_of[ph] = ph < p.nphases ? sv_band_cr0(p, ph * p.nbands + band) : 0;
-        tiles_of[ph] = ph < p.nphases ? sv_band_cr0(p, ph * p.nbands + band + 1) - first_of[ph] : 0;
+        first_of[ph] = ph < p.nphases ? sv_band_cr0(p, ph, band) : 0;
+        tiles_of[ph] = ph < p.nphases ? sv_band_cr0(p, ph, band + 1) - first_of[ph] : 0;
     }
     const int mw0 = 256 * wc0;  // matrix words [mw0, mw1) of each row
     const int mw1 = min(Wp, 256 * wc1);
