@@ -360,8 +360,12 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    # defaults: 200 timed solves (~20 ms of device time on cfg4: the clocks are sampled
+    # every millisecond, and a 2 ms region right after the synchronize still shows the
+    # clock ramp: 0.108 ms per solve at 20 steps, 0.104 at 100 and 400); the CPU arm's
+    # steps are whole-matrix solves of ~1 s each, so it defaults to 20
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=None)
     ap.add_argument("--config", default="cfg4",
                     choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "cfg4_p99", "cfg4_planted"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -369,6 +373,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 20 if args.impl == "reference" else 200
+    if args.warmup is None:
+        args.warmup = 5 if args.impl == "reference" else 10
     rank, world, local = env_dist()
     if args.impl == "reference":
         return run_reference(args, rank, world)
