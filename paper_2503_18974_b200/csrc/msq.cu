@@ -514,15 +514,20 @@ cudaError_t launch_carry(const msq_plan* pl, void* ws, const uint32_t* base, cud
     // programmatic dependent launch: the CTAs launch while the band pass drains
     // and wait (griddepcontrol.wait) for its writes
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)ceil_div(pl->words * 32, 256));
-    cfg.blockDim = dim3(32, msq::CARRY_SEG);
+    const int lanes = pl->words * 32 <= 32768 ? 16 : 32;  // columns per CTA = 8 * lanes
+    cfg.gridDim = dim3((unsigned)ceil_div(pl->words * 32, 8 * lanes));
+    cfg.blockDim = dim3(lanes, msq::CARRY_SEG);
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, msq::carry_scan_kernel, (int)pl->rows, (int)pl->cols, pl->words, pl->nbands,
+    if (lanes == 16)
+        return cudaLaunchKernelEx(&cfg, msq::carry_scan_kernel<16>, (int)pl->rows, (int)pl->cols, pl->words,
+                                  pl->nbands, pl->words * 32, (const uint16_t*)(w + L.zb),
+                                  (const uint32_t*)(w + L.ao), base, (uint16_t*)(w + L.carry));
+    return cudaLaunchKernelEx(&cfg, msq::carry_scan_kernel<32>, (int)pl->rows, (int)pl->cols, pl->words, pl->nbands,
                               pl->words * 32, (const uint16_t*)(w + L.zb), (const uint32_t*)(w + L.ao), base,
                               (uint16_t*)(w + L.carry));
 }

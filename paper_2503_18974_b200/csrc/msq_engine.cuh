@@ -2014,19 +2014,23 @@ __global__ void __launch_bounds__(512, 1) fixup_kernel(const FixParams p) {
 // the map c -> (all ones ? c + h_q : b_q); a segment composes its maps
 // (pass 1), then folds the maps of the segments above from base and writes
 // its carries (pass 2) -- 2 reads of the summaries, CARRY_SEG-way parallel.
-constexpr int CARRY_SEG = 8;
-__global__ void __launch_bounds__(32 * CARRY_SEG) carry_scan_kernel(int rows, int cols, int W, int nbands,
-                                                                    int cols_pad, const uint16_t* b_in,
-                                                                    const uint32_t* ao_in, const uint32_t* base,
-                                                                    uint16_t* carry_out) {
-    __shared__ uint32_t fval[CARRY_SEG][32][8];
-    __shared__ uint8_t fconst[CARRY_SEG][32];
+// LANES x 8 columns per CTA: 16 lanes for matrices up to 32768 columns (twice the
+// CTAs: cfg3's 16384 columns gave 64 CTAs of 256 columns on 148 SMs), and 16
+// segments (half the bands per thread of round 1's 8): cfg3 16.3 -> see DESIGN.
+constexpr int CARRY_SEG = 16;
+template <int LANES>
+__global__ void __launch_bounds__(LANES * CARRY_SEG) carry_scan_kernel(int rows, int cols, int W, int nbands,
+                                                                       int cols_pad, const uint16_t* b_in,
+                                                                       const uint32_t* ao_in, const uint32_t* base,
+                                                                       uint16_t* carry_out) {
+    __shared__ uint32_t fval[CARRY_SEG][LANES][8];
+    __shared__ uint8_t fconst[CARRY_SEG][LANES];
     // launched as a programmatic dependent of the band pass: wait for its writes,
     // then let the fix-up's CTAs launch (they wait for this grid in turn)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int lane = threadIdx.x, sg = threadIdx.y;
-    const int j0 = (blockIdx.x * 32 + lane) * 8;  // 8 columns; cols_pad is a multiple of 32
+    const int j0 = (blockIdx.x * LANES + lane) * 8;  // 8 columns; cols_pad is a multiple of 32
     const int nq = nbands - 1;                     // transitions: carry of band q+1 from band q
     const int L = (nq + CARRY_SEG - 1) / CARRY_SEG;
     const int q0 = min(nq, sg * L), q1 = min(nq, q0 + L);
