@@ -34,8 +34,8 @@
 //                       saturating bit-planes per lane (one 32-block word per
 //                       lane, lane 0 of a warp is the left halo), one level
 //                       test per block row -- "a run of >= l blocks of height
-//                       >= l", l = best D - 1 -- four rows per vote.  A unit
-//                       owns 32 block rows and warms its heights up on the 31
+//                       >= l", l = best D - 1 -- two rows per vote.  A unit
+//                       owns 16 block rows and warms its heights up on the 31
 //                       rows above.  Hits (rare) get their exact D and go to a
 //                       candidate list.
 //   sieve_verify_kernel (runs beside the coarse pass, taking candidates as they
@@ -70,7 +70,7 @@ constexpr int SV_MAXSLOTS = 16;    // TMA ring depth
 constexpr int SV_HALO_ROWS = 256;  // rows a rank borrows from the rank above
 constexpr int SV_VROWS = 8 * SV_DMAX + 21;
 constexpr int SV_VWARPS = 8;       // verifier warps per CTA (one candidate per CTA; a power of two)
-constexpr int SV_EWARPS = 4;       // edge-kernel warps per CTA
+constexpr int SV_EWARPS = 4;       // coarse-kernel warps per CTA (one unit each)
 
 struct SieveCtl {
     int best;   // largest D found so far
@@ -105,9 +105,8 @@ __device__ __forceinline__ const uint8_t* sv_row(const SieveParams& p, int r) {
     return r < p.halo_rows ? p.halo + (size_t)r * p.halo_ld_bytes
                            : p.src + (size_t)(r - p.halo_rows) * p.ld_bytes;
 }
-// Phase ph of the streaming pass covers block rows [prow[ph], prow[ph + 1]) (the last
-// phase is the short one: what the coarse pass still has to do when the streaming
-// pass ends); CTA (band b) streams one contiguous piece of every phase.
+// Phase (sweep) ph of the streaming pass covers block rows [prow[ph], prow[ph + 1]); CTA
+// (band b) streams one contiguous piece of every phase.
 __device__ __forceinline__ int sv_band_cr0(const SieveParams& p, int ph, int band) {
     return p.prow[ph] + (int)(((long long)(p.prow[ph + 1] - p.prow[ph]) * band) / p.nbands);
 }
@@ -289,7 +288,7 @@ __global__ void __launch_bounds__(288, 1) sieve_pass_kernel(const SieveParams p)
     const int WF = (Wp + 255) / 256;   // warp columns of 256 matrix words
     const int wc0 = WF * chunk / p.nchunks, wc1 = WF * (chunk + 1) / p.nchunks;
     const int ncw = wc1 - wc0;  // consumer warps of this chunk
-    // SV_PHASES contiguous sub-bands per CTA, one per quarter of the matrix, so the
+    // nphases contiguous sub-bands per CTA, one per sweep (quarter) of the matrix, so the
     // bitmap of a quarter is complete while the next one streams and the coarse pass
     // (launched beside this kernel) works on it.  (Interleaving single tiles instead
     // cost 30% of the bandwidth: 89 -> 116 us on cfg4.)
