@@ -640,8 +640,10 @@ msq::SieveParams make_sieve(const msq_plan* pl, const void* d_src, const void* d
     p.cand = (unsigned long long*)(w + g.cand);
     p.G = (uint32_t*)(w + g.G);
     // a sweep should give every CTA a few tiles: short slices (one rank of many) take fewer
+    // (measured on slices of cfg4, tools/time_slice_phases.py: 8192 rows 0.042 ms with 2
+    // sweeps against 0.045 with 1; 16384 rows 0.049 with 4 against 0.053 with 1)
     p.nphases = g_sieve_phases > 0 ? std::min(g_sieve_phases, msq::SV_PHASES)
-                                   : (int)std::max<long long>(1, std::min<long long>(msq::SV_PHASES, g.CR / (8ll * g.nbands)));
+                                   : (int)std::max<long long>(1, std::min<long long>(msq::SV_PHASES, g.CR / (3ll * g.nbands)));
     // equal sweeps.  (A short last sweep -- 3:3:3:1 or 4:3:2:1 of the rows, to leave less
     // of the coarse pass behind the streaming pass -- measured slower on cfg4: 0.114 and
     // 0.107 ms against 0.1045: the short pieces cost the streaming pass more than the
