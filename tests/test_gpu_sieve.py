@@ -226,7 +226,10 @@ def test_workspace_is_not_overrun(torch):
         be.ws = buf[guard:guard + need]
         resbuf = torch.full((256 + 32 + 256,), 0x5A, dtype=torch.uint8, device="cuda")
         be.res = resbuf[256:288]
-        be.sieve(full[SIEVE_HALO:], full[:SIEVE_HALO])
+        # the halo comes with its own row stride (msq_rank_sieve's halo_ld)
+        halo = torch.full((SIEVE_HALO, full.shape[1] + 8), -1, dtype=full.dtype, device="cuda")
+        halo[:, :full.shape[1]] = full[:SIEVE_HALO]
+        be.sieve(full[SIEVE_HALO:], halo[:, :full.shape[1]])
         torch.cuda.synchronize()
         assert bool((buf[:guard] == 0x5A).all()) and bool((buf[guard + need:] == 0x5A).all())
         assert bool((resbuf[:256] == 0x5A).all()) and bool((resbuf[288:] == 0x5A).all())
